@@ -1,0 +1,25 @@
+"""CPU oracle for SAND's adaptive T-MLP query path.  TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import, call or execute anything under ``oracle/``.  The product path
+(``paper_2604_25936_b200``) never imports it and has no CPU fallback.
+
+The oracle is a plain, slow, obviously-correct restatement of the paper (PAPER.md = arxiv
+2604.25936), in float64 for the network (the paper fixes no precision) and in float32 only where the
+kernel's float32 arithmetic decides an integer (the depth-map cell index, reading R1).
+
+Pins (tests/test_oracle_*.py, all ``-m "not gpu"``): plain-SIREN special case vs torch float64
+library layers; hand-computed L=2/H=1 golden values (tests/golden/); zero-parameter net; prefix
+consistency; NaN poisoning of unused layers; Appendix-A quadratic form; init bounds/moments;
+octree descent vs brute-force leaf scan; grid-point cells vs the integer closed form.
+Parity unpinned: nothing in this module.
+"""
+from .sand_oracle import (
+    cell_coords, lookup_voxel, lookup_octree, lookup_bruteforce, lookup,
+    tmlp_forward, tmlp_trace, query, query_full, NONFINITE_DEPTH,
+)
+
+__all__ = [
+    "cell_coords", "lookup_voxel", "lookup_octree", "lookup_bruteforce", "lookup",
+    "tmlp_forward", "tmlp_trace", "query", "query_full", "NONFINITE_DEPTH",
+]

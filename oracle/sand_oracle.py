@@ -1,0 +1,201 @@
+"""SAND oracle (TEST INFRASTRUCTURE ONLY -- see oracle/__init__.py).
+
+Every function cites the PAPER.md passage it restates.  No blocking, fusion or reordering beyond
+the definitions: the network is evaluated layer by layer exactly as Eq. 2 / Eq. 3 are written, with
+numpy float64 matrix-vector products as the only library primitive.
+
+Parameters are passed duck-typed (any object with the attributes below), so this module imports
+nothing from the product package or from the input generators:
+    W[i-1] : [H][fan_in] float32   (fan_in = 3 for i = 1, else H)      -- W_i of Eq. 2
+    b[i-1] : [H] float32                                               -- b_i of Eq. 2
+    a[i-1] : [H] float32, c[i-1] : float  -- LINEAR tail W_i^out, b_i^out (Eq. 2); for MULT, the
+                                              t_{i0} factor W_{i0}^out, b_{i0}^out (Eq. 3, i >= 2)
+    a1[i-2], c1[i-2]                        -- MULT only: the t_{i1} factor (Eq. 3, i >= 2)
+    spec.omega0, spec.tail (0 = LINEAR, 1 = MULT), spec.L, spec.H
+"""
+import numpy as np
+
+NONFINITE_DEPTH = 255   # include/sand.h: non-finite query points report exit depth 255, sdf NaN
+LINEAR, MULT = 0, 1
+
+
+# --------------------------------------------------------------------------------------------
+# Volumetric network-depth map lookup   (Sec. 3.4 "we first query the
+# volumetric network-depth map (octree) for all points"; octree = Sec. 3.2, Eq. 7)
+# --------------------------------------------------------------------------------------------
+def cell_coords(points: np.ndarray, level: int) -> np.ndarray:
+    """Integer cell (ix, iy, iz) of each point in the 2^level grid over [-1,1]^3.
+
+    DESIGN.md reading R1 (the paper gives no cell arithmetic; SPEC S:318/S:337 fixes half-open
+    [lo, hi) with the global upper face closed).  The cell index is decided in float32, the
+    kernel's precision:  u = fl32(x + 1);  v = u * 2^(level-1) (exact);  v = min(max(v, 0),
+    2^level - 1);  c = floor(v).   Points outside [-1,1]^3 clamp to the boundary cell.
+    """
+    p = np.asarray(points, np.float32)
+    with np.errstate(over="ignore", invalid="ignore"):
+        u = p + np.float32(1.0)                              # one float32 rounding
+        v = u * np.float32(2.0 ** (level - 1))               # exact (power of two)
+        v = np.minimum(np.maximum(v, np.float32(0.0)), np.float32((1 << level) - 1))
+    return np.floor(v).astype(np.int64)
+
+
+def _finite_rows(points):
+    return np.isfinite(np.asarray(points, np.float32)).all(axis=1)
+
+
+def lookup_voxel(level, depth, far_sdf, points):
+    """Dense voxel depth map (BJ configs[0], [1]): payload of cell i + G*(j + G*k)."""
+    G = 1 << level
+    c = cell_coords(np.nan_to_num(points, nan=0.0), level)
+    lin = c[:, 0] + G * (c[:, 1] + G * c[:, 2])
+    d = np.asarray(depth, np.uint8)[lin]
+    f = np.asarray(far_sdf, np.float32)[lin] if far_sdf is not None else np.zeros(len(lin), np.float32)
+    return d, f, lin
+
+
+def lookup_octree(level, nodes, leaf_depth, leaf_far, points):
+    """Root-to-leaf descent (Sec. 3.2: the octree's leaf O(x) containing x, Eq. 5-7).
+
+    At step k the child octant is bit (level-1-k) of the level-`level` cell coordinates,
+    octant = xbit | ybit<<1 | zbit<<2 (include/sand.h node encoding).
+    """
+    nodes = np.asarray(nodes, np.uint32)
+    c = cell_coords(np.nan_to_num(points, nan=0.0), level)
+    n = c.shape[0]
+    node = np.zeros(n, np.int64)
+    leaf = np.full(n, -1, np.int64)
+    active = np.ones(n, bool)
+    for k in range(level + 1):
+        payload = nodes[node[active]]
+        is_leaf = (payload >> np.uint32(31)) == 1
+        idx_active = np.nonzero(active)[0]
+        done = idx_active[is_leaf]
+        leaf[done] = (payload[is_leaf] & np.uint32(0x7FFFFFFF)).astype(np.int64)
+        active[done] = False
+        if not active.any():
+            break
+        go = idx_active[~is_leaf]
+        child = payload[~is_leaf].astype(np.int64)
+        bit = level - 1 - k
+        oct_ = (((c[go, 0] >> bit) & 1) | (((c[go, 1] >> bit) & 1) << 1) | (((c[go, 2] >> bit) & 1) << 2))
+        node[go] = child + oct_
+    assert not active.any(), "octree deeper than its declared level"
+    d = np.asarray(leaf_depth, np.uint8)[leaf]
+    f = np.asarray(leaf_far, np.float32)[leaf] if leaf_far is not None else np.zeros(n, np.float32)
+    return d, f, leaf
+
+
+def lookup_bruteforce(leaf_level, leaf_ijk, leaf_depth, leaf_far, points):
+    """Brute-force linear scan over the leaf list (SPEC S:317 'traversal result equals linear scan
+    over serialized leaf list'): a leaf (l, i, j, k) contains x iff x's level-l cell is (i, j, k).
+    For tiny inputs only (O(n_points * n_leaves))."""
+    pts = np.nan_to_num(np.asarray(points, np.float32), nan=0.0)
+    n = pts.shape[0]
+    owner = np.full(n, -1, np.int64)
+    hits = np.zeros(n, np.int64)
+    for li in range(len(leaf_level)):
+        c = cell_coords(pts, int(leaf_level[li]))
+        inside = (c == np.asarray(leaf_ijk[li])[None, :]).all(axis=1)
+        owner[inside] = li
+        hits += inside
+    assert (hits == 1).all(), "leaves do not partition the domain"
+    d = np.asarray(leaf_depth, np.uint8)[owner]
+    f = np.asarray(leaf_far, np.float32)[owner] if leaf_far is not None else np.zeros(n, np.float32)
+    return d, f, owner
+
+
+def lookup(depthmap, points):
+    """Dispatch on a VoxelMap-like (level, depth, far_sdf) or Octree-like (level, nodes, ...)."""
+    if hasattr(depthmap, "nodes"):
+        return lookup_octree(depthmap.level, depthmap.nodes, depthmap.leaf_depth,
+                             depthmap.leaf_far_sdf, points)
+    return lookup_voxel(depthmap.level, depthmap.depth, depthmap.far_sdf, points)
+
+
+# --------------------------------------------------------------------------------------------
+# T-MLP   (Eq. 2; Eq. 3; sigma = sin(omega0 * .), SIREN)
+# --------------------------------------------------------------------------------------------
+def _layer(params, i, h):
+    """h_i = sigma(W_i h_{i-1} + b_i), sigma(z) = sin(omega0 z)  (Eq. 2; reading R4)."""
+    W = np.asarray(params.W[i - 1], np.float64)
+    b = np.asarray(params.b[i - 1], np.float64)
+    return np.sin(params.spec.omega0 * (h @ W.T + b))
+
+
+def _tail(params, i, h):
+    """t_i.  LINEAR: W_i^out h_i + b_i^out (Eq. 2).  MULT (i >= 2): t_{i0} * t_{i1} with
+    t_{i0} = W_{i0}^out h_i + b_{i0}^out, t_{i1} = W_{i1}^out h_i + b_{i1}^out (Eq. 3); the first
+    tail is always linear (Eq. 3 starts at i = 2)."""
+    a = np.asarray(params.a[i - 1], np.float64)
+    t = h @ a + float(params.c[i - 1])
+    if params.spec.tail == MULT and i >= 2:
+        a1 = np.asarray(params.a1[i - 2], np.float64)
+        t = t * (h @ a1 + float(params.c1[i - 2]))
+    return t
+
+
+def tmlp_trace(params, x):
+    """All cumulative outputs: returns (h list, t [L][n], y [L][n]) for h_0 = x, y_0 = 0,
+    y_i = y_{i-1} + t_i, i = 1..L (Eq. 2)."""
+    h = np.asarray(x, np.float64)
+    L = params.spec.L
+    n = h.shape[0]
+    y = np.zeros(n)
+    ts, ys, hs = [], [], []
+    for i in range(1, L + 1):
+        h = _layer(params, i, h)
+        t = _tail(params, i, h)
+        y = y + t
+        hs.append(h); ts.append(t); ys.append(y)
+    return hs, np.array(ts), np.array(ys)
+
+
+def tmlp_forward(params, x, depth):
+    """y_{d(x)}(x) = sum_{k <= d(x)} t_k(x) for a per-point depth d >= 1 (Eq. 2 truncated at the
+    exit depth; Sec. 3.4 P:368 'network evaluation with point-wise adaptive depths').  Layers
+    beyond a point's depth are never evaluated for that point (only rows with d >= i enter layer i).
+    """
+    x = np.asarray(x, np.float64)
+    depth = np.broadcast_to(np.asarray(depth, np.int64), (x.shape[0],))
+    n = x.shape[0]
+    H = params.spec.H
+    y = np.zeros(n)
+    h = np.zeros((n, H))
+    dmax = int(depth.max()) if n else 0
+    for i in range(1, dmax + 1):
+        act = np.nonzero(depth >= i)[0]
+        hin = x[act] if i == 1 else h[act]
+        hi = _layer(params, i, hin)
+        h[act] = hi
+        y[act] = y[act] + _tail(params, i, hi)
+    return y
+
+
+def query(params, depthmap, points, lod_cap=None):
+    """SAND adaptive inference (Sec. 3.4):
+      1. look up every point in the depth map;
+      2. far leaves (depth 0, Eq. 7): return the cached sdf(c_N), no network evaluation;
+      3. near leaves: evaluate the T-MLP to d = min(d(N), cap) (LOD cap) and return y_d.
+    Non-finite points -> (NaN, 255) (include/sand.h).  Returns (sdf float64 [n], exit depth u8 [n]).
+    """
+    pts = np.asarray(points, np.float32)
+    n = pts.shape[0]
+    fin = _finite_rows(pts)
+    d, far, _ = lookup(depthmap, pts)
+    d = d.astype(np.int64)
+    if lod_cap is not None:
+        d = np.where(d > 0, np.minimum(d, int(lod_cap)), d)   # reading R16: cap only d >= 1
+    sdf = np.zeros(n)
+    isfar = fin & (d == 0)
+    sdf[isfar] = far[isfar].astype(np.float64)
+    near = np.nonzero(fin & (d > 0))[0]
+    if near.size:
+        sdf[near] = tmlp_forward(params, pts[near], d[near])
+    sdf[~fin] = np.nan
+    ed = np.where(fin, d, NONFINITE_DEPTH).astype(np.uint8)
+    return sdf, ed
+
+
+def query_full(params, points):
+    """Uniform full-depth evaluation y_L for every point (Eq. 2 at i = L; SPEC query_full S:374)."""
+    return tmlp_forward(params, np.asarray(points, np.float32), params.spec.L)
