@@ -1,0 +1,163 @@
+/*
+ * sand.h -- C ABI of libsand, the B200 (sm_100a) engine for SAND's adaptive-depth T-MLP query path.
+ *
+ * Method: SAND, "Spatially Adaptive Network Depth for Fast Sampling of Neural Implicit Surfaces"
+ * (arxiv 2604.25936; /root/reference/PAPER.md = "P:<line>").  A query point x first looks up its
+ * required network depth d(x) in a volumetric network-depth map (Sec. 3.2; inference
+ * Sec. 3.4); far leaves (d = 0) return a cached SDF value (Eq. 7); near
+ * points evaluate the tailed MLP (T-MLP, Eq. 2; multiplicative tails Eq. 3)
+ * only up to layer d and return the cumulative output y_d = sum_{k<=d} t_k.
+ *
+ * Conventions for every entry point:
+ *   - Return value: 0 (SAND_OK) on success, a negative sand_status on error.  No C++ exception
+ *     crosses the ABI.  sand_last_error(ctx) returns a human-readable message for the last error.
+ *   - Ownership: the caller owns every pointer it passes in; libsand copies what it keeps (weights,
+ *     depth map).  The context owns its device copies and its workspace.
+ *   - Threading: one context per device; calls on one context must not race.  Different contexts
+ *     are independent (the multi-GPU driver uses one context per rank/GPU).
+ *   - No collective communication happens inside the library.
+ *   - Device pointers ("d_" prefix) must be CUDA device memory of the context's device.
+ */
+#ifndef SAND_H_
+#define SAND_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SAND_ABI_VERSION 1
+#define SAND_MAX_L 32
+#define SAND_DEPTH_NONFINITE 255
+
+typedef enum {
+  SAND_OK = 0,
+  SAND_ERR_ARG = -1,         /* NULL where not allowed, negative size, out-of-range knob      */
+  SAND_ERR_STATE = -2,       /* e.g. sand_query before both sand_load_weights and _depthmap    */
+  SAND_ERR_SIZE = -3,        /* weight blob length does not match (L, H, tail)                  */
+  SAND_ERR_DEPTHMAP = -4,    /* malformed depth map (depth > L, bad node index, cycle, level)   */
+  SAND_ERR_CUDA = -5,        /* a CUDA runtime error; message via sand_last_error               */
+  SAND_ERR_OOM = -6,         /* device allocation failed                                         */
+  SAND_ERR_UNSUPPORTED = -7  /* configuration not supported by this build (e.g. H for a precision) */
+} sand_status;
+
+/* Arithmetic of the H x H layers.
+ *   SAND_FP32  : FP32 SIMT kernels (FFMA, accurate sinf); supported H in {16, 32, 64}.
+ *                Tolerance vs the oracle: 1e-4 max-abs (BASELINE.json north_star).
+ *   SAND_BF16  : tcgen05 tensor cores, BF16 operands, FP32 accumulate in TMEM; layer 1 (K = 3)
+ *                and all tails in FP32; supported H in {64, 128, 256, 336}.  Tolerance 5e-3.
+ *   SAND_TF32X3: reserved (returns SAND_ERR_UNSUPPORTED in this build).                        */
+typedef enum { SAND_FP32 = 0, SAND_TF32X3 = 1, SAND_BF16 = 2 } sand_precision;
+
+/* Tail form: LINEAR t_i = a_i . h_i + c_i for every layer (BASELINE.json configs);
+ * MULT t_1 linear, t_i = (a_i0 . h_i + c_i0) * (a_i1 . h_i + c_i1) for i >= 2 (Eq. 3).        */
+typedef enum { SAND_TAIL_LINEAR = 0, SAND_TAIL_MULT = 1 } sand_tail_mode;
+
+typedef struct {
+  int L;                 /* hidden layers, 1..SAND_MAX_L                                       */
+  int H;                 /* hidden width                                                        */
+  float omega0;          /* SIREN frequency: h_i = sin(omega0 * (W_i h_{i-1} + b_i)), > 0       */
+  sand_precision prec;
+  sand_tail_mode tail;
+  int device;            /* CUDA device ordinal the context binds to                            */
+} sand_config;
+
+typedef struct sand_ctx sand_ctx;   /* opaque */
+
+/* Create a context on cfg->device.  Validates L in [1, 32], omega0 > 0 and that (prec, H) is a
+ * supported pair.  *out is set only on success.  Errors: SAND_ERR_ARG, SAND_ERR_UNSUPPORTED,
+ * SAND_ERR_CUDA. */
+int sand_create(const sand_config* cfg, sand_ctx** out);
+
+/* Release every device resource of ctx.  NULL-safe.  Synchronizes ctx's stream first. */
+int sand_destroy(sand_ctx* ctx);
+
+/* Load the T-MLP parameters (Eq. 2/3) from a HOST FP32 blob in canonical order:
+ *   for i = 1..L: W_i [H][fan_in] row-major (fan_in = 3 if i == 1 else H), b_i [H];
+ *   LINEAR tails: for i = 1..L: a_i [H], c_i;
+ *   MULT tails  : a_1 [H], c_1, then for i = 2..L: a_i0 [H], c_i0, a_i1 [H], c_i1.
+ * n_floats must match exactly (else SAND_ERR_SIZE).  The blob is copied, converted on the device
+ * (BF16 round-to-nearest-even for the H x H matrices in SAND_BF16 mode, laid out in the tcgen05
+ * shared-memory image) and never referenced again.  Synchronous w.r.t. the host blob. */
+int sand_load_weights(sand_ctx* ctx, const float* host_blob, size_t n_floats);
+
+/* Volumetric network-depth map (Sec. 3.2; Eq. 7).  Domain [-1,1]^3; cell membership half-open
+ * [lo, hi) per axis with the global upper face closed; points outside the domain clamp to the
+ * boundary cell (their network input stays unclamped).  Cell arithmetic (float32, exact except
+ * one rounding): u = x + 1; v = u * 2^(level-1); v = min(max(v, 0), 2^level - 1); c = floor(v).  */
+typedef struct {
+  int kind;                 /* 0 = dense voxel grid, 1 = octree                                 */
+  int level;                /* voxel: G = 2^level cells per axis (1..10); octree: max level (0..20) */
+  const uint8_t* depth;     /* HOST. voxel: G^3 depths, index i + G*(j + G*k) (x fastest);
+                               octree: per-leaf depth.  0 = far (cached SDF), 1..L = exit depth  */
+  const float* far_sdf;     /* HOST, optional (NULL if no depth-0 entry): cached SDF per cell/leaf */
+  const uint32_t* nodes;    /* HOST, octree only: node i: bit31 = 1 -> leaf, low 31 bits = leaf
+                               index; bit31 = 0 -> index of the first of 8 contiguous children,
+                               octant = xbit | ybit<<1 | zbit<<2.  Node 0 is the root.           */
+  int64_t n_nodes, n_leaves;
+} sand_depthmap;
+
+/* Copy a depth map to the device.  Validates depth <= L, child/leaf indices in range, descent
+ * terminates within `level` steps; octrees with level <= 8 are baked on the device into a dense
+ * 2^level grid (one load per query).  Errors: SAND_ERR_ARG, SAND_ERR_DEPTHMAP, SAND_ERR_OOM.     */
+int sand_load_depthmap(sand_ctx* ctx, const sand_depthmap* dm);
+
+/* Stream on which every subsequent kernel of ctx is enqueued (a cudaStream_t; NULL = legacy 0). */
+int sand_set_stream(sand_ctx* ctx, void* cuda_stream);
+
+/* Level-of-detail cap (Sec. 3.4; Fig. 4): evaluated depth = min(d, cap) for d >= 1;
+ * depth-0 (far) entries are unaffected.  cap in 1..L (default L).  Error: SAND_ERR_ARG.          */
+int sand_set_lod_cap(sand_ctx* ctx, int cap);
+
+/* Optional: pre-size the workspace for queries of up to n_max points (avoids allocation inside
+ * sand_query, required before CUDA-graph capture). */
+int sand_reserve(sand_ctx* ctx, int64_t n_max);
+
+/* Adaptive SDF query (Sec. 3.4): for each of n points (d_points: n x 3 float32 AoS, device),
+ *   d_out_exit_depth[i] = evaluated depth (0 = far/cached, 1..L, 255 = non-finite point);
+ *   d_out_sdf[i]        = cached sdf (depth 0), y_d (Eq. 2), or NaN (non-finite point).
+ * Asynchronous on ctx's stream; n == 0 is a no-op; outputs fully overwritten; inputs untouched.
+ * d_points needs 4-byte alignment (16-byte alignment takes the vectorised path).
+ * Errors: SAND_ERR_ARG, SAND_ERR_STATE, SAND_ERR_OOM, SAND_ERR_CUDA.                            */
+int sand_query(sand_ctx* ctx, const float* d_points, int64_t n,
+               float* d_out_sdf, uint8_t* d_out_exit_depth);
+
+/* End-to-end variant with HOST buffers: copies points host->device, runs sand_query, copies the
+ * results device->host, in chunks of at most chunk_points (0 = whole array) double-buffered over
+ * two streams.  Host buffers should be pinned for full bandwidth.  Returns after the results are
+ * in host memory (synchronous). */
+int sand_query_host(sand_ctx* ctx, const float* h_points, int64_t n,
+                    float* h_out_sdf, uint8_t* h_out_exit_depth, int64_t chunk_points);
+
+typedef struct {
+  int64_t n;                      /* points in the last query                                    */
+  int64_t n_nonfinite;            /* points with a non-finite coordinate                         */
+  int64_t per_depth[SAND_MAX_L + 1]; /* per evaluated depth 0..L (conservation: sum + nonfinite = n) */
+  int64_t tiles;                  /* 128-row tiles the fused T-MLP kernel processed              */
+  double flops_exec;              /* executed H x H FLOPs: sum_p (d_p - 1) * 2 H^2               */
+  double flops_ns;                /* north-star formula: sum_p d_p * 2 H^2                        */
+  float ms_lookup, ms_bin, ms_mlp, ms_total;  /* CUDA-event times of the last sand_query         */
+} sand_stats;
+
+/* Statistics of the last sand_query on ctx.  Synchronizes ctx's stream. */
+int sand_get_stats(sand_ctx* ctx, sand_stats* out);
+
+/* Diagnostic: copy the depth-binning permutation of the last query to host_perm[0 .. min(cap,
+ * n_binned)): indices of the points with evaluated depth 1..L, grouped by depth (deepest first) and
+ * in ascending point order within a depth.  *n_binned = number of such points.  host_perm may be
+ * NULL to query the count only.  Synchronizes ctx's stream. */
+int sand_debug_perm(sand_ctx* ctx, uint32_t* host_perm, int64_t cap, int64_t* n_binned);
+
+/* Message for the last error on ctx (or of the last failed sand_create if ctx is NULL).
+ * Valid until the next call on ctx.  Never NULL. */
+const char* sand_last_error(const sand_ctx* ctx);
+
+/* ABI version (SAND_ABI_VERSION) of the loaded library. */
+int sand_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SAND_H_ */

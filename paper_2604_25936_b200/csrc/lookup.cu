@@ -1,0 +1,325 @@
+// lookup.cu -- K1 depth-map lookup, K2a scan, K2b stable binning scatter, octree baking.
+//
+// K1 (Sec. 3.4, "we first query the volumetric network-depth map for all points";
+// Eq. 7 P:237-246 far leaves return the cached SDF; LOD cap P:370): one pass over the n x 3 float32
+// points (float4-vectorised, 12 B/pt) -> exit depth (1 B/pt), cached SDF for depth-0 points, and a
+// per-block depth histogram.  K2a scans the histograms (deepest depth first) and K2b scatters point
+// indices into perm[] so that every 128-row tile of the T-MLP kernel has one uniform depth (SPEC
+// S:412 "depth-bucketed batching").  All three are HBM/L2-bound streaming kernels.
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "sand_internal.h"
+
+namespace sand {
+
+// Cell index along one axis; float32, no contraction: u = x + 1 (one rounding), v = u * 2^(l-1)
+// (exact), clamp in float, floor.  Identical arithmetic to the oracle (reading R1).
+__device__ __forceinline__ uint32_t cell_of(float x, float scale, float maxc) {
+  float u = __fadd_rn(x, 1.0f);
+  float v = __fmul_rn(u, scale);
+  v = fminf(fmaxf(v, 0.0f), maxc);
+  return (uint32_t)v;  // v >= 0 : truncation == floor
+}
+
+struct LookupResult {
+  uint32_t d;   // 0..L, or 255
+  float far;
+};
+
+__device__ __forceinline__ LookupResult lookup_one(float x, float y, float z, const LookupParams& lp,
+                                                   float scale, float maxc) {
+  LookupResult r;
+  if (!(isfinite(x) && isfinite(y) && isfinite(z))) {
+    r.d = SAND_DEPTH_NONFINITE;
+    r.far = __int_as_float(0x7fc00000);
+    return r;
+  }
+  const uint32_t cx = cell_of(x, scale, maxc), cy = cell_of(y, scale, maxc), cz = cell_of(z, scale, maxc);
+  uint32_t d;
+  float far = 0.0f;
+  if (lp.dense) {
+    const uint64_t lin = (uint64_t)cx + ((uint64_t)cy << lp.level) + ((uint64_t)cz << (2 * lp.level));
+    d = __ldg(lp.grid + lin);
+    if (d == 0 && lp.grid_far) far = __ldg(lp.grid_far + lin);
+  } else {
+    uint32_t node = 0, v = __ldg(lp.nodes);
+    for (int bit = lp.level - 1; !(v >> 31) && bit >= 0; --bit) {
+      const uint32_t oct = ((cx >> bit) & 1u) | (((cy >> bit) & 1u) << 1) | (((cz >> bit) & 1u) << 2);
+      node = v + oct;
+      v = __ldg(lp.nodes + node);
+    }
+    const uint32_t leaf = v & 0x7FFFFFFFu;
+    d = __ldg(lp.leaf_depth + leaf);
+    if (d == 0 && lp.leaf_far) far = __ldg(lp.leaf_far + leaf);
+  }
+  if (d > (uint32_t)lp.cap) d = (uint32_t)lp.cap;  // d >= 1 only: cap >= 1 leaves 0 untouched
+  r.d = d;
+  r.far = far;
+  return r;
+}
+
+__global__ void __launch_bounds__(kLookupThreads) k_lookup(const float* __restrict__ pts, long long n,
+                                                            LookupParams lp, uint8_t* __restrict__ out_depth,
+                                                            float* __restrict__ out_sdf,
+                                                            uint32_t* __restrict__ hist, long long nblk,
+                                                            int vec_in, int vec_out) {
+  __shared__ uint32_t sh[kMaxBins];
+  const int nb = lp.L + 2;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  const float scale = (float)(1u << lp.level) * 0.5f;
+  const float maxc = (float)((1u << lp.level) - 1u);
+  const long long base = (long long)blockIdx.x * kLookupChunk;
+  const int lane = threadIdx.x & 31;
+#pragma unroll 1
+  for (int it = 0; it < kLookupChunk / (4 * kLookupThreads); ++it) {
+    const long long p0 = base + (long long)it * 4 * kLookupThreads + 4 * threadIdx.x;
+    const long long rem = n - p0;
+    const int cnt = rem >= 4 ? 4 : (rem > 0 ? (int)rem : 0);
+    float px[4], py[4], pz[4];
+    if (cnt == 4 && vec_in) {
+      const float4* q = reinterpret_cast<const float4*>(pts + 3 * p0);
+      const float4 a = __ldcs(q), b = __ldcs(q + 1), c = __ldcs(q + 2);
+      px[0] = a.x; py[0] = a.y; pz[0] = a.z; px[1] = a.w;
+      py[1] = b.x; pz[1] = b.y; px[2] = b.z; py[2] = b.w;
+      pz[2] = c.x; px[3] = c.y; py[3] = c.z; pz[3] = c.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (j < cnt) {
+          px[j] = pts[3 * (p0 + j)]; py[j] = pts[3 * (p0 + j) + 1]; pz[j] = pts[3 * (p0 + j) + 2];
+        } else {
+          px[j] = py[j] = pz[j] = 0.0f;
+        }
+      }
+    }
+    uint32_t dw = 0;
+    int bins[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const LookupResult r = lookup_one(px[j], py[j], pz[j], lp, scale, maxc);
+      dw |= (r.d & 0xFFu) << (8 * j);
+      bins[j] = (j < cnt) ? (r.d == SAND_DEPTH_NONFINITE ? lp.L + 1 : (int)r.d) : -1;
+      if (j < cnt && (r.d == 0 || r.d == SAND_DEPTH_NONFINITE)) out_sdf[p0 + j] = r.far;
+    }
+    if (cnt == 4 && vec_out) {
+      *reinterpret_cast<uint32_t*>(out_depth + p0) = dw;
+    } else {
+      for (int j = 0; j < cnt; ++j) out_depth[p0 + j] = (uint8_t)(dw >> (8 * j));
+    }
+    // warp-aggregated shared-memory histogram
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const unsigned m = __match_any_sync(0xffffffffu, bins[j]);
+      if (bins[j] >= 0 && lane == (__ffs(m) - 1)) atomicAdd(&sh[bins[j]], (uint32_t)__popc(m));
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) hist[(long long)i * nblk + blockIdx.x] = sh[i];
+}
+
+// Block-wide exclusive scan helper (1024 threads).
+__device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long v, unsigned long long* tot) {
+  __shared__ unsigned long long ws[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned long long inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  if (lane == 31) ws[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    unsigned long long s = (lane < (int)(blockDim.x >> 5)) ? ws[lane] : 0ull;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long t = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += t;
+    }
+    ws[lane] = s;
+  }
+  __syncthreads();
+  const unsigned long long wpre = w ? ws[w - 1] : 0ull;
+  *tot = ws[(blockDim.x >> 5) - 1];
+  __syncthreads();
+  return wpre + inc - v;
+}
+
+__global__ void __launch_bounds__(1024) k_scan(const uint32_t* __restrict__ hist, long long nblk, int L,
+                                               uint32_t* __restrict__ offs, QueryMeta* __restrict__ meta) {
+  __shared__ long long counts[kMaxBins];
+  const long long per = (nblk + blockDim.x - 1) / blockDim.x;
+  const long long b0 = threadIdx.x * per;
+  const long long b1 = (b0 + per < nblk) ? b0 + per : nblk;
+  unsigned long long running = 0;
+  // depth-0 and non-finite bins: totals only
+  for (int bin = 0; bin < L + 2; ++bin) {
+    unsigned long long s = 0;
+    for (long long b = b0; b < b1; ++b) s += hist[(long long)bin * nblk + b];
+    unsigned long long tot;
+    const unsigned long long ex = block_excl_scan(s, &tot);
+    if (bin >= 1 && bin <= L) {
+      // (recomputed below in deepest-first order)
+    }
+    if (threadIdx.x == 0) counts[bin] = (long long)tot;
+    (void)ex;
+  }
+  __syncthreads();
+  // deepest-first scatter offsets
+  for (int d = L; d >= 1; --d) {
+    unsigned long long s = 0;
+    for (long long b = b0; b < b1; ++b) s += hist[(long long)d * nblk + b];
+    unsigned long long tot;
+    unsigned long long ex = block_excl_scan(s, &tot) + running;
+    for (long long b = b0; b < b1; ++b) {
+      offs[(long long)d * nblk + b] = (uint32_t)ex;
+      ex += hist[(long long)d * nblk + b];
+    }
+    if (threadIdx.x == 0) meta->start[d] = (long long)running;
+    running += tot;
+  }
+  if (threadIdx.x == 0) {
+    long long tb = 0;
+    for (int b = 0; b < kMaxBins; ++b) {
+      meta->count[b] = (b < L + 2) ? counts[b] : 0;
+      meta->tile_begin[b] = meta->tile_end[b] = 0;
+    }
+    meta->start[0] = 0;
+    for (int d = L; d >= 1; --d) {
+      meta->tile_begin[d] = tb;
+      tb += (counts[d] + kTileM - 1) / kTileM;
+      meta->tile_end[d] = tb;
+    }
+    meta->total_tiles = tb;
+  }
+}
+
+__global__ void __launch_bounds__(kLookupThreads) k_scatter(const uint8_t* __restrict__ depth, long long n,
+                                                             int L, const uint32_t* __restrict__ offs,
+                                                             uint32_t* __restrict__ perm, long long nblk,
+                                                             int vec) {
+  constexpr int kWarps = kLookupThreads / 32;
+  __shared__ uint32_t run[kMaxBins];
+  __shared__ uint32_t wtot[kWarps][kMaxBins];
+  __shared__ uint32_t btot[kMaxBins];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int d = tid; d < kMaxBins; d += blockDim.x) {
+    run[d] = (d >= 1 && d <= L) ? offs[(long long)d * nblk + blockIdx.x] : 0u;
+    for (int w = 0; w < kWarps; ++w) wtot[w][d] = 0;
+  }
+  __syncthreads();
+  const long long base = (long long)blockIdx.x * kLookupChunk;
+#pragma unroll 1
+  for (int it = 0; it < kLookupChunk / (4 * kLookupThreads); ++it) {
+    const long long p0 = base + (long long)it * 4 * kLookupThreads + 4 * tid;
+    const long long rem = n - p0;
+    const int cnt = rem >= 4 ? 4 : (rem > 0 ? (int)rem : 0);
+    int dj[4];
+    if (cnt == 4 && vec) {
+      const uint32_t w4 = *reinterpret_cast<const uint32_t*>(depth + p0);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dj[j] = (w4 >> (8 * j)) & 0xFF;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dj[j] = (j < cnt) ? depth[p0 + j] : 0;
+    }
+    unsigned mine = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (dj[j] < 1 || dj[j] > L) dj[j] = 0;  // not binned: far, non-finite or padding
+      if (dj[j]) mine |= 1u << (dj[j] - 1);
+    }
+    unsigned present = __reduce_or_sync(0xffffffffu, mine);
+    int rank[4] = {0, 0, 0, 0};
+    while (present) {
+      const int v = __ffs(present);  // depth value v (bit v-1)
+      present &= present - 1;
+      unsigned tot = 0, before = 0;
+      unsigned m[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        m[j] = __ballot_sync(0xffffffffu, dj[j] == v);
+        tot += __popc(m[j]);
+        before += __popc(m[j] & lt);
+      }
+      int local = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (dj[j] == v) { rank[j] = (int)before + local; ++local; }
+      }
+      if (lane == 0) wtot[warp][v] = tot;
+    }
+    __syncthreads();
+    if (tid >= 1 && tid <= L) {
+      uint32_t acc = 0;
+      for (int w = 0; w < kWarps; ++w) { const uint32_t t = wtot[w][tid]; wtot[w][tid] = acc; acc += t; }
+      btot[tid] = acc;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (dj[j]) perm[run[dj[j]] + wtot[warp][dj[j]] + rank[j]] = (uint32_t)(p0 + j);
+    }
+    __syncthreads();
+    if (tid >= 1 && tid <= L) {
+      run[tid] += btot[tid];
+      for (int w = 0; w < kWarps; ++w) wtot[w][tid] = 0;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_bake(const uint32_t* __restrict__ nodes, const uint8_t* __restrict__ leaf_depth,
+                       const float* __restrict__ leaf_far, int level, uint8_t* __restrict__ grid,
+                       float* __restrict__ grid_far, int* err) {
+  const long long G = 1ll << level;
+  const long long total = G * G * G;
+  for (long long lin = blockIdx.x * (long long)blockDim.x + threadIdx.x; lin < total;
+       lin += (long long)gridDim.x * blockDim.x) {
+    const uint32_t cx = (uint32_t)(lin & (G - 1)), cy = (uint32_t)((lin >> level) & (G - 1)),
+                   cz = (uint32_t)(lin >> (2 * level));
+    uint32_t v = nodes[0];
+    int bit = level - 1;
+    for (; !(v >> 31) && bit >= 0; --bit) {
+      const uint32_t oct = ((cx >> bit) & 1u) | (((cy >> bit) & 1u) << 1) | (((cz >> bit) & 1u) << 2);
+      v = nodes[v + oct];
+    }
+    if (!(v >> 31)) { *err = 1; continue; }
+    const uint32_t leaf = v & 0x7FFFFFFFu;
+    grid[lin] = leaf_depth[leaf];
+    if (grid_far) grid_far[lin] = leaf_far ? leaf_far[leaf] : 0.0f;
+  }
+}
+
+cudaError_t launch_lookup(const float* pts, long long n, const LookupParams& lp, uint8_t* out_depth,
+                          float* out_sdf, uint32_t* hist, long long nblk, cudaStream_t st) {
+  const int vec_in = ((reinterpret_cast<uintptr_t>(pts) & 15) == 0) ? 1 : 0;
+  const int vec_out = ((reinterpret_cast<uintptr_t>(out_depth) & 3) == 0) ? 1 : 0;
+  k_lookup<<<(unsigned)nblk, kLookupThreads, 0, st>>>(pts, n, lp, out_depth, out_sdf, hist, nblk, vec_in,
+                                                      vec_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scan(const uint32_t* hist, long long nblk, int L, uint32_t* offs, QueryMeta* meta,
+                        cudaStream_t st) {
+  k_scan<<<1, 1024, 0, st>>>(hist, nblk, L, offs, meta);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scatter(const uint8_t* depth, long long n, int L, const uint32_t* offs, uint32_t* perm,
+                           long long nblk, cudaStream_t st) {
+  const int vec = ((reinterpret_cast<uintptr_t>(depth) & 3) == 0) ? 1 : 0;
+  k_scatter<<<(unsigned)nblk, kLookupThreads, 0, st>>>(depth, n, L, offs, perm, nblk, vec);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bake_octree(const uint32_t* nodes, const uint8_t* leaf_depth, const float* leaf_far,
+                               int level, uint8_t* grid, float* grid_far, int* err_flag, cudaStream_t st) {
+  k_bake<<<148 * 8, 256, 0, st>>>(nodes, leaf_depth, leaf_far, level, grid, grid_far, err_flag);
+  return cudaGetLastError();
+}
+
+}  // namespace sand

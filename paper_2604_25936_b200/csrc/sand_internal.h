@@ -1,0 +1,74 @@
+// sand_internal.h -- device-side structures shared by libsand's kernels and its host code.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/sand.h"
+
+namespace sand {
+
+constexpr int kTileM = 128;           // rows (points) per T-MLP tile = tcgen05 M
+constexpr int kLookupThreads = 256;   // K1 / K2b block size
+constexpr int kLookupChunk = 4096;    // points per K1 / K2b block (16 per thread, 4 x float4 groups)
+constexpr int kMaxBins = SAND_MAX_L + 2;  // depths 0..L plus one bin for non-finite points
+
+// Written by the scan kernel (K2a), read by the T-MLP kernels and by sand_get_stats.
+// Tiles are ordered deepest depth first; tile t belongs to depth d iff tile_begin[d] <= t < tile_end[d].
+struct QueryMeta {
+  long long count[kMaxBins];      // points per bin (bin L+1 = non-finite)
+  long long start[kMaxBins];      // first perm[] row of depth d (d >= 1)
+  long long tile_begin[kMaxBins];
+  long long tile_end[kMaxBins];
+  long long total_tiles;
+};
+
+struct LookupParams {
+  int dense;              // 1: dense grid (voxel or baked octree), 0: octree descent
+  int level;
+  int L;
+  int cap;                // LOD cap (1..L)
+  const uint8_t* grid;    // dense: G^3 depth
+  const float* grid_far;  // dense: G^3 cached sdf or nullptr
+  const uint32_t* nodes;  // octree
+  const uint8_t* leaf_depth;
+  const float* leaf_far;
+};
+
+// Host-side launchers (lookup.cu)
+cudaError_t launch_lookup(const float* pts, long long n, const LookupParams& lp, uint8_t* out_depth,
+                          float* out_sdf, uint32_t* hist, long long nblk, cudaStream_t st);
+cudaError_t launch_scan(const uint32_t* hist, long long nblk, int L, uint32_t* offs, QueryMeta* meta,
+                        cudaStream_t st);
+cudaError_t launch_scatter(const uint8_t* depth, long long n, int L, const uint32_t* offs, uint32_t* perm,
+                           long long nblk, cudaStream_t st);
+cudaError_t launch_bake_octree(const uint32_t* nodes, const uint8_t* leaf_depth, const float* leaf_far,
+                               int level, uint8_t* grid, float* grid_far, int* err_flag, cudaStream_t st);
+
+// T-MLP parameters as the kernels consume them (built by sand_load_weights).
+struct MlpDev {
+  int L, H, tail;
+  float omega0;
+  // FP32 SIMT path: raw hidden weights [L-1][H][H] (row-major W_i[j][k]) and biases
+  const float* w_hidden;     // (L-1)*H*H
+  // BF16 tcgen05 path: pre-swizzled SW128 K-major image [L-1][KC][H rows][128 B]
+  const void* w_image;
+  // FP32 tables (both paths):
+  //   w1: float4[H] = (w0*W1[j][0], w0*W1[j][1], w0*W1[j][2], w0*b1[j])
+  //   bias: [L-1][H] = w0 * b_i (i >= 2);  a: [L][H] tail (a_i or a_i0); c: [L]
+  //   a1: [L-1][H] (MULT, i >= 2) ; c1: [L-1]
+  const float* tables;
+  long long off_w1, off_bias, off_a, off_c, off_a1, off_c1, tables_floats;
+};
+
+cudaError_t launch_tmlp_simt(const MlpDev& m, const float* pts, const uint32_t* perm, const QueryMeta* meta,
+                             float* out_sdf, int num_sms, cudaStream_t st);
+cudaError_t launch_tmlp_tc(const MlpDev& m, const float* pts, const uint32_t* perm, const QueryMeta* meta,
+                           float* out_sdf, int num_sms, cudaStream_t st);
+// configuration query: dynamic smem bytes for the tc kernel, 0 if unsupported
+size_t tc_smem_bytes(int L, int H, int tail);
+bool tc_supported_H(int H);
+bool simt_supported_H(int H);
+size_t simt_smem_bytes(int L, int H, int tail);
+cudaError_t prepare_tmlp_kernels(int L, int H, int tail, int prec);
+
+}  // namespace sand

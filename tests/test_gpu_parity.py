@@ -1,0 +1,232 @@
+"""GPU parity: libsand (CUDA, via the C ABI) vs the oracle on the same seeded inputs.
+
+Bar (BASELINE.json north_star): exit depths bit-exact on every compared point; SDF max-abs <= 5e-3
+(BF16 path) / 1e-4 (FP32 path); sign agreement wherever |oracle| > 5e-3.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import sandgen as g
+from _engine import (TOL_BF16, TOL_FP32, assert_parity, make_ctx, run_engine, stratified_sample)
+
+pytestmark = pytest.mark.gpu
+
+BF16, FP32 = 2, 0
+
+
+def _random_voxel_map(level, L, seed, far=False):
+    rng = np.random.default_rng(seed)
+    G = 1 << level
+    lo = 0 if far else 1
+    dep = rng.integers(lo, L + 1, G ** 3).astype(np.uint8)
+    fs = rng.normal(size=G ** 3).astype(np.float32) if far else None
+    return g.VoxelMap(level, dep, fs)
+
+
+def _pts(n, seed, lo=-1.0, hi=1.0):
+    return np.random.default_rng(seed).uniform(lo, hi, (n, 3)).astype(np.float32)
+
+
+@pytest.mark.parametrize("H", [64, 128, 256, 336])
+@pytest.mark.parametrize("tail", [0, 1])
+def test_bf16_random_depths_small(H, tail):
+    """All depths 1..L mixed, several tiles per depth with ragged tails, n not a multiple of 4."""
+    L = 5
+    spec = g.TMlpSpec(L=L, H=H, omega0=30.0, tail=tail, seed=4)
+    p = g.make_weights(spec)
+    dm = _random_voxel_map(3, L, 1)
+    pts = _pts(7001, 2)
+    with make_ctx(spec, BF16) as ctx:
+        sdf, dep = run_engine(ctx, p, dm, pts)
+    sdf_or, dep_or = oracle.query(p, dm, pts)
+    assert_parity(sdf, dep, sdf_or, dep_or, TOL_BF16)
+
+
+@pytest.mark.parametrize("H", [16, 32, 64])
+@pytest.mark.parametrize("tail", [0, 1])
+def test_fp32_random_depths_small(H, tail):
+    L = 4
+    spec = g.TMlpSpec(L=L, H=H, omega0=30.0, tail=tail, seed=5)
+    p = g.make_weights(spec)
+    dm = _random_voxel_map(4, L, 3)
+    pts = _pts(5003, 4)
+    with make_ctx(spec, FP32) as ctx:
+        sdf, dep = run_engine(ctx, p, dm, pts)
+    sdf_or, dep_or = oracle.query(p, dm, pts)
+    assert_parity(sdf, dep, sdf_or, dep_or, TOL_FP32)
+
+
+def test_C0_full_fp32():
+    """BASELINE.json configs[0] at full size (262,144 points), every point vs the oracle."""
+    c = g.make_config("C0")
+    p = c.params()
+    pts = c.points_fn()
+    with make_ctx(c.spec, FP32) as ctx:
+        sdf, dep = run_engine(ctx, p, c.depthmap, pts)
+        st = ctx.sand_get_stats()
+    sdf_or, dep_or = oracle.query(p, c.depthmap, pts)
+    assert_parity(sdf, dep, sdf_or, dep_or, TOL_FP32)
+    assert sum(st["per_depth"]) + st["n_nonfinite"] == pts.shape[0]
+    np.testing.assert_array_equal(st["per_depth"], np.bincount(dep_or, minlength=c.spec.L + 1))
+
+
+def test_C1_full_bf16():
+    """configs[1] (256^3 grid, 16.8M points): exit depth of every point bit-exact; SDF on a seeded
+    uniform + per-depth stratified sample."""
+    c = g.make_config("C1")
+    p = c.params()
+    pts = c.points_fn()
+    with make_ctx(c.spec, BF16) as ctx:
+        sdf, dep = run_engine(ctx, p, c.depthmap, pts)
+    d_or, _, _ = oracle.lookup(c.depthmap, pts)
+    np.testing.assert_array_equal(dep, d_or)
+    idx = stratified_sample(dep, 4096, 1 << 16, seed=1)
+    sdf_or, dep_or = oracle.query(p, c.depthmap, pts[idx])
+    assert_parity(sdf, dep, sdf_or, dep_or, TOL_BF16, idx=idx)
+
+
+@pytest.mark.parametrize("name", ["C2", "C3"])
+def test_C2_C3_full_size_sampled(name):
+    """configs[2] (512^3 grid, 134M points, level-7 octree) and configs[3] (8x336, 8M cloud) in the
+    bench's launch configuration: exit depths bit-exact on sampled z-slabs (C2) / all points (C3),
+    SDF on a stratified sample."""
+    c = g.make_config(name)
+    p = c.params()
+    pts = c.points_fn()
+    with make_ctx(c.spec, BF16) as ctx:
+        sdf, dep = run_engine(ctx, p, c.depthmap, pts)
+        st = ctx.sand_get_stats()
+    n = pts.shape[0]
+    if name == "C2":
+        R = c.grid_R
+        planes = np.arange(0, R, 37)
+        chk = (planes[:, None] * R * R + np.arange(R * R)[None, :]).ravel()
+    else:
+        chk = np.arange(n)
+    d_or, _, _ = oracle.lookup(c.depthmap, pts[chk])
+    np.testing.assert_array_equal(dep[chk], d_or)
+    idx = stratified_sample(dep, 4096, 1 << 15, seed=2)
+    sdf_or, dep_or = oracle.query(p, c.depthmap, pts[idx])
+    assert_parity(sdf, dep, sdf_or, dep_or, TOL_BF16, idx=idx)
+    assert sum(st["per_depth"]) + st["n_nonfinite"] == n
+    assert st["per_depth"][0] == 0   # BJ configs have no far leaves
+
+
+@pytest.mark.parametrize("prec,H", [(BF16, 64), (FP32, 32)])
+def test_far_field_and_lod_caps(prec, H):
+    """Eq. 7 depth-0 cached values; LOD cap 1..L (Sec. 3.4) incl. cap = L no-op."""
+    L = 4
+    spec = g.TMlpSpec(L=L, H=H, omega0=30.0, seed=6)
+    p = g.make_weights(spec)
+    dm = _random_voxel_map(3, L, 7, far=True)
+    pts = _pts(3000, 8)
+    tol = TOL_BF16 if prec == BF16 else TOL_FP32
+    with make_ctx(spec, prec) as ctx:
+        for cap in (1, 2, 3, L):
+            sdf, dep = run_engine(ctx, p, dm, pts, cap=cap)
+            sdf_or, dep_or = oracle.query(p, dm, pts, lod_cap=cap)
+            assert_parity(sdf, dep, sdf_or, dep_or, tol)
+    far = dep_or == 0
+    assert far.any()
+    np.testing.assert_array_equal(sdf[far], sdf_or[far].astype(np.float32))
+
+
+def test_octree_descent_and_baked_paths():
+    """Octree level 9 (device descent, no baking) and level 6 (baked dense grid), far-field leaves
+    included; out-of-domain and face points."""
+    L = 6
+    spec = g.TMlpSpec(L=L, H=64, omega0=30.0, seed=9)
+    p = g.make_weights(spec)
+    sph = g.make_spheres(3, n=4)
+    rng = np.random.default_rng(0)
+    pts = np.concatenate([rng.uniform(-1.2, 1.2, (20000, 3)),
+                          -1 + rng.integers(0, 513, (2000, 3)) * (2.0 / 512)]).astype(np.float32)
+    for lev in (6, 9):
+        oc = g.build_octree(sph, lev, g.configs.BANDS_8, L, score_seed=1, far_band=True,
+                            subdivide_factor=0.3)
+        with make_ctx(spec, BF16) as ctx:
+            sdf, dep = run_engine(ctx, p, oc, pts)
+        sdf_or, dep_or = oracle.query(p, oc, pts)
+        assert_parity(sdf, dep, sdf_or, dep_or, TOL_BF16)
+
+
+def test_nonfinite_and_edge_sizes():
+    """NaN/Inf points -> depth 255, sdf NaN; n in {0, 1, 3, 129}; unaligned (4-byte) point buffer."""
+    import torch
+    L = 3
+    spec = g.TMlpSpec(L=L, H=64, omega0=30.0, seed=10)
+    p = g.make_weights(spec)
+    dm = _random_voxel_map(2, L, 11)
+    base = _pts(200, 12)
+    base[5] = [np.nan, 0, 0]
+    base[17] = [0, np.inf, 0]
+    base[18] = [0, 0, -np.inf]
+    with make_ctx(spec, BF16) as ctx:
+        ctx.sand_load_weights(g.pack_blob(p))
+        ctx.sand_load_depthmap(dm)
+        for n in (0, 1, 3, 129, 200):
+            pts = base[:n]
+            sdf_or, dep_or = oracle.query(p, dm, pts)
+            sdf, dep = run_engine(ctx, p, dm, pts) if n else (np.zeros(0, np.float32), np.zeros(0, np.uint8))
+            if n:
+                assert_parity(sdf, dep, sdf_or, dep_or, TOL_BF16)
+        # unaligned: points start 1 float into the buffer (4-byte but not 16-byte aligned)
+        flat = torch.from_numpy(np.concatenate([[0.0], base.ravel()]).astype(np.float32)).cuda()
+        sdf_t = torch.empty(200, dtype=torch.float32, device="cuda")
+        dep_t = torch.empty(201, dtype=torch.uint8, device="cuda")
+        ctx.sand_set_stream(torch.cuda.current_stream().cuda_stream)
+        ctx.sand_query(flat.data_ptr() + 4, 200, sdf_t.data_ptr(), dep_t.data_ptr() + 1)
+        torch.cuda.synchronize()
+        sdf_or, dep_or = oracle.query(p, dm, base)
+        assert_parity(sdf_t.cpu().numpy(), dep_t.cpu().numpy()[1:], sdf_or, dep_or, TOL_BF16)
+
+
+def test_binning_is_stable_depth_partition():
+    """K2 (S:412 depth-bucketed batching): perm is a permutation of the near points, grouped by
+    depth deepest-first, ascending point order within a depth (stable)."""
+    L = 6
+    spec = g.TMlpSpec(L=L, H=64, omega0=30.0, seed=12)
+    p = g.make_weights(spec)
+    dm = _random_voxel_map(3, L, 13, far=True)
+    pts = _pts(50001, 14)
+    with make_ctx(spec, BF16) as ctx:
+        _, dep = run_engine(ctx, p, dm, pts)
+        perm = ctx.sand_debug_perm()
+    _, dep_or = oracle.query(p, dm, pts)
+    expect = np.concatenate([np.nonzero(dep_or == d)[0] for d in range(L, 0, -1)])
+    np.testing.assert_array_equal(perm, expect.astype(np.uint32))
+
+
+def test_determinism_and_host_e2e():
+    """Two runs bit-identical; sand_query_host (chunked, pinned host buffers) equals sand_query."""
+    import torch
+    c = g.make_config("C1")
+    p = c.params()
+    pts = c.points_fn(0, 64)   # first 64 z-planes of the 256^3 grid
+    with make_ctx(c.spec, BF16) as ctx:
+        s1, d1 = run_engine(ctx, p, c.depthmap, pts)
+        s2, d2 = run_engine(ctx, p, c.depthmap, pts)
+        np.testing.assert_array_equal(s1, s2)
+        np.testing.assert_array_equal(d1, d2)
+        n = pts.shape[0]
+        hp = torch.from_numpy(pts).pin_memory()
+        hs = torch.empty(n, dtype=torch.float32).pin_memory()
+        hd = torch.empty(n, dtype=torch.uint8).pin_memory()
+        ctx.sand_query_host(hp.data_ptr(), n, hs.data_ptr(), hd.data_ptr(), chunk_points=1 << 20)
+        np.testing.assert_array_equal(hs.numpy(), s1)
+        np.testing.assert_array_equal(hd.numpy(), d1)
+
+
+def test_all_max_depth_equals_full_depth():
+    """BJ oracle check 2 on the GPU: an all-L map == uniform full-depth evaluation (query_full)."""
+    L = 8
+    spec = g.TMlpSpec(L=L, H=256, omega0=30.0, seed=15)
+    p = g.make_weights(spec)
+    dm = g.VoxelMap(1, np.full(8, L, np.uint8), None)
+    pts = _pts(20000, 16)
+    with make_ctx(spec, BF16) as ctx:
+        sdf, dep = run_engine(ctx, p, dm, pts)
+    assert (dep == L).all()
+    full = oracle.query_full(p, pts)
+    assert np.abs(sdf - full).max() <= TOL_BF16
