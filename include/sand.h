@@ -139,9 +139,13 @@ typedef struct {
   double flops_exec;              /* executed H x H FLOPs: sum_p (d_p - 1) * 2 H^2               */
   double flops_ns;                /* north-star formula: sum_p d_p * 2 H^2                        */
   float ms_lookup, ms_bin, ms_mlp, ms_total;  /* CUDA-event times of the last sand_query         */
+  int64_t queries;                /* sand_query calls since the previous sand_get_stats (<= 1024) */
+  double ms_lookup_sum, ms_bin_sum, ms_mlp_sum, ms_total_sum; /* summed over those queries       */
 } sand_stats;
 
-/* Statistics of the last sand_query on ctx.  Synchronizes ctx's stream. */
+/* Statistics of the last sand_query on ctx (counts) and per-stage CUDA-event times of every query
+ * since the previous sand_get_stats (sums), recorded on ctx's stream without synchronising inside
+ * sand_query.  Resets the time sums.  Synchronizes ctx's stream. */
 int sand_get_stats(sand_ctx* ctx, sand_stats* out);
 
 /* Diagnostic: copy the depth-binning permutation of the last query to host_perm[0 .. min(cap,

@@ -7,8 +7,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libsand.so")
-SOURCES = ["sand_api.cu", "lookup.cu", "tmlp_simt.cu", "tmlp_tc.cu"]
-HEADERS = ["ptx.cuh", "sand_internal.h"]
+SOURCES = ["sand_api.cu", "lookup.cu", "tmlp_simt.cu", "tmlp_tc.cu", "tmlp_tc2.cu"]
+HEADERS = ["ptx.cuh", "sand_internal.h", "tmlp_common.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall", "--expt-relaxed-constexpr",

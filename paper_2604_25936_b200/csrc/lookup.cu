@@ -148,7 +148,8 @@ __device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long
 }
 
 __global__ void __launch_bounds__(1024) k_scan(const uint32_t* __restrict__ hist, long long nblk, int L,
-                                               uint32_t* __restrict__ offs, QueryMeta* __restrict__ meta) {
+                                               int tile_rows, uint32_t* __restrict__ offs,
+                                               QueryMeta* __restrict__ meta) {
   __shared__ long long counts[kMaxBins];
   const long long per = (nblk + blockDim.x - 1) / blockDim.x;
   const long long b0 = threadIdx.x * per;
@@ -159,12 +160,8 @@ __global__ void __launch_bounds__(1024) k_scan(const uint32_t* __restrict__ hist
     unsigned long long s = 0;
     for (long long b = b0; b < b1; ++b) s += hist[(long long)bin * nblk + b];
     unsigned long long tot;
-    const unsigned long long ex = block_excl_scan(s, &tot);
-    if (bin >= 1 && bin <= L) {
-      // (recomputed below in deepest-first order)
-    }
+    (void)block_excl_scan(s, &tot);
     if (threadIdx.x == 0) counts[bin] = (long long)tot;
-    (void)ex;
   }
   __syncthreads();
   // deepest-first scatter offsets
@@ -189,10 +186,11 @@ __global__ void __launch_bounds__(1024) k_scan(const uint32_t* __restrict__ hist
     meta->start[0] = 0;
     for (int d = L; d >= 1; --d) {
       meta->tile_begin[d] = tb;
-      tb += (counts[d] + kTileM - 1) / kTileM;
+      tb += (counts[d] + tile_rows - 1) / tile_rows;
       meta->tile_end[d] = tb;
     }
     meta->total_tiles = tb;
+    meta->tile_rows = tile_rows;
   }
 }
 
@@ -303,9 +301,9 @@ cudaError_t launch_lookup(const float* pts, long long n, const LookupParams& lp,
   return cudaGetLastError();
 }
 
-cudaError_t launch_scan(const uint32_t* hist, long long nblk, int L, uint32_t* offs, QueryMeta* meta,
-                        cudaStream_t st) {
-  k_scan<<<1, 1024, 0, st>>>(hist, nblk, L, offs, meta);
+cudaError_t launch_scan(const uint32_t* hist, long long nblk, int L, int tile_rows, uint32_t* offs,
+                        QueryMeta* meta, cudaStream_t st) {
+  k_scan<<<1, 1024, 0, st>>>(hist, nblk, L, tile_rows, offs, meta);
   return cudaGetLastError();
 }
 

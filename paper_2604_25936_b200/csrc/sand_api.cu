@@ -7,9 +7,11 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -25,6 +27,7 @@ struct sand_ctx {
   int num_sms = 0;
   cudaStream_t stream = nullptr;
   int lod_cap = 0;
+  bool use_pair = true;   // CTA-pair tcgen05 kernel where available (env SAND_PAIR=0 disables)
   std::string err;
   // weights
   bool have_w = false;
@@ -46,8 +49,11 @@ struct sand_ctx {
   uint32_t* d_offs = nullptr;
   uint32_t* d_perm = nullptr;
   QueryMeta* d_meta = nullptr;
-  // timing
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  // timing: one event quad per query since the last sand_get_stats (grown on demand; never
+  // synchronised inside sand_query, so back-to-back queries stay asynchronous)
+  std::vector<std::array<cudaEvent_t, 4>> evq;
+  size_t nq = 0;      // quads used since the last sand_get_stats
+  size_t last_q = 0;  // quad of the last query
   bool have_stats = false;
   long long last_n = 0;
   // host-buffer pipeline
@@ -126,10 +132,9 @@ extern "C" int sand_create(const sand_config* cfg, sand_ctx** out) {
     return bail(SAND_ERR_UNSUPPORTED);
   }
   ctx->num_sms = prop.multiProcessorCount;
+  if (const char* ev = getenv("SAND_PAIR")) ctx->use_pair = std::atoi(ev) != 0;
   cudaError_t e = prepare_tmlp_kernels(cfg->L, cfg->H, cfg->tail, cfg->prec);
   if (e != cudaSuccess) { fail(ctx, SAND_ERR_CUDA, "kernel attribute setup: %s", cudaGetErrorString(e)); return bail(SAND_ERR_CUDA); }
-  for (auto& v : ctx->ev)
-    if (cudaEventCreate(&v) != cudaSuccess) { fail(ctx, SAND_ERR_CUDA, "cudaEventCreate failed"); return bail(SAND_ERR_CUDA); }
   *out = ctx;
   return SAND_OK;
 }
@@ -170,8 +175,9 @@ extern "C" int sand_destroy(sand_ctx* ctx) {
   free_depthmap(ctx);
   free_weights(ctx);
   free_hostpipe(ctx);
-  for (auto& v : ctx->ev)
-    if (v) cudaEventDestroy(v);
+  for (auto& q : ctx->evq)
+    for (auto& v : q)
+      if (v) cudaEventDestroy(v);
   delete ctx;
   return SAND_OK;
 }
@@ -214,12 +220,13 @@ extern "C" int sand_load_weights(sand_ctx* ctx, const float* blob, size_t n_floa
   // ---- FP32 tables (layout documented in sand_internal.h MlpDev)
   MlpDev m{};
   m.L = L; m.H = H; m.tail = tail; m.omega0 = w0;
+  // every per-layer row starts on a 16-byte boundary (H % 16 == 0): float4 table loads
   m.off_w1 = 0;
   m.off_bias = 4ll * H;
   m.off_a = m.off_bias + (long long)(L - 1) * H;
-  m.off_c = m.off_a + (long long)L * H;
-  m.off_a1 = m.off_c + L;
-  m.off_c1 = m.off_a1 + (tail == SAND_TAIL_MULT ? (long long)(L - 1) * H : 0);
+  m.off_a1 = m.off_a + (long long)L * H;
+  m.off_c = m.off_a1 + (tail == SAND_TAIL_MULT ? (long long)(L - 1) * H : 0);
+  m.off_c1 = m.off_c + L;
   long long ntab = m.off_c1 + (tail == SAND_TAIL_MULT ? (L - 1) : 0);
   ntab = (ntab + 3) & ~3ll;
   m.tables_floats = ntab;
@@ -425,17 +432,27 @@ extern "C" int sand_query(sand_ctx* ctx, const float* d_points, int64_t n, float
   LookupParams lp = ctx->lp;
   lp.cap = ctx->lod_cap;
   cudaStream_t st = ctx->stream;
-  CU(cudaEventRecord(ctx->ev[0], st));
+  if (ctx->nq == 1024) ctx->nq = 0;  // bounded: sums cover at most the last 1024 queries
+  if (ctx->nq == ctx->evq.size()) {
+    std::array<cudaEvent_t, 4> q{};
+    for (auto& v : q) CU(cudaEventCreate(&v));
+    ctx->evq.push_back(q);
+  }
+  const size_t qi = ctx->nq++;
+  cudaEvent_t* ev = ctx->evq[qi].data();
+  CU(cudaEventRecord(ev[0], st));
   CU(launch_lookup(d_points, n, lp, d_depth, d_sdf, ctx->d_hist, nblk, st));
-  CU(cudaEventRecord(ctx->ev[1], st));
-  CU(launch_scan(ctx->d_hist, nblk, ctx->cfg.L, ctx->d_offs, ctx->d_meta, st));
+  CU(cudaEventRecord(ev[1], st));
+  CU(launch_scan(ctx->d_hist, nblk, ctx->cfg.L, tmlp_tile_rows(ctx->cfg.H, ctx->cfg.prec, ctx->use_pair), ctx->d_offs,
+                 ctx->d_meta, st));
   CU(launch_scatter(d_depth, n, ctx->cfg.L, ctx->d_offs, ctx->d_perm, nblk, st));
-  CU(cudaEventRecord(ctx->ev[2], st));
+  CU(cudaEventRecord(ev[2], st));
   if (ctx->cfg.prec == SAND_FP32)
     CU(launch_tmlp_simt(ctx->mlp, d_points, ctx->d_perm, ctx->d_meta, d_sdf, ctx->num_sms, st));
   else
-    CU(launch_tmlp_tc(ctx->mlp, d_points, ctx->d_perm, ctx->d_meta, d_sdf, ctx->num_sms, st));
-  CU(cudaEventRecord(ctx->ev[3], st));
+    CU(launch_tmlp_tc(ctx->mlp, d_points, ctx->d_perm, ctx->d_meta, d_sdf, ctx->num_sms, st, ctx->use_pair));
+  CU(cudaEventRecord(ev[3], st));
+  ctx->last_q = qi;
   ctx->have_stats = true;
   ctx->last_n = n;
   return SAND_OK;
@@ -531,10 +548,18 @@ extern "C" int sand_get_stats(sand_ctx* ctx, sand_stats* out) {
     }
   }
   out->tiles = m.total_tiles;
-  CU(cudaEventElapsedTime(&out->ms_lookup, ctx->ev[0], ctx->ev[1]));
-  CU(cudaEventElapsedTime(&out->ms_bin, ctx->ev[1], ctx->ev[2]));
-  CU(cudaEventElapsedTime(&out->ms_mlp, ctx->ev[2], ctx->ev[3]));
-  CU(cudaEventElapsedTime(&out->ms_total, ctx->ev[0], ctx->ev[3]));
+  for (size_t i = 0; i < ctx->nq; ++i) {
+    cudaEvent_t* ev = ctx->evq[i].data();
+    float a, b, c, t;
+    CU(cudaEventElapsedTime(&a, ev[0], ev[1]));
+    CU(cudaEventElapsedTime(&b, ev[1], ev[2]));
+    CU(cudaEventElapsedTime(&c, ev[2], ev[3]));
+    CU(cudaEventElapsedTime(&t, ev[0], ev[3]));
+    out->ms_lookup_sum += a; out->ms_bin_sum += b; out->ms_mlp_sum += c; out->ms_total_sum += t;
+    if (i == ctx->last_q) { out->ms_lookup = a; out->ms_bin = b; out->ms_mlp = c; out->ms_total = t; }
+  }
+  out->queries = (int64_t)ctx->nq;
+  ctx->nq = 0;
   return SAND_OK;
 }
 

@@ -20,6 +20,7 @@ struct QueryMeta {
   long long tile_begin[kMaxBins];
   long long tile_end[kMaxBins];
   long long total_tiles;
+  long long tile_rows;            // rows per tile (128: 1-CTA / SIMT kernels, 256: CTA-pair kernel)
 };
 
 struct LookupParams {
@@ -37,8 +38,8 @@ struct LookupParams {
 // Host-side launchers (lookup.cu)
 cudaError_t launch_lookup(const float* pts, long long n, const LookupParams& lp, uint8_t* out_depth,
                           float* out_sdf, uint32_t* hist, long long nblk, cudaStream_t st);
-cudaError_t launch_scan(const uint32_t* hist, long long nblk, int L, uint32_t* offs, QueryMeta* meta,
-                        cudaStream_t st);
+cudaError_t launch_scan(const uint32_t* hist, long long nblk, int L, int tile_rows, uint32_t* offs,
+                        QueryMeta* meta, cudaStream_t st);
 cudaError_t launch_scatter(const uint8_t* depth, long long n, int L, const uint32_t* offs, uint32_t* perm,
                            long long nblk, cudaStream_t st);
 cudaError_t launch_bake_octree(const uint32_t* nodes, const uint8_t* leaf_depth, const float* leaf_far,
@@ -54,18 +55,20 @@ struct MlpDev {
   const void* w_image;
   // FP32 tables (both paths):
   //   w1: float4[H] = (w0*W1[j][0], w0*W1[j][1], w0*W1[j][2], w0*b1[j])
-  //   bias: [L-1][H] = w0 * b_i (i >= 2);  a: [L][H] tail (a_i or a_i0); c: [L]
-  //   a1: [L-1][H] (MULT, i >= 2) ; c1: [L-1]
+  //   bias: [L-1][H] = w0 * b_i (i >= 2);  a: [L][H] tail (a_i or a_i0);
+  //   a1: [L-1][H] (MULT, i >= 2);  c: [L];  c1: [L-1] (MULT)   -- in this order
   const float* tables;
   long long off_w1, off_bias, off_a, off_c, off_a1, off_c1, tables_floats;
 };
 
 cudaError_t launch_tmlp_simt(const MlpDev& m, const float* pts, const uint32_t* perm, const QueryMeta* meta,
                              float* out_sdf, int num_sms, cudaStream_t st);
+// use_pair: CTA-pair (cta_group::2, 256-row tiles) kernel where available (H in {128, 256})
 cudaError_t launch_tmlp_tc(const MlpDev& m, const float* pts, const uint32_t* perm, const QueryMeta* meta,
-                           float* out_sdf, int num_sms, cudaStream_t st);
+                           float* out_sdf, int num_sms, cudaStream_t st, bool use_pair);
 // configuration query: dynamic smem bytes for the tc kernel, 0 if unsupported
 size_t tc_smem_bytes(int L, int H, int tail);
+int tmlp_tile_rows(int H, int prec, bool use_pair);   // tile size the selected T-MLP kernel consumes
 bool tc_supported_H(int H);
 bool simt_supported_H(int H);
 size_t simt_smem_bytes(int L, int H, int tail);

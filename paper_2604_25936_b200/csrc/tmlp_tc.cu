@@ -22,6 +22,7 @@
 
 #include "ptx.cuh"
 #include "sand_internal.h"
+#include "tmlp_common.cuh"
 
 namespace sand {
 
@@ -49,57 +50,6 @@ struct TcParams {
   const QueryMeta* meta;
   float* out;
   int nst;  // weight ring stages
-};
-
-struct SlotState {
-  long long t;
-  int i, d, l, done;
-};
-
-__device__ __forceinline__ int tile_depth(long long t, const long long* tile_end, int L) {
-  for (int d = L; d >= 1; --d)
-    if (t < tile_end[d]) return d;
-  return 0;
-}
-
-template <int NSLOT>
-struct JobGen {
-  SlotState S[NSLOT];
-  int cur;
-  long long T;
-  const long long* tile_end;
-  int L;
-  __device__ __forceinline__ void set_tile(int s) {
-    const long long t = (long long)blockIdx.x + (long long)gridDim.x * ((long long)NSLOT * S[s].i + s);
-    S[s].t = t;
-    if (t >= T) {
-      S[s].done = 1;
-    } else {
-      S[s].d = tile_depth(t, tile_end, L);
-      S[s].l = 2;
-    }
-  }
-  __device__ __forceinline__ void init(long long T_, const long long* te, int L_) {
-    T = T_; tile_end = te; L = L_; cur = 0;
-#pragma unroll
-    for (int s = 0; s < NSLOT; ++s) { S[s].i = 0; S[s].done = 0; set_tile(s); }
-  }
-  // Next MMA job (slot, layer) in round-robin order; tiles without remaining H x H layers (depth 1
-  // or finished) are skipped.  Producer and MMA warps run identical copies of this generator.
-  __device__ __forceinline__ bool next(int& s_out, int& l_out) {
-#pragma unroll 1
-    for (int tries = 0; tries < NSLOT; ++tries) {
-      const int s = cur;
-      cur = (cur + 1 == NSLOT) ? 0 : cur + 1;
-      while (!S[s].done && S[s].l > S[s].d) { S[s].i++; set_tile(s); }
-      if (!S[s].done) {
-        s_out = s;
-        l_out = S[s].l++;
-        return true;
-      }
-    }
-    return false;
-  }
 };
 
 template <int H, int TAIL>
@@ -158,7 +108,7 @@ __global__ void __launch_bounds__(TcShape<H>::THREADS, 1) k_tmlp_tc(const TcPara
     // =========================== weight producer ===========================
     if (lane == 0) {
       JobGen<NSLOT> gen;
-      gen.init(T, s_tile_end, L);
+      gen.init(T, s_tile_end, L, blockIdx.x, gridDim.x);
       int s, l, st = 0;
       uint32_t ph = 0;
       const uint8_t* img = reinterpret_cast<const uint8_t*>(p.m.w_image);
@@ -176,7 +126,7 @@ __global__ void __launch_bounds__(TcShape<H>::THREADS, 1) k_tmlp_tc(const TcPara
     // =========================== MMA issuer ===========================
     if (lane == 0) {
       JobGen<NSLOT> gen;
-      gen.init(T, s_tile_end, L);
+      gen.init(T, s_tile_end, L, blockIdx.x, gridDim.x);
       constexpr uint32_t ID0 = idesc_bf16(128, C::N0);
       constexpr uint32_t ID1 = idesc_bf16(128, C::N1 > 0 ? C::N1 : 16);
       int s, l, st = 0;
@@ -228,19 +178,27 @@ __global__ void __launch_bounds__(TcShape<H>::THREADS, 1) k_tmlp_tc(const TcPara
       const uint32_t idx = p.perm[valid ? r0 + row : r0];
       const float px = p.pts[3ll * idx], py = p.pts[3ll * idx + 1], pz = p.pts[3ll * idx + 2];
       // ---------------- layer 1 (FP32 SIMT, K = 3) + tail 1
-      float y = tab[p.m.off_c];
+      float2 acc = make_float2(tab[p.m.off_c], 0.0f);
       {
-        const float* a = tab + p.m.off_a;
-#pragma unroll 2
+        const float4* a4p = reinterpret_cast<const float4*>(tab + p.m.off_a);
+        const float2 X = make_float2(px, px), Y = make_float2(py, py), Z = make_float2(pz, pz);
+#pragma unroll 1
         for (int u = 0; u < H / 8; ++u) {
           float hv[8];
 #pragma unroll
-          for (int jj = 0; jj < 8; ++jj) {
-            const int j = 8 * u + jj;
-            const float4 w = w1[j];
-            hv[jj] = __sinf(fmaf(w.z, pz, fmaf(w.y, py, fmaf(w.x, px, w.w))));
-            y = fmaf(a[j], hv[jj], y);
+          for (int jj = 0; jj < 8; jj += 2) {
+            const float4 wa = w1[8 * u + jj], wb = w1[8 * u + jj + 1];
+            float2 z = __ffma2_rn(make_float2(wa.x, wb.x), X, make_float2(wa.w, wb.w));
+            z = __ffma2_rn(make_float2(wa.y, wb.y), Y, z);
+            z = __ffma2_rn(make_float2(wa.z, wb.z), Z, z);
+            hv[jj] = __sinf(z.x);
+            hv[jj + 1] = __sinf(z.y);
           }
+          const float4 a0 = a4p[2 * u], a1v = a4p[2 * u + 1];
+          acc = __ffma2_rn(make_float2(a0.x, a0.y), make_float2(hv[0], hv[1]), acc);
+          acc = __ffma2_rn(make_float2(a0.z, a0.w), make_float2(hv[2], hv[3]), acc);
+          acc = __ffma2_rn(make_float2(a1v.x, a1v.y), make_float2(hv[4], hv[5]), acc);
+          acc = __ffma2_rn(make_float2(a1v.z, a1v.w), make_float2(hv[6], hv[7]), acc);
           if (d >= 2) {
             const uint32_t addr = a_row + (u >> 3) * C::A_CHUNK + ((((uint32_t)u & 7u) ^ swz) << 4);
             asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(pack_bf16x2(hv[0], hv[1])),
@@ -250,6 +208,7 @@ __global__ void __launch_bounds__(TcShape<H>::THREADS, 1) k_tmlp_tc(const TcPara
           }
         }
       }
+      float y = acc.x + acc.y;
       if (d >= 2) {
         fence_proxy_async_smem();
         tc_fence_before();
@@ -261,44 +220,37 @@ __global__ void __launch_bounds__(TcShape<H>::THREADS, 1) k_tmlp_tc(const TcPara
         mbar_wait(b_accfull + 8 * s, pe);
         pe ^= 1u;
         tc_fence_after();
-        const bool last = (l == d);
+        const bool store = (l != d);
         const float* bias = tab + p.m.off_bias + (long long)(l - 2) * H;
         const float* a = tab + p.m.off_a + (long long)(l - 1) * H;
         const float* a1 = tab + p.m.off_a1 + (long long)(l - 2) * H;
-        float s0 = 0.0f, s1 = 0.0f;
+        float2 s0 = make_float2(0.0f, 0.0f), s1 = make_float2(0.0f, 0.0f);
+        constexpr int NC = H / 32;
+        uint32_t ra[32], rb[32];
+        tmem_ld32(tm_row, ra);
 #pragma unroll 1
-        for (int c = 0; c < H / 16; ++c) {
-          uint32_t r[16];
-          tmem_ld16(tm_row + 16 * c, r);
-          tmem_wait_ld();
-          float hv[16];
-#pragma unroll
-          for (int jj = 0; jj < 16; ++jj) {
-            const int j = 16 * c + jj;
-            hv[jj] = __sinf(fmaf(__uint_as_float(r[jj]), w0, bias[j]));
-            s0 = fmaf(a[j], hv[jj], s0);
-            if (TAIL == SAND_TAIL_MULT) s1 = fmaf(a1[j], hv[jj], s1);
-          }
-          if (!last) {
-#pragma unroll
-            for (int h2 = 0; h2 < 2; ++h2) {
-              const uint32_t u = 2 * c + h2;
-              const uint32_t addr = a_row + (u >> 3) * C::A_CHUNK + (((u & 7u) ^ swz) << 4);
-              asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr),
-                           "r"(pack_bf16x2(hv[8 * h2 + 0], hv[8 * h2 + 1])),
-                           "r"(pack_bf16x2(hv[8 * h2 + 2], hv[8 * h2 + 3])),
-                           "r"(pack_bf16x2(hv[8 * h2 + 4], hv[8 * h2 + 5])),
-                           "r"(pack_bf16x2(hv[8 * h2 + 6], hv[8 * h2 + 7]))
-                           : "memory");
-            }
+        for (int c = 0; c < NC; c += 2) {
+          tmem_wait_ld_dep(ra);
+          if (c + 1 < NC) tmem_ld32(tm_row + 32 * (c + 1), rb);
+          epi_cols<32, TAIL>(ra, 32 * c, bias, a, a1, w0, s0, s1, store, a_row, swz, C::A_CHUNK);
+          if (c + 1 < NC) {
+            tmem_wait_ld_dep(rb);
+            if (c + 2 < NC) tmem_ld32(tm_row + 32 * (c + 2), ra);
+            epi_cols<32, TAIL>(rb, 32 * (c + 1), bias, a, a1, w0, s0, s1, store, a_row, swz, C::A_CHUNK);
           }
         }
+        if (H % 32) {
+          uint32_t rc[16];
+          tmem_ld16(tm_row + 32 * NC, rc);
+          tmem_wait_ld_dep(rc);
+          epi_cols<16, TAIL>(rc, 32 * NC, bias, a, a1, w0, s0, s1, store, a_row, swz, C::A_CHUNK);
+        }
         if (TAIL == SAND_TAIL_MULT)
-          y += (s0 + tab[p.m.off_c + (l - 1)]) * (s1 + tab[p.m.off_c1 + (l - 2)]);
+          y += (s0.x + s0.y + tab[p.m.off_c + (l - 1)]) * (s1.x + s1.y + tab[p.m.off_c1 + (l - 2)]);
         else
-          y += s0 + tab[p.m.off_c + (l - 1)];
+          y += s0.x + s0.y + tab[p.m.off_c + (l - 1)];
         tc_fence_before();
-        if (!last) {
+        if (store) {
           fence_proxy_async_smem();
           mbar_arrive(b_afull + 8 * s);
         }
@@ -364,8 +316,19 @@ static cudaError_t prep_tc_t() {
   return cudaFuncSetAttribute(k_tmlp_tc<H, TAIL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
 }
 
+cudaError_t launch_tmlp_tc2(const MlpDev& m, const float* pts, const uint32_t* perm, const QueryMeta* meta,
+                            float* out, int num_sms, cudaStream_t st);
+cudaError_t prepare_tc2(int H, int tail);
+
+bool tc2_available(int H) { return H == 128 || H == 256; }
+
+int tmlp_tile_rows(int H, int prec, bool use_pair) {
+  return (prec == SAND_BF16 && use_pair && tc2_available(H)) ? 256 : kTileM;
+}
+
 cudaError_t launch_tmlp_tc(const MlpDev& m, const float* pts, const uint32_t* perm, const QueryMeta* meta,
-                           float* out, int num_sms, cudaStream_t st) {
+                           float* out, int num_sms, cudaStream_t st, bool use_pair) {
+  if (use_pair && tc2_available(m.H)) return launch_tmlp_tc2(m, pts, perm, meta, out, num_sms, st);
   const bool mult = m.tail == SAND_TAIL_MULT;
 #define SAND_TC_CASE(HH)                                                                     \
   case HH:                                                                                   \
@@ -386,6 +349,10 @@ cudaError_t prepare_simt(int L, int H, int tail);
 cudaError_t prepare_tmlp_kernels(int L, int H, int tail, int prec) {
   if (prec == SAND_FP32) return prepare_simt(L, H, tail);
   const bool mult = tail == SAND_TAIL_MULT;
+  if (tc2_available(H)) {
+    const cudaError_t e = prepare_tc2(H, tail);
+    if (e != cudaSuccess) return e;
+  }
   switch (H) {
     case 64: return mult ? prep_tc_t<64, 1>() : prep_tc_t<64, 0>();
     case 128: return mult ? prep_tc_t<128, 1>() : prep_tc_t<128, 0>();

@@ -43,7 +43,9 @@ class sand_stats(ctypes.Structure):
                 ("per_depth", ctypes.c_int64 * (SAND_MAX_L + 1)), ("tiles", ctypes.c_int64),
                 ("flops_exec", ctypes.c_double), ("flops_ns", ctypes.c_double),
                 ("ms_lookup", ctypes.c_float), ("ms_bin", ctypes.c_float),
-                ("ms_mlp", ctypes.c_float), ("ms_total", ctypes.c_float)]
+                ("ms_mlp", ctypes.c_float), ("ms_total", ctypes.c_float),
+                ("queries", ctypes.c_int64), ("ms_lookup_sum", ctypes.c_double), ("ms_bin_sum", ctypes.c_double),
+                ("ms_mlp_sum", ctypes.c_double), ("ms_total_sum", ctypes.c_double)]
 
 
 EXPORTS = ("sand_create", "sand_destroy", "sand_load_weights", "sand_load_depthmap", "sand_set_stream",
@@ -169,7 +171,8 @@ class SandContext:
         L = self.cfg.L
         return dict(n=s.n, n_nonfinite=s.n_nonfinite, per_depth=list(s.per_depth[:L + 1]), tiles=s.tiles,
                     flops_exec=s.flops_exec, flops_ns=s.flops_ns, ms_lookup=s.ms_lookup, ms_bin=s.ms_bin,
-                    ms_mlp=s.ms_mlp, ms_total=s.ms_total)
+                    ms_mlp=s.ms_mlp, ms_total=s.ms_total, queries=s.queries, ms_lookup_sum=s.ms_lookup_sum,
+                    ms_bin_sum=s.ms_bin_sum, ms_mlp_sum=s.ms_mlp_sum, ms_total_sum=s.ms_total_sum)
 
     def sand_debug_perm(self):
         nb = ctypes.c_int64()
