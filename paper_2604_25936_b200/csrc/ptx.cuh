@@ -71,8 +71,14 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
   return r;
 }
+// Arrive on an mbarrier of another CTA of the cluster.  Default (.release.cta) semantics on purpose: a
+// .release.cluster arrive compiles to MEMBAR.ALL.GPU, which drains every outstanding global load/store
+// of the thread (the epilogue's point prefetches, output stores) before the arrive.  The data this
+// arrive publishes is either written by the async proxy (TMA) or made visible to it with
+// fence.proxy.async by the writing threads before a warp/CTA barrier, so cluster-scope release of the
+// generic proxy is not needed.
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");

@@ -32,6 +32,7 @@ struct sand_ctx {
   // weights
   bool have_w = false;
   float* d_tables = nullptr;
+  float* d_pair_tables = nullptr;
   void* d_wimage = nullptr;
   float* d_whidden = nullptr;
   MlpDev mlp{};
@@ -148,7 +149,7 @@ static void free_depthmap(sand_ctx* c) {
   c->have_dm = false;
 }
 static void free_weights(sand_ctx* c) {
-  dfree(c->d_tables); dfree(c->d_wimage); dfree(c->d_whidden);
+  dfree(c->d_tables); dfree(c->d_pair_tables); dfree(c->d_wimage); dfree(c->d_whidden);
   c->have_w = false;
 }
 static void free_hostpipe(sand_ctx* c) {
@@ -252,6 +253,51 @@ extern "C" int sand_load_weights(sand_ctx* ctx, const float* blob, size_t n_floa
   CU(cudaMalloc(&ctx->d_tables, sizeof(float) * ntab));
   CU(cudaMemcpy(ctx->d_tables, tab.data(), sizeof(float) * ntab, cudaMemcpyHostToDevice));
   m.tables = ctx->d_tables;
+  if (ctx->cfg.prec == SAND_BF16 && tc2_available(H)) {
+    // CTA-pair kernel tables (layout in sand_internal.h MlpDev): per-column scale by sine path
+    const int np = tc2_npoly();
+    const double kInvPi = 0.31830988618379067;
+    auto scale = [&](int j) { return (j % 16) < np ? (double)w0 * kInvPi : (double)w0; };
+    auto al4 = [](long long v) { return (v + 3) & ~3ll; };
+    m.pt_npoly = np;
+    m.pt_off_l1 = 0;
+    m.pt_off_bias = al4(m.pt_off_l1 + 4ll * H);
+    m.pt_off_a = al4(m.pt_off_bias + (long long)(L - 1) * H);
+    m.pt_off_a1 = al4(m.pt_off_a + (long long)L * H);
+    m.pt_off_c = al4(m.pt_off_a1 + (tail == SAND_TAIL_MULT ? (long long)(L - 1) * H : 0));
+    m.pt_off_c1 = al4(m.pt_off_c + L);
+    m.pt_off_csum = al4(m.pt_off_c1 + L);
+    m.pt_floats = al4(m.pt_off_csum + L + 1);
+    std::vector<float> pt((size_t)m.pt_floats, 0.f);
+    for (int j = 0; j < H; j += 2) {
+      float* e = &pt[m.pt_off_l1 + 4 * (size_t)j];
+      for (int h = 0; h < 2; ++h) {
+        const double sc = scale(j + h);
+        e[0 + h] = (float)(sc * W[0][3 * (j + h) + 0]);
+        e[2 + h] = (float)(sc * W[0][3 * (j + h) + 1]);
+        e[4 + h] = (float)(sc * W[0][3 * (j + h) + 2]);
+        e[6 + h] = (float)(sc * b[0][j + h]);
+      }
+    }
+    for (int i = 1; i < L; ++i)
+      for (int j = 0; j < H; ++j) pt[m.pt_off_bias + (size_t)(i - 1) * H + j] = (float)(scale(j) * b[i][j]);
+    for (int i = 0; i < L; ++i) {
+      std::memcpy(&pt[m.pt_off_a + (size_t)i * H], a[i], sizeof(float) * H);
+      pt[m.pt_off_c + i] = c[i];
+      pt[m.pt_off_c1 + i] = c1[i];
+    }
+    if (tail == SAND_TAIL_MULT)
+      for (int i = 1; i < L; ++i) std::memcpy(&pt[m.pt_off_a1 + (size_t)(i - 1) * H], a1[i], sizeof(float) * H);
+    double cs = 0.0;
+    pt[m.pt_off_csum] = 0.f;
+    for (int d = 1; d <= L; ++d) {
+      cs += (tail == SAND_TAIL_LINEAR || d == 1) ? c[d - 1] : 0.0;
+      pt[m.pt_off_csum + d] = (float)cs;
+    }
+    CU(cudaMalloc(&ctx->d_pair_tables, sizeof(float) * pt.size()));
+    CU(cudaMemcpy(ctx->d_pair_tables, pt.data(), sizeof(float) * pt.size(), cudaMemcpyHostToDevice));
+    m.pair_tables = ctx->d_pair_tables;
+  }
   if (L >= 2) {
     if (ctx->cfg.prec == SAND_FP32) {
       std::vector<float> wh((size_t)(L - 1) * H * H);

@@ -59,7 +59,18 @@ struct MlpDev {
   //   a1: [L-1][H] (MULT, i >= 2);  c: [L];  c1: [L-1] (MULT)   -- in this order
   const float* tables;
   long long off_w1, off_bias, off_a, off_c, off_a1, off_c1, tables_floats;
+  // CTA-pair kernel tables (tmlp_tc2.cu), pre-scaled per column for its sine path: of every 16 columns
+  // the first pt_npoly use the FMA-pipe polynomial (scale w0/pi), the rest MUFU.SIN (scale w0):
+  //   l1  : [H/2][8] = per column pair (wx0, wx1, wy0, wy1, wz0, wz1, b0, b1) * scale(col)
+  //   bias: [L-1][H] = scale(col) * b_i (i >= 2);  a: [L][H];  a1: [L-1][H] (MULT)
+  //   c   : [L] tail biases (MULT: c_i0);  c1: [L] (MULT: c_i1 at index i-1, i >= 2)
+  //   csum: [L+1] LINEAR: sum_{i <= d} c_i;  MULT: c_1 (d >= 1)
+  const float* pair_tables;
+  long long pt_floats, pt_off_l1, pt_off_bias, pt_off_a, pt_off_a1, pt_off_c, pt_off_c1, pt_off_csum;
+  int pt_npoly;
 };
+
+constexpr int kPairPolyDefault = 4;   // polynomial-sine columns per 16 in the CTA-pair kernel
 
 cudaError_t launch_tmlp_simt(const MlpDev& m, const float* pts, const uint32_t* perm, const QueryMeta* meta,
                              float* out_sdf, int num_sms, cudaStream_t st);
@@ -73,5 +84,11 @@ bool tc_supported_H(int H);
 bool simt_supported_H(int H);
 size_t simt_smem_bytes(int L, int H, int tail);
 cudaError_t prepare_tmlp_kernels(int L, int H, int tail, int prec);
+// CTA-pair kernel (tmlp_tc2.cu)
+bool tc2_available(int H);
+int tc2_npoly();   // polynomial share in use (SAND_NPOLY env override: 0, 4, 6, 8)
+cudaError_t launch_tmlp_tc2(const MlpDev& m, const float* pts, const uint32_t* perm, const QueryMeta* meta,
+                            float* out, int num_sms, cudaStream_t st);
+cudaError_t prepare_tc2(int H, int tail);
 
 }  // namespace sand

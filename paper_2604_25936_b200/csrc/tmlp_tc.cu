@@ -316,11 +316,7 @@ static cudaError_t prep_tc_t() {
   return cudaFuncSetAttribute(k_tmlp_tc<H, TAIL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
 }
 
-cudaError_t launch_tmlp_tc2(const MlpDev& m, const float* pts, const uint32_t* perm, const QueryMeta* meta,
-                            float* out, int num_sms, cudaStream_t st);
-cudaError_t prepare_tc2(int H, int tail);
 
-bool tc2_available(int H) { return H == 128 || H == 256; }
 
 int tmlp_tile_rows(int H, int prec, bool use_pair) {
   return (prec == SAND_BF16 && use_pair && tc2_available(H)) ? 256 : kTileM;
