@@ -10,6 +10,8 @@ LIB = os.path.join(HERE, "libsand.so")
 SOURCES = ["sand_api.cu", "lookup.cu", "tmlp_simt.cu", "tmlp_tc.cu", "tmlp_tc2.cu"]
 HEADERS = ["ptx.cuh", "sand_internal.h", "tmlp_common.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+# extra defines for diagnostic builds, e.g. SAND_BUILD_DEFS="-DSAND_HANG_DEBUG" (bounded mbarrier waits)
+EXTRA = os.environ.get("SAND_BUILD_DEFS", "").split()
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall", "--expt-relaxed-constexpr",
          "-I", os.path.join(ROOT, "include")]
@@ -30,7 +32,7 @@ def build(force=False, verbose=True, ptxas_v=False):
     procs = []
     for src in SOURCES:
         obj = os.path.join(CSRC, src.replace(".cu", ".o"))
-        cmd = [NVCC, *FLAGS, "-dc" if False else "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC, *FLAGS, *EXTRA, "-c", os.path.join(CSRC, src), "-o", obj]
         if ptxas_v:
             cmd += ["-Xptxas", "-v"]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))

@@ -27,6 +27,26 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t byt
 // Blocking wait for phase `parity`.  The suspend-time hint lets the hardware park the warp until the
 // phase completes (or the hint expires) instead of spinning: spinning waiters would steal issue
 // slots from the epilogue warps that share their SM sub-partition.
+#ifdef SAND_HANG_DEBUG
+// Debug build: bounded waits.  A wait that spins ~2^26 times records (block, thread, barrier smem
+// address, parity) in g_hang and gives up, so a protocol deadlock surfaces as a report, not a hang.
+__device__ unsigned long long g_hang[4];
+__device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred P1;\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\nselp.u32 %0, 1, 0, P1;\n}\n"
+      : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  for (long long i = 0; i < (1ll << 26); ++i)
+    if (mbar_try(bar, parity)) return;
+  if (atomicCAS(&g_hang[0], 0ull, 1ull) == 0ull) {
+    g_hang[1] = ((unsigned long long)blockIdx.x << 32) | threadIdx.x;
+    g_hang[2] = ((unsigned long long)bar << 32) | parity;
+  }
+}
+#else
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -41,7 +61,15 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       : "memory");
 }
 
+#endif
 // Same wait with cluster-scope acquire (pairs with a release.cluster arrive from the peer CTA).
+#ifdef SAND_HANG_DEBUG
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
+  asm volatile("fence.acq_rel.cluster;" ::: "memory");
+  mbar_wait(bar, parity);
+  asm volatile("fence.acq_rel.cluster;" ::: "memory");
+}
+#else
 __device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -55,6 +83,8 @@ __device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity)
       "r"(parity), "r"(0x989680)
       : "memory");
 }
+
+#endif
 
 // ---------------------------------------------------------------- clusters (CTA pairs)
 __device__ __forceinline__ uint32_t cluster_ctarank() {
@@ -201,6 +231,17 @@ __device__ __forceinline__ void tmem_wait_ld_dep(uint32_t (&r)[N]) {
 __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
   return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// Shared-memory matrix descriptor, K-major, no swizzle ("interleaved" core matrices of 8 rows x 16 B):
+// lbo = byte stride between K-adjacent core matrices, sbo = byte stride between 8-row groups.
+__device__ __forceinline__ uint64_t desc_nosw(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);
+}
+// Byte offset of element (row, k), k < 16, of a 16-wide bf16 K-major operand in that layout with
+// lbo = 128, sbo = 256 (the layer-1 operands of the CTA-pair kernel).
+__host__ __device__ constexpr uint32_t l1_off(uint32_t row, uint32_t k) {
+  return (row >> 3) * 256 + (k >> 3) * 128 + (row & 7) * 16 + (k & 7) * 2;
 }
 // Instruction descriptor: kind::f16, A = B = BF16, D = F32, both K-major, shape M x N.
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {

@@ -33,6 +33,7 @@ struct sand_ctx {
   bool have_w = false;
   float* d_tables = nullptr;
   float* d_pair_tables = nullptr;
+  void* d_w1_image = nullptr;
   void* d_wimage = nullptr;
   float* d_whidden = nullptr;
   MlpDev mlp{};
@@ -149,7 +150,7 @@ static void free_depthmap(sand_ctx* c) {
   c->have_dm = false;
 }
 static void free_weights(sand_ctx* c) {
-  dfree(c->d_tables); dfree(c->d_pair_tables); dfree(c->d_wimage); dfree(c->d_whidden);
+  dfree(c->d_tables); dfree(c->d_pair_tables); dfree(c->d_w1_image); dfree(c->d_wimage); dfree(c->d_whidden);
   c->have_w = false;
 }
 static void free_hostpipe(sand_ctx* c) {
@@ -261,26 +262,16 @@ extern "C" int sand_load_weights(sand_ctx* ctx, const float* blob, size_t n_floa
     auto al4 = [](long long v) { return (v + 3) & ~3ll; };
     m.pt_npoly = np;
     m.pt_off_l1 = 0;
-    m.pt_off_bias = al4(m.pt_off_l1 + 4ll * H);
-    m.pt_off_a = al4(m.pt_off_bias + (long long)(L - 1) * H);
+    m.pt_off_bias = 0;
+    m.pt_off_a = al4(m.pt_off_bias + (long long)L * H);
     m.pt_off_a1 = al4(m.pt_off_a + (long long)L * H);
     m.pt_off_c = al4(m.pt_off_a1 + (tail == SAND_TAIL_MULT ? (long long)(L - 1) * H : 0));
     m.pt_off_c1 = al4(m.pt_off_c + L);
     m.pt_off_csum = al4(m.pt_off_c1 + L);
     m.pt_floats = al4(m.pt_off_csum + L + 1);
     std::vector<float> pt((size_t)m.pt_floats, 0.f);
-    for (int j = 0; j < H; j += 2) {
-      float* e = &pt[m.pt_off_l1 + 4 * (size_t)j];
-      for (int h = 0; h < 2; ++h) {
-        const double sc = scale(j + h);
-        e[0 + h] = (float)(sc * W[0][3 * (j + h) + 0]);
-        e[2 + h] = (float)(sc * W[0][3 * (j + h) + 1]);
-        e[4 + h] = (float)(sc * W[0][3 * (j + h) + 2]);
-        e[6 + h] = (float)(sc * b[0][j + h]);
-      }
-    }
     for (int i = 1; i < L; ++i)
-      for (int j = 0; j < H; ++j) pt[m.pt_off_bias + (size_t)(i - 1) * H + j] = (float)(scale(j) * b[i][j]);
+      for (int j = 0; j < H; ++j) pt[m.pt_off_bias + (size_t)i * H + j] = (float)(scale(j) * b[i][j]);
     for (int i = 0; i < L; ++i) {
       std::memcpy(&pt[m.pt_off_a + (size_t)i * H], a[i], sizeof(float) * H);
       pt[m.pt_off_c + i] = c[i];
@@ -294,6 +285,31 @@ extern "C" int sand_load_weights(sand_ctx* ctx, const float* blob, size_t n_floa
       cs += (tail == SAND_TAIL_LINEAR || d == 1) ? c[d - 1] : 0.0;
       pt[m.pt_off_csum + d] = (float)cs;
     }
+    // layer-1 split-BF16 B operand: row n = (W_hi x y z | W_lo x y z | W_hi x y z | b_hi b_lo | 0 ...),
+    // matching the IO warp's A row (x_hi | x_hi | x_lo | 1 1 | 0): x_hi W_hi + x_hi W_lo + x_lo W_hi + b
+    std::vector<uint16_t> w1img((size_t)H * 16, 0);
+    auto put = [&](int n, int k, uint16_t v) { w1img[tc2_w1_offset(H, n, k) / 2] = v; };
+    auto lo_of = [](float v, uint16_t hi) {
+      uint32_t u = (uint32_t)hi << 16;
+      float h;
+      std::memcpy(&h, &u, 4);
+      return bf16_rne(v - h);
+    };
+    for (int n = 0; n < H; ++n) {
+      for (int k = 0; k < 3; ++k) {
+        const float w = W[0][3 * n + k];
+        const uint16_t hi = bf16_rne(w);
+        put(n, k, hi);
+        put(n, 3 + k, lo_of(w, hi));
+        put(n, 6 + k, hi);
+      }
+      const uint16_t bhi = bf16_rne(b[0][n]);
+      put(n, 9, bhi);
+      put(n, 10, lo_of(b[0][n], bhi));
+    }
+    CU(cudaMalloc(&ctx->d_w1_image, w1img.size() * 2));
+    CU(cudaMemcpy(ctx->d_w1_image, w1img.data(), w1img.size() * 2, cudaMemcpyHostToDevice));
+    m.w1_image = ctx->d_w1_image;
     CU(cudaMalloc(&ctx->d_pair_tables, sizeof(float) * pt.size()));
     CU(cudaMemcpy(ctx->d_pair_tables, pt.data(), sizeof(float) * pt.size(), cudaMemcpyHostToDevice));
     m.pair_tables = ctx->d_pair_tables;

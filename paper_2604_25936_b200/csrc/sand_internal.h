@@ -61,11 +61,12 @@ struct MlpDev {
   long long off_w1, off_bias, off_a, off_c, off_a1, off_c1, tables_floats;
   // CTA-pair kernel tables (tmlp_tc2.cu), pre-scaled per column for its sine path: of every 16 columns
   // the first pt_npoly use the FMA-pipe polynomial (scale w0/pi), the rest MUFU.SIN (scale w0):
-  //   l1  : [H/2][8] = per column pair (wx0, wx1, wy0, wy1, wz0, wz1, b0, b1) * scale(col)
-  //   bias: [L-1][H] = scale(col) * b_i (i >= 2);  a: [L][H];  a1: [L-1][H] (MULT)
+  //   bias: [L][H] = scale(col) * b_i, row 0 (i = 1) zero: b_1 rides in the layer-1 MMA
+  //   a: [L][H];  a1: [L-1][H] (MULT)
   //   c   : [L] tail biases (MULT: c_i0);  c1: [L] (MULT: c_i1 at index i-1, i >= 2)
   //   csum: [L+1] LINEAR: sum_{i <= d} c_i;  MULT: c_1 (d >= 1)
   const float* pair_tables;
+  const void* w1_image;      // layer-1 split-BF16 B operand, [2 halves][H/2 rows][16 bf16] (l1_off layout)
   long long pt_floats, pt_off_l1, pt_off_bias, pt_off_a, pt_off_a1, pt_off_c, pt_off_c1, pt_off_csum;
   int pt_npoly;
 };
@@ -90,5 +91,6 @@ int tc2_npoly();   // polynomial share in use (SAND_NPOLY env override: 0, 4, 6,
 cudaError_t launch_tmlp_tc2(const MlpDev& m, const float* pts, const uint32_t* perm, const QueryMeta* meta,
                             float* out, int num_sms, cudaStream_t st);
 cudaError_t prepare_tc2(int H, int tail);
+size_t tc2_w1_offset(int H, int n, int k);   // byte offset of (unit n, column k) in MlpDev::w1_image
 
 }  // namespace sand
