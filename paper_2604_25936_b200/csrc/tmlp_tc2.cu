@@ -54,7 +54,7 @@ struct Tc2Shape {
   static constexpr int HQ = H / 4;                 // columns per epilogue thread (column quarter)
   static constexpr int NG = HQ / 16;               // 16-column TMEM load groups per thread
   static constexpr int TMEM_COLS = 2 * H <= 128 ? 128 : (2 * H <= 256 ? 256 : 512);
-  static constexpr int THREADS = 128 + 512;
+  static constexpr int THREADS = 96 + 512;      // 3 control warps + 16 epilogue warps
   static constexpr int TILE = 256;
   static_assert(H % 64 == 0 && H <= 256 && HQ % 16 == 0, "CTA-pair kernel: H in {64, 128, 192, 256}");
 };
@@ -222,7 +222,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
     }
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc_cg2(smem_u32(tmem_slot), C::TMEM_COLS);
+  if (warp == 1) tmem_alloc_cg2(smem_u32(tmem_slot), C::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
   cluster_sync();   // both CTAs' barriers initialised before any remote arrive / multicast commit
@@ -325,7 +325,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
           for (int k = 4; k < 6; ++k) g_kprof[blockIdx.x][k] = pc[k];
       }
     }
-  } else if (warp == 3) {
+  } else if (warp == 2) {
     // =========================== IO warp: every global access of the tile rows
     // Tile i of slot s uses buffer i & 1.  Fill (perm rows loaded one tile earlier, so only the point
     // gather is on the critical path) writes the split-BF16 layer-1 A rows and the perm rows; it waits
@@ -429,9 +429,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
       }
     }
     if (p.prof && lane == 0) { g_kprof[blockIdx.x][10] = io_wait; g_kprof[blockIdx.x][11] = io_busy; }
-  } else if (warp >= 4) {
+  } else if (warp >= 3) {
     // =========================== epilogue (16 warps, both slots, step by step)
-    const int ew = warp - 4;
+    const int ew = warp - 3;
     const int q = warp & 3;                  // TMEM lane quadrant = warp % 4
     const int cq = ew >> 2;                  // column quarter
     const int row = 32 * q + lane;           // TMEM lane / local A row
@@ -476,14 +476,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
       const float* a1 = ta1 + (l - 2) * H;
       const bool prod = TAIL == SAND_TAIL_MULT && l >= 2;
       const uint32_t tm = tm_row + (uint32_t)(s * H);
-      uint32_t ra[16], rb[16];
-      tmem_ld16(tm, ra);
+      // TMEM loads in 32-column batches (two 16-column groups per wait): half the exposed load latencies
+      uint32_t rr[32];
 #pragma unroll
       for (int g = 0; g < C::NG; ++g) {
-        uint32_t (&r)[16] = (g & 1) ? rb : ra;
-        uint32_t (&rn)[16] = (g & 1) ? ra : rb;
-        tmem_wait_ld_dep(r);
-        if (g + 1 < C::NG) tmem_ld16(tm + 16 * (g + 1), rn);
+        if ((g & 1) == 0) {
+          if (g + 1 < C::NG) {
+            tmem_ld32(tm + 16 * g, rr);
+            tmem_wait_ld_dep(rr);
+          } else {
+            uint32_t (&r16)[16] = *reinterpret_cast<uint32_t(*)[16]>(rr);
+            tmem_ld16(tm + 16 * g, r16);
+            tmem_wait_ld_dep(r16);
+          }
+        }
+        const uint32_t (&r)[16] = *reinterpret_cast<const uint32_t(*)[16]>(rr + 16 * (g & 1));
         uint32_t pk[8];
 #pragma unroll
         for (int qd = 0; qd < 4; ++qd) {
@@ -557,7 +564,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
       if (!e0.w.done) step(e0, 0);
       if (!e1.w.done) step(e1, 1);
     }
-    if (p.prof && warp == 4 && lane == 0) {
+    if (p.prof && warp == 3 && lane == 0) {
       g_kprof[blockIdx.x][6] = ep_wait;
       g_kprof[blockIdx.x][7] = ep_busy;
       g_kprof[blockIdx.x][8] = clock64() - t_start;
@@ -568,7 +575,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
   __syncthreads();
   cluster_sync();
   tc_fence_after();
-  if (warp == 2) tmem_dealloc_cg2(tmem_base, C::TMEM_COLS);
+  if (warp == 1) tmem_dealloc_cg2(tmem_base, C::TMEM_COLS);
 }
 
 // ------------------------------------------------------------------------------------ host side
