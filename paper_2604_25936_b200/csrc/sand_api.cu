@@ -35,6 +35,7 @@ struct sand_ctx {
   float* d_pair_tables = nullptr;
   void* d_w1_image = nullptr;
   void* d_wimage = nullptr;
+  void* d_wimage_pair = nullptr;
   float* d_whidden = nullptr;
   MlpDev mlp{};
   // depth map
@@ -150,7 +151,7 @@ static void free_depthmap(sand_ctx* c) {
   c->have_dm = false;
 }
 static void free_weights(sand_ctx* c) {
-  dfree(c->d_tables); dfree(c->d_pair_tables); dfree(c->d_w1_image); dfree(c->d_wimage); dfree(c->d_whidden);
+  dfree(c->d_tables); dfree(c->d_pair_tables); dfree(c->d_w1_image); dfree(c->d_wimage); dfree(c->d_wimage_pair); dfree(c->d_whidden);
   c->have_w = false;
 }
 static void free_hostpipe(sand_ctx* c) {
@@ -339,10 +340,24 @@ extern "C" int sand_load_weights(sand_ctx* ctx, const float* blob, size_t n_floa
         }
       CU(cudaMalloc(&ctx->d_wimage, img.size() * 2));
       CU(cudaMemcpy(ctx->d_wimage, img.data(), img.size() * 2, cudaMemcpyHostToDevice));
+      if (tc2_available(H)) {
+        // pair image: chunk (i, kc) half r -> [(i-1)][r][kc]
+        const size_t half = chunk / 2;
+        std::vector<uint8_t> pimg(img.size() * 2);
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(img.data());
+        for (int i = 1; i < L; ++i)
+          for (int r = 0; r < 2; ++r)
+            for (int kc = 0; kc < KC; ++kc)
+              std::memcpy(&pimg[(((size_t)(i - 1) * 2 + r) * KC + kc) * half],
+                          src + ((size_t)(i - 1) * KC + kc) * chunk + r * half, half);
+        CU(cudaMalloc(&ctx->d_wimage_pair, pimg.size()));
+        CU(cudaMemcpy(ctx->d_wimage_pair, pimg.data(), pimg.size(), cudaMemcpyHostToDevice));
+      }
     }
   }
   m.w_hidden = ctx->d_whidden;
   m.w_image = ctx->d_wimage;
+  m.w_image_pair = ctx->d_wimage_pair;
   ctx->mlp = m;
   ctx->have_w = true;
   return SAND_OK;

@@ -53,6 +53,9 @@ struct MlpDev {
   const float* w_hidden;     // (L-1)*H*H
   // BF16 tcgen05 path: pre-swizzled SW128 K-major image [L-1][KC][H rows][128 B]
   const void* w_image;
+  // same BF16 tiles regrouped for the CTA-pair kernel: [L-1][2 CTA halves][KC][H/2 rows][128 B], so a CTA's
+  // half of a layer is one contiguous run (bulk copies of 2 K-chunks)
+  const void* w_image_pair;
   // FP32 tables (both paths):
   //   w1: float4[H] = (w0*W1[j][0], w0*W1[j][1], w0*W1[j][2], w0*b1[j])
   //   bias: [L-1][H] = w0 * b_i (i >= 2);  a: [L][H] tail (a_i or a_i0);

@@ -48,6 +48,9 @@ struct Tc2Shape {
   static constexpr int A_BYTES = KC * A_CHUNK;
   static constexpr int W_CHUNK = H * 128;          // full K-chunk of W (both halves) in the image
   static constexpr int WH_CHUNK = (H / 2) * 128;   // this CTA's half (N/2 rows)
+  static constexpr int SC = KC >= 2 ? 2 : 1;       // K-chunks per weight-ring stage (one bulk copy:
+  static constexpr int STAGE = SC * WH_CHUNK;      // a bulk copy costs ~400 clk of the SM's TMA unit
+  static constexpr int NSJ = KC / SC;              // regardless of size up to 32 KB); stages per job
   static constexpr int A1_BYTES = 128 * 32;        // layer-1 A operand: 128 rows x 16 bf16
   static constexpr int W1_HALF = (H / 2) * 32;     // layer-1 B operand: this CTA's H/2 rows x 16 bf16
   static constexpr int NSLOT = 2;
@@ -149,40 +152,42 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
   using C = Tc2Shape<H>;
   constexpr int NSLOT = C::NSLOT;
   extern __shared__ uint8_t smem_raw[];
-  const uint32_t raw = smem_u32(smem_raw);
-  const uint32_t base = (raw + 1023u) & ~1023u;
-  uint8_t* gbase = smem_raw + (base - raw);
+  // The dynamic window starts after the 1 KB reserved system area, i.e. 1024-aligned (required by the
+  // SW128 operands; no slack is budgeted for re-alignment).
+  const uint32_t base = smem_u32(smem_raw);
+  if (base & 1023u) __trap();
+  uint8_t* gbase = smem_raw;
   const int nst = p.nst;
   const int L = p.m.L;
   const uint32_t rank = cluster_ctarank();
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
   // ---- shared memory carve-up (identical offsets in both CTAs: the pair MMA relies on it)
   const uint32_t sA = base;                                       // [slot] KC x 16 KB, SW128 K-major
-  const uint32_t sW = sA + NSLOT * C::A_BYTES;                    // weight ring, nst x WH_CHUNK
-  const uint32_t sW1 = sW + nst * C::WH_CHUNK;                    // layer-1 B half (resident)
-  const uint32_t sA1 = sW1 + C::W1_HALF;                          // [slot][buf] layer-1 A operand
-  const uint32_t off_tab = (sA1 + NSLOT * 2 * C::A1_BYTES) - base;
-  float* tab = reinterpret_cast<float*>(gbase + off_tab);
+  const uint32_t sW = sA + NSLOT * C::A_BYTES;                    // weight ring, nst x STAGE
+  const uint32_t sW1 = sW + nst * C::STAGE;                       // layer-1 B half (resident)
+  const uint32_t sA1 = sW1 + C::W1_HALF;                          // [slot] layer-1 A operand
+  float* tab = reinterpret_cast<float*>(gbase + ((sA1 + NSLOT * C::A1_BYTES) - base));
   const long long ntab = p.m.pt_floats;
-  uint32_t* io_idx = reinterpret_cast<uint32_t*>(tab + ((ntab + 3) & ~3ll));   // [slot][buf][128] perm rows
-  float* io_part = reinterpret_cast<float*>(io_idx + NSLOT * 2 * 128);           // [slot][buf][cq][128]
-  float2* red2 = reinterpret_cast<float2*>(io_part + NSLOT * 2 * 4 * 128);       // MULT: [slot][kpar][cq][128]
+  float* part = tab + ((ntab + 3) & ~3ll);                        // [slot][cq][128] tile-end partials
+  float* out_y = part + NSLOT * 4 * 128;                          // [slot][buf][128] finished y_d
+  float2* red2 = reinterpret_cast<float2*>(out_y + NSLOT * 2 * 128);   // MULT: [slot][kpar][cq][128]
   const int red2_floats = (TAIL == SAND_TAIL_MULT) ? NSLOT * 2 * 4 * 128 * 2 : 0;
-  long long* meta_s = reinterpret_cast<long long*>(io_part + NSLOT * 2 * 4 * 128 + red2_floats);
+  const int nb = L + 2;
+  long long* meta_s = reinterpret_cast<long long*>(out_y + NSLOT * 2 * 128 + red2_floats);
   long long* s_tile_end = meta_s;
-  long long* s_tile_begin = meta_s + kMaxBins;
-  long long* s_start = meta_s + 2 * kMaxBins;
-  long long* s_count = meta_s + 3 * kMaxBins;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(meta_s + 4 * kMaxBins);
+  long long* s_tile_begin = meta_s + nb;
+  long long* s_start = meta_s + 2 * nb;
+  long long* s_count = meta_s + 3 * nb;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(meta_s + 4 * nb);
   const uint32_t b_wfull = smem_u32(bars);
   const uint32_t b_wempty = b_wfull + 8 * nst;
   const uint32_t b_wpeer = b_wempty + 8 * nst;
-  const uint32_t b_afull = b_wpeer + 8 * nst;           // [slot]  A of layer l >= 2 published
+  const uint32_t b_afull = b_wpeer + 8 * nst;           // [slot]  epilogue step done (A written / acc read)
   const uint32_t b_accfull = b_afull + 8 * NSLOT;       // [slot]  accumulator ready
-  const uint32_t b_a1full = b_accfull + 8 * NSLOT;      // [slot][buf] layer-1 A written (leader: 2 arrivals)
-  const uint32_t b_a1free = b_a1full + 8 * NSLOT * 2;   // [slot][buf] layer-1 MMA done with the buffer
-  const uint32_t b_iodone = b_a1free + 8 * NSLOT * 2;   // [slot][buf] tile partials written
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * nst + 2 * NSLOT + 6 * NSLOT);
+  const uint32_t b_a1full = b_accfull + 8 * NSLOT;      // [slot]  layer-1 A written (leader: 2 arrivals)
+  const uint32_t b_a1free = b_a1full + 8 * NSLOT;       // [slot]  layer-1 MMA done with the A1 buffer
+  const uint32_t b_iodone = b_a1free + 8 * NSLOT;       // [slot][buf] y_d of a tile in out_y
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * nst + 7 * NSLOT);
 #ifdef SAND_HANG_DEBUG
   if (blockIdx.x == 0 && threadIdx.x == 0)
     printf("[bars] wfull 0x%x wempty 0x%x wpeer 0x%x afull 0x%x accfull 0x%x a1full 0x%x a1free 0x%x iodone 0x%x\n",
@@ -198,7 +203,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
                                                       rank * C::W1_HALF);
     uint4* w1d = reinterpret_cast<uint4*>(gbase + (sW1 - base));
     for (int i = tid; i < C::W1_HALF / 16; i += blockDim.x) w1d[i] = w1s[i];
-    if (tid < kMaxBins) {
+    if (tid < nb) {
       s_tile_end[tid] = p.meta->tile_end[tid];
       s_tile_begin[tid] = p.meta->tile_begin[tid];
       s_start[tid] = p.meta->start[tid];
@@ -215,11 +220,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
     }
     // a_full: one arrive per epilogue warp of both CTAs
     for (int s = 0; s < NSLOT; ++s) { mbar_init(b_afull + 8 * s, 2 * kEpiWarps); mbar_init(b_accfull + 8 * s, 1); }
-    for (int i = 0; i < 2 * NSLOT; ++i) {
-      mbar_init(b_a1full + 8 * i, 2);
-      mbar_init(b_a1free + 8 * i, 1);
-      mbar_init(b_iodone + 8 * i, kEpiWarps);
-    }
+    for (int s = 0; s < NSLOT; ++s) { mbar_init(b_a1full + 8 * s, 2); mbar_init(b_a1free + 8 * s, 1); }
+    for (int i = 0; i < 2 * NSLOT; ++i) mbar_init(b_iodone + 8 * i, 4);   // the 4 column-quarter-0 warps
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc_cg2(smem_u32(tmem_slot), C::TMEM_COLS);
@@ -237,7 +239,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
       SlotWalk w0, w1;
       w0.start(pair, T, s_tile_end, L);
       w1.start(pair + npairs, T, s_tile_end, L);
-      const uint8_t* img = reinterpret_cast<const uint8_t*>(p.m.w_image) + rank * C::WH_CHUNK;
+      // pair weight image: [L-1][2 CTA halves][KC][H/2 rows][128 B]: a CTA's half of a layer is contiguous
+      const uint8_t* img = reinterpret_cast<const uint8_t*>(p.m.w_image_pair) + (size_t)rank * C::KC * C::WH_CHUNK;
       const uint32_t peer_wpeer = mapa_shared(b_wpeer, 0);
       constexpr uint32_t ID = idesc_bf16(256, H);
       uint32_t pa0 = 0, pa1 = 0;
@@ -261,26 +264,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
         if (l == 1) {
           if (warp != 1 || rank != 0) return;
           // ---- layer 1: one K = 16 MMA on the split-BF16 operands written by the IO warps
-          const int b = w.ti & 1;
           wait_prev_step(w, s);
           const long long c0_ = p.prof ? clock64() : 0;
-          mbar_wait_cluster(b_a1full + 8 * (s * 2 + b), (uint32_t)((w.ti >> 1) & 1));
+          mbar_wait_cluster(b_a1full + 8 * s, (uint32_t)(w.ti & 1));
           if (p.prof) { pc[0] += clock64() - c0_; pc[3] += 1; }
           tc_fence_after();
-          mma_bf16_cg2(tmem_base + (uint32_t)(s * H), desc_nosw(sA1 + (s * 2 + b) * C::A1_BYTES, 128, 256),
+          mma_bf16_cg2(tmem_base + (uint32_t)(s * H), desc_nosw(sA1 + s * C::A1_BYTES, 128, 256),
                        desc_nosw(sW1, 128, 256), ID, 0u);
-          mma_commit_cg2_mc(b_a1free + 8 * (s * 2 + b), 0x3);
+          mma_commit_cg2_mc(b_a1free + 8 * s, 0x3);
           mma_commit_cg2_mc(b_accfull + 8 * s, 0x3);
           return;
         }
         if (warp == 0) {
-          const uint8_t* src = img + (size_t)(l - 2) * C::KC * C::W_CHUNK;
-          for (int kc = 0; kc < C::KC; ++kc) {
+          const uint8_t* src = img + (size_t)(l - 2) * 2 * C::KC * C::WH_CHUNK;
+          for (int j = 0; j < C::NSJ; ++j) {
             const long long c0_ = p.prof ? clock64() : 0;
             mbar_wait(b_wempty + 8 * st, ph ^ 1u);
             if (p.prof) { pc[4] += clock64() - c0_; pc[5] += 1; }
-            mbar_arrive_expect_tx(b_wfull + 8 * st, C::WH_CHUNK);
-            bulk_g2s(sW + st * C::WH_CHUNK, src + (size_t)kc * C::W_CHUNK, C::WH_CHUNK, b_wfull + 8 * st);
+            mbar_arrive_expect_tx(b_wfull + 8 * st, C::STAGE);
+            bulk_g2s(sW + st * C::STAGE, src + (size_t)j * C::STAGE, C::STAGE, b_wfull + 8 * st);
             if (++st == nst) { st = 0; ph ^= 1u; }
           }
         } else if (rank == 0) {
@@ -289,23 +291,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
           tc_fence_after();
           const uint32_t acc = tmem_base + (uint32_t)(s * H);
           const uint32_t a_base = sA + s * C::A_BYTES;
-          for (int kc = 0; kc < C::KC; ++kc) {
+          for (int j = 0; j < C::NSJ; ++j) {
             c0_ = p.prof ? clock64() : 0;
             mbar_wait(b_wfull + 8 * st, ph);
             mbar_wait_cluster(b_wpeer + 8 * st, ph);
             if (p.prof) pc[1] += clock64() - c0_;
             tc_fence_after();
-            const uint32_t w_base = sW + st * C::WH_CHUNK;
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              mma_bf16_cg2(acc, desc_sw128(a_base + kc * C::A_CHUNK + 32 * k), desc_sw128(w_base + 32 * k), ID,
-                           (kc | k) ? 1u : 0u);
+            for (int c = 0; c < C::SC; ++c) {
+              const int kc = j * C::SC + c;
+              const uint32_t w_base = sW + st * C::STAGE + c * C::WH_CHUNK;
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                mma_bf16_cg2(acc, desc_sw128(a_base + kc * C::A_CHUNK + 32 * k), desc_sw128(w_base + 32 * k), ID,
+                             (kc | k) ? 1u : 0u);
+            }
             mma_commit_cg2_mc(b_wempty + 8 * st, 0x3);
             if (++st == nst) { st = 0; ph ^= 1u; }
           }
           mma_commit_cg2_mc(b_accfull + 8 * s, 0x3);
         } else {
-          for (int kc = 0; kc < C::KC; ++kc) {
+          for (int j = 0; j < C::NSJ; ++j) {
             mbar_wait(b_wfull + 8 * st, ph);
             mbar_arrive_remote(peer_wpeer + 8 * st);
             if (++st == nst) { st = 0; ph ^= 1u; }
@@ -327,11 +333,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
     }
   } else if (warp == 2) {
     // =========================== IO warp: every global access of the tile rows
-    // Tile i of slot s uses buffer i & 1.  Fill (perm rows loaded one tile earlier, so only the point
-    // gather is on the critical path) writes the split-BF16 layer-1 A rows and the perm rows; it waits
-    // for the layer-1 MMA of tile i - 2 to release the buffer (a1_free).  Drain (at tile end, in the
-    // epilogue's order) sums the 4 column-quarter partials + csum[d] and stores sdf[perm[row]].
-    const float* tcs = tab + p.m.pt_off_csum;
+    // Walks the epilogue's step order.  At a tile's layer-1 step it waits until the layer-1 MMA has
+    // consumed the slot's A1 buffer (a1_free) and refills it with the slot's next tile (perm rows were
+    // loaded one tile earlier, so only the point gather is on the critical path), then prefetches the
+    // perm rows of the tile after.  At a tile's last step it waits for y_d (io_done) and stores
+    // sdf[perm[row]].  Perm rows live in registers: cur (tile being computed), nxt (next tile, in A1
+    // once filled), pre (the tile after).
     const uint32_t a1full_dst = rank == 0 ? b_a1full : mapa_shared(b_a1full, 0);
     unsigned long long io_wait = 0, io_busy = 0;
     auto load_perm = [&](long long t, uint32_t (&ix)[4]) {
@@ -344,18 +351,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
         ix[k] = r < rend ? __ldg(p.perm + r) : 0xFFFFFFFFu;
       }
     };
-    auto fill = [&](int s, int b, const uint32_t (&ix)[4]) {
+    auto fill = [&](int s, const uint32_t (&ix)[4]) {
       float x[4], y[4], z[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const size_t i = ix[k] == 0xFFFFFFFFu ? 0 : ix[k];
         x[k] = __ldg(p.pts + 3 * i); y[k] = __ldg(p.pts + 3 * i + 1); z[k] = __ldg(p.pts + 3 * i + 2);
       }
-      const uint32_t a1 = sA1 + (s * 2 + b) * C::A1_BYTES;
+      const uint32_t a1 = sA1 + s * C::A1_BYTES;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const int row = lane + 32 * k;
-        io_idx[(s * 2 + b) * 128 + row] = ix[k];
         // split v = hi + lo (bf16 each).  A row, k = 0..15:
         //   x_hi y_hi z_hi | x_hi y_hi z_hi | x_lo y_lo z_lo | 1 1 | 0 0 0 0 0
         const uint32_t hxy = pack_bf16x2(x[k], y[k]);                // lo half = x_hi, hi half = y_hi
@@ -376,57 +382,55 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-        if (rank == 0) mbar_arrive(a1full_dst + 8 * (s * 2 + b));
-        else mbar_arrive_remote(a1full_dst + 8 * (s * 2 + b));
+        if (rank == 0) mbar_arrive(a1full_dst + 8 * s);
+        else mbar_arrive_remote(a1full_dst + 8 * s);
       }
     };
+    struct IoSlot { uint32_t cur[4], nxt[4], pre[4]; };
     SlotWalk w0, w1;
     w0.start(pair, T, s_tile_end, L);
     w1.start(pair + npairs, T, s_tile_end, L);
-    uint32_t nx0[4], nx1[4];   // perm rows of the next tile to fill, per slot
+    IoSlot q0, q1;
 #pragma unroll
     for (int s = 0; s < NSLOT; ++s) {
+      IoSlot& q = s ? q1 : q0;
       const long long t0 = pair + (long long)npairs * s;
-      uint32_t ix[4];
-      for (int i = 0; i < 2; ++i)
-        if (t0 + i * tstride < T) { load_perm(t0 + i * tstride, ix); fill(s, i, ix); }
-      uint32_t (&nx)[4] = s ? nx1 : nx0;
-      if (t0 + 2 * tstride < T) load_perm(t0 + 2 * tstride, nx);
-    }
-    auto tile_end = [&](const SlotWalk& w, int s, uint32_t (&nx)[4]) {
-      const int b = w.ti & 1;
-      const uint32_t par = (uint32_t)((w.ti >> 1) & 1);
-      const long long c0_ = p.prof ? clock64() : 0;
-      mbar_wait(b_iodone + 8 * (s * 2 + b), par);
-      const long long c1_ = p.prof ? clock64() : 0;
-      const float cs = tcs[w.d];
-      const float* part = io_part + (s * 2 + b) * 4 * 128;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int row = lane + 32 * k;
-        const uint32_t ix = io_idx[(s * 2 + b) * 128 + row];
-        const float y = cs + part[row] + part[128 + row] + part[256 + row] + part[384 + row];
-        if (ix != 0xFFFFFFFFu) p.out[ix] = y;
+      for (int k = 0; k < 4; ++k) q.cur[k] = q.nxt[k] = q.pre[k] = 0xFFFFFFFFu;
+      if (t0 < T) { load_perm(t0, q.cur); fill(s, q.cur); }
+      if (t0 + tstride < T) load_perm(t0 + tstride, q.nxt);
+    }
+    auto io_step = [&](const SlotWalk& w, int s, IoSlot& q) {
+      const long long c0_ = p.prof ? clock64() : 0;
+      long long waited = 0;
+      if (w.l == 1) {
+        const long long t1 = w.t + tstride;
+        if (t1 < T) {
+          mbar_wait(b_a1free + 8 * s, (uint32_t)(w.ti & 1));   // this tile's layer-1 MMA read A1
+          if (p.prof) waited += clock64() - c0_;
+          fill(s, q.nxt);
+          if (t1 + tstride < T) load_perm(t1 + tstride, q.pre);
+        }
       }
-      __syncwarp();
-      const long long t2 = w.t + 2 * tstride;
-      if (t2 < T) {
-        mbar_wait(b_a1free + 8 * (s * 2 + b), par);   // layer-1 MMA of this tile done with the buffer
-        fill(s, b, nx);
-        if (t2 + tstride < T) load_perm(t2 + tstride, nx);
+      if (w.l == w.d) {
+        const int b = w.ti & 1;
+        const long long c1_ = p.prof ? clock64() : 0;
+        mbar_wait(b_iodone + 8 * (s * 2 + b), (uint32_t)((w.ti >> 1) & 1));
+        if (p.prof) waited += clock64() - c1_;
+        const float* yb = out_y + (s * 2 + b) * 128;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (q.cur[k] != 0xFFFFFFFFu) p.out[q.cur[k]] = yb[lane + 32 * k];
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < 4; ++k) { q.cur[k] = q.nxt[k]; q.nxt[k] = q.pre[k]; }
       }
-      if (p.prof) { io_wait += c1_ - c0_; io_busy += clock64() - c1_; }
+      if (p.prof) { io_wait += waited; io_busy += clock64() - c0_ - waited; }
     };
 #pragma unroll 1
     while (!(w0.done && w1.done)) {
-      if (!w0.done) {
-        if (w0.l == w0.d) tile_end(w0, 0, nx0);
-        w0.advance(tstride, T, s_tile_end, L);
-      }
-      if (!w1.done) {
-        if (w1.l == w1.d) tile_end(w1, 1, nx1);
-        w1.advance(tstride, T, s_tile_end, L);
-      }
+      if (!w0.done) { io_step(w0, 0, q0); w0.advance(tstride, T, s_tile_end, L); }
+      if (!w1.done) { io_step(w1, 1, q1); w1.advance(tstride, T, s_tile_end, L); }
     }
     if (p.prof && lane == 0) { g_kprof[blockIdx.x][10] = io_wait; g_kprof[blockIdx.x][11] = io_busy; }
   } else if (warp >= 3) {
@@ -446,7 +450,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
     const float* ta1 = tab + p.m.pt_off_a1;    // [L-1][H] (MULT)
     const float* tc0 = tab + p.m.pt_off_c;     // [L]
     const float* tc1 = tab + p.m.pt_off_c1;    // [L] (MULT, index l-1)
-    const uint32_t bar_q = 1 + q;              // per-quadrant named barrier (MULT reductions)
+    const float* tcs = tab + p.m.pt_off_csum;  // [L+1]
+    const uint32_t bar_q = 1 + q;              // per-quadrant named barrier (tile-end / MULT reductions)
     const uint32_t afull_dst0 = rank == 0 ? b_afull : mapa_shared(b_afull, 0);
     unsigned long long ep_wait = 0, ep_busy = 0, ep_steps = 0;
 
@@ -524,7 +529,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
                        pk[7]);
         }
       }
-      publish(s, store);
       if (prod) {
         // Eq. 3: t_l = (a_l0 . h + c_l0)(a_l1 . h + c_l1) needs both full dot products of the row
         float2* rb2 = red2 + ((s * 2 + e.kpar) * 4) * 128;
@@ -541,14 +545,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
         e.ylin += yv.x + yv.y;
       }
       if (l == d) {
-        // tile end: hand this thread's partial of y_d to the IO warp
-        const int b = e.w.ti & 1;
-        io_part[((s * 2 + b) * 4 + cq) * 128 + row] = e.ylin + e.yprod;
-        __syncwarp();
-        if (lane == 0) mbar_arrive(b_iodone + 8 * (s * 2 + b));
+        // tile end: reduce the four column quarters of every row (per-quadrant barrier); column quarter
+        // 0 adds the tail-bias prefix sum and hands y_d to the IO warp.  Done before this step's
+        // publish, so the next tile's MMA (and its tile end) cannot overwrite `part` before it is read.
+        float* pq = part + s * 4 * 128;
+        pq[cq * 128 + row] = e.ylin + e.yprod;
+        named_bar_sync(bar_q, 128);
+        if (cq == 0) {
+          const int b = e.w.ti & 1;
+          out_y[(s * 2 + b) * 128 + row] = tcs[d] + pq[row] + pq[128 + row] + pq[256 + row] + pq[384 + row];
+          __syncwarp();
+          if (lane == 0) mbar_arrive(b_iodone + 8 * (s * 2 + b));
+        }
         e.ylin = 0.f;
         e.yprod = 0.f;
       }
+      publish(s, store);
       e.w.advance(tstride, T, s_tile_end, L);
       if (p.prof) { ep_wait += c1_ - c0_; ep_busy += clock64() - c1_; ep_steps += 1; }
     };
@@ -580,23 +592,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
 
 // ------------------------------------------------------------------------------------ host side
 template <int H>
-static size_t smem_for2(long long pt_floats, int tail, int nst) {
+static size_t smem_for2(long long pt_floats, int L, int tail, int nst) {
   using C = Tc2Shape<H>;
   const size_t tab_bytes = (size_t)((pt_floats + 3) & ~3ll) * 4;
-  const size_t io_bytes = (size_t)C::NSLOT * 2 * 128 * 4 + (size_t)C::NSLOT * 2 * 4 * 128 * 4;
+  const size_t io_bytes = (size_t)C::NSLOT * 4 * 128 * 4 + (size_t)C::NSLOT * 2 * 128 * 4;
   const size_t red_bytes = tail == SAND_TAIL_MULT ? (size_t)C::NSLOT * 2 * 4 * 128 * 8 : 0;
-  return 1024 + (size_t)C::NSLOT * C::A_BYTES + (size_t)nst * C::WH_CHUNK + C::W1_HALF +
-         (size_t)C::NSLOT * 2 * C::A1_BYTES + tab_bytes + io_bytes + red_bytes + 4 * kMaxBins * sizeof(long long) +
-         (3 * nst + 8 * C::NSLOT) * 8 + 16;
+  return (size_t)C::NSLOT * C::A_BYTES + (size_t)nst * C::STAGE + C::W1_HALF + (size_t)C::NSLOT * C::A1_BYTES +
+         tab_bytes + io_bytes + red_bytes + 4 * (size_t)(L + 2) * sizeof(long long) + (3 * nst + 7 * C::NSLOT) * 8 +
+         16;
 }
 
 static constexpr size_t kSmemMax2 = 232448;
 
 template <int H>
-static int pick_nst2(long long pt_floats, int tail) {
+static int pick_nst2(long long pt_floats, int L, int tail) {
   int best = 0;
-  for (int nst = 2; nst <= 8; ++nst)
-    if (smem_for2<H>(pt_floats, tail, nst) <= kSmemMax2) best = nst;
+  for (int nst = 1; nst <= 8; ++nst)
+    if (smem_for2<H>(pt_floats, L, tail, nst) <= kSmemMax2) best = nst;
   return best;
 }
 
@@ -623,9 +635,9 @@ size_t tc2_w1_offset(int H, int n, int k) {
 template <int H, int TAIL, int NP>
 static cudaError_t launch_tc2_t(const MlpDev& m, const float* pts, const uint32_t* perm, const QueryMeta* meta,
                                 float* out, int num_sms, cudaStream_t st) {
-  const int nst = pick_nst2<H>(m.pt_floats, TAIL);
+  const int nst = pick_nst2<H>(m.pt_floats, m.L, TAIL);
   if (!nst) return cudaErrorInvalidConfiguration;
-  const size_t sm = smem_for2<H>(m.pt_floats, TAIL, nst);
+  const size_t sm = smem_for2<H>(m.pt_floats, m.L, TAIL, nst);
   static const int prof = getenv("SAND_KPROF") ? atoi(getenv("SAND_KPROF")) : 0;
   Tc2Params p{m, pts, perm, meta, out, nst, prof};
   const int grid = num_sms & ~1;
