@@ -46,8 +46,11 @@ typedef enum {
 /* Arithmetic of the H x H layers.
  *   SAND_FP32  : FP32 SIMT kernels (FFMA, accurate sinf); supported H in {16, 32, 64}.
  *                Tolerance vs the oracle: 1e-4 max-abs (BASELINE.json north_star).
- *   SAND_BF16  : tcgen05 tensor cores, BF16 operands, FP32 accumulate in TMEM; layer 1 (K = 3)
- *                and all tails in FP32; supported H in {64, 128, 256, 336}.  Tolerance 5e-3.
+ *   SAND_BF16  : tcgen05 tensor cores, BF16 operands, FP32 accumulate in TMEM; layer 1 (K = 3) as a
+ *                split-BF16 MMA (x = x_hi + x_lo, relative error ~2^-16) or FP32 SIMT, all tails and
+ *                the sine in FP32; supported H in {64, 128, 256, 336}; the per-column tables stay on
+ *                chip, which bounds L (e.g. L <= 24 at H = 256; larger -> SAND_ERR_UNSUPPORTED).
+ *                Tolerance 5e-3.
  *   SAND_TF32X3: reserved (returns SAND_ERR_UNSUPPORTED in this build).                        */
 typedef enum { SAND_FP32 = 0, SAND_TF32X3 = 1, SAND_BF16 = 2 } sand_precision;
 

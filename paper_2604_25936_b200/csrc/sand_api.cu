@@ -96,7 +96,8 @@ static void dfree(T*& p) {
 
 static bool supported(const sand_config& c) {
   if (c.prec == SAND_FP32) return simt_supported_H(c.H) && simt_smem_bytes(c.L, c.H, c.tail) <= 232448;
-  if (c.prec == SAND_BF16) return tc_supported_H(c.H) && tc_smem_bytes(c.L, c.H, c.tail) > 0;
+  if (c.prec == SAND_BF16)
+    return tc_supported_H(c.H) && (tc2_usable(c.L, c.H, c.tail) || tc_smem_bytes(c.L, c.H, c.tail) > 0);
   return false;
 }
 
@@ -136,6 +137,8 @@ extern "C" int sand_create(const sand_config* cfg, sand_ctx** out) {
   }
   ctx->num_sms = prop.multiProcessorCount;
   if (const char* ev = getenv("SAND_PAIR")) ctx->use_pair = std::atoi(ev) != 0;
+  // the CTA-pair kernel keeps its per-column tables in shared memory: large L falls back to the 1-CTA kernel
+  if (cfg->prec == SAND_BF16) ctx->use_pair = ctx->use_pair && tc2_usable(cfg->L, cfg->H, cfg->tail);
   cudaError_t e = prepare_tmlp_kernels(cfg->L, cfg->H, cfg->tail, cfg->prec);
   if (e != cudaSuccess) { fail(ctx, SAND_ERR_CUDA, "kernel attribute setup: %s", cudaGetErrorString(e)); return bail(SAND_ERR_CUDA); }
   *out = ctx;
@@ -259,17 +262,10 @@ extern "C" int sand_load_weights(sand_ctx* ctx, const float* blob, size_t n_floa
     // CTA-pair kernel tables (layout in sand_internal.h MlpDev): per-column scale by sine path
     const int np = tc2_npoly();
     const double kInvPi = 0.31830988618379067;
-    auto scale = [&](int j) { return (j % 16) < np ? (double)w0 * kInvPi : (double)w0; };
-    auto al4 = [](long long v) { return (v + 3) & ~3ll; };
+    // polynomial columns: the first np of every 32 within each epilogue thread's column quarter
+    auto scale = [&](int j) { return ((j % (H / 4)) % 32) < np ? (double)w0 * kInvPi : (double)w0; };
     m.pt_npoly = np;
-    m.pt_off_l1 = 0;
-    m.pt_off_bias = 0;
-    m.pt_off_a = al4(m.pt_off_bias + (long long)L * H);
-    m.pt_off_a1 = al4(m.pt_off_a + (long long)L * H);
-    m.pt_off_c = al4(m.pt_off_a1 + (tail == SAND_TAIL_MULT ? (long long)(L - 1) * H : 0));
-    m.pt_off_c1 = al4(m.pt_off_c + L);
-    m.pt_off_csum = al4(m.pt_off_c1 + L);
-    m.pt_floats = al4(m.pt_off_csum + L + 1);
+    tc2_table_layout(L, H, tail, &m);
     std::vector<float> pt((size_t)m.pt_floats, 0.f);
     for (int i = 1; i < L; ++i)
       for (int j = 0; j < H; ++j) pt[m.pt_off_bias + (size_t)i * H + j] = (float)(scale(j) * b[i][j]);

@@ -62,8 +62,9 @@ struct MlpDev {
   //   a1: [L-1][H] (MULT, i >= 2);  c: [L];  c1: [L-1] (MULT)   -- in this order
   const float* tables;
   long long off_w1, off_bias, off_a, off_c, off_a1, off_c1, tables_floats;
-  // CTA-pair kernel tables (tmlp_tc2.cu), pre-scaled per column for its sine path: of every 16 columns
-  // the first pt_npoly use the FMA-pipe polynomial (scale w0/pi), the rest MUFU.SIN (scale w0):
+  // CTA-pair kernel tables (tmlp_tc2.cu), pre-scaled per column for its sine path: of every BW =
+  // min(32, H/4) columns the first min(pt_npoly, BW) use the FMA-pipe polynomial (scale w0/pi), the rest
+  // MUFU.SIN (scale w0):
   //   bias: [L][H] = scale(col) * b_i, row 0 (i = 1) zero: b_1 rides in the layer-1 MMA
   //   a: [L][H];  a1: [L-1][H] (MULT)
   //   c   : [L] tail biases (MULT: c_i0);  c1: [L] (MULT: c_i1 at index i-1, i >= 2)
@@ -74,7 +75,7 @@ struct MlpDev {
   int pt_npoly;
 };
 
-constexpr int kPairPolyDefault = 4;   // polynomial-sine columns per 16 in the CTA-pair kernel
+constexpr int kPairPolyDefault = 0;   // polynomial-sine columns per 32 in the CTA-pair kernel (0, 8, 16)
 
 cudaError_t launch_tmlp_simt(const MlpDev& m, const float* pts, const uint32_t* perm, const QueryMeta* meta,
                              float* out_sdf, int num_sms, cudaStream_t st);
@@ -90,7 +91,9 @@ size_t simt_smem_bytes(int L, int H, int tail);
 cudaError_t prepare_tmlp_kernels(int L, int H, int tail, int prec);
 // CTA-pair kernel (tmlp_tc2.cu)
 bool tc2_available(int H);
-int tc2_npoly();   // polynomial share in use (SAND_NPOLY env override: 0, 4, 6, 8)
+bool tc2_usable(int L, int H, int tail);           // H supported and the kernel's shared memory fits
+void tc2_table_layout(int L, int H, int tail, MlpDev* m);   // pair-table offsets (pt_off_*, pt_floats)
+int tc2_npoly();   // polynomial columns per 32 in use (SAND_NPOLY env override: 0, 8, 16)
 cudaError_t launch_tmlp_tc2(const MlpDev& m, const float* pts, const uint32_t* perm, const QueryMeta* meta,
                             float* out, int num_sms, cudaStream_t st);
 cudaError_t prepare_tc2(int H, int tail);

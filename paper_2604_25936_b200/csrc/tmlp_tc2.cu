@@ -142,8 +142,8 @@ struct EpiSlot {
   SlotWalk w;
   uint32_t pe;        // acc_full parity
   uint32_t kpar;      // MULT per-step reduction buffer parity
-  float ylin;         // this thread's running partial of the linear tail terms
-  float yprod;        // MULT: sum of the Eq. 3 products (column-quarter 0 only)
+  float ylin[4];      // this thread's running partials of the linear tail terms (its 4 rows)
+  float yprod;        // MULT: sum of the Eq. 3 products (column-quarter 0 warps, row 32 q + lane)
 };
 
 template <int H, int TAIL, int NP>
@@ -438,11 +438,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
     const int ew = warp - 3;
     const int q = warp & 3;                  // TMEM lane quadrant = warp % 4
     const int cq = ew >> 2;                  // column quarter
-    const int row = 32 * q + lane;           // TMEM lane / local A row
+    // TMEM access in the 16x256b shape: thread (quad = lane / 4, tq = lane % 4) owns rows
+    // R_k = 32q + quad + 8k (k = 0..3) and, in every 8-column chunk, columns 2 tq and 2 tq + 1.  Each
+    // per-column table value it loads serves 4 rows (4x fewer shared-memory table reads than one row per
+    // thread), at the price of 4-byte A-operand stores.
+    const int quad = lane >> 2, tq = lane & 3;
     const int c0 = cq * C::HQ;
-    const uint32_t tm_row = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)c0;
-    const uint32_t a_row = sA + (row >> 3) * 1024 + (row & 7) * 128;
-    const uint32_t swz = row & 7;
+    constexpr int BW = 16;                        // columns per TMEM load batch (2 x 8 registers)
+    constexpr int CB = BW / 8;                    // 8-column chunks per batch
+    const uint32_t tm_q = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)c0;
+    const uint32_t a_q = sA + (uint32_t)(4 * q) * 1024 + quad * 128 + 4 * tq;
     const float2 SM2 = make_float2(p.m.omega0, p.m.omega0);
     const float2 SP2 = make_float2(p.m.omega0 * 0.31830988618379067f, p.m.omega0 * 0.31830988618379067f);
     const float* tb = tab + p.m.pt_off_bias;   // [L][H] (row 0 = 0: b_1 is inside the layer-1 MMA)
@@ -464,100 +469,107 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
         else mbar_arrive_remote(afull_dst0 + 8 * s);
       }
     };
+    auto quad_sum = [](float v) {
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      return v;
+    };
 
     // one epilogue step (layer l of the current tile) of slot s
     auto step = [&](EpiSlot& e, const int s) {
       const int d = e.w.d, l = e.w.l;
-      const uint32_t aS = a_row + s * C::A_BYTES;
-      float2 yv = make_float2(0.f, 0.f), yv1 = make_float2(0.f, 0.f);
+      const uint32_t aS = a_q + s * C::A_BYTES;
+      float2 yv[4], yv1[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) { yv[k] = make_float2(0.f, 0.f); yv1[k] = make_float2(0.f, 0.f); }
       const long long c0_ = p.prof ? clock64() : 0;
       mbar_wait(b_accfull + 8 * s, e.pe);
       const long long c1_ = p.prof ? clock64() : 0;
       e.pe ^= 1u;
       tc_fence_after();
       const bool store = l != d;
-      const float* bias = tb + (l - 1) * H;
-      const float* a = ta + (l - 1) * H;
-      const float* a1 = ta1 + (l - 2) * H;
+      const float* bias = tb + (l - 1) * H + c0 + 2 * tq;
+      const float* a = ta + (l - 1) * H + c0 + 2 * tq;
+      const float* a1 = ta1 + (l - 2) * H + c0 + 2 * tq;
       const bool prod = TAIL == SAND_TAIL_MULT && l >= 2;
-      const uint32_t tm = tm_row + (uint32_t)(s * H);
-      // TMEM loads in 32-column batches (two 16-column groups per wait): half the exposed load latencies
-      uint32_t rr[32];
+      const uint32_t tm = tm_q + (uint32_t)(s * H);
 #pragma unroll
-      for (int g = 0; g < C::NG; ++g) {
-        if ((g & 1) == 0) {
-          if (g + 1 < C::NG) {
-            tmem_ld32(tm + 16 * g, rr);
-            tmem_wait_ld_dep(rr);
-          } else {
-            uint32_t (&r16)[16] = *reinterpret_cast<uint32_t(*)[16]>(rr);
-            tmem_ld16(tm + 16 * g, r16);
-            tmem_wait_ld_dep(r16);
-          }
-        }
-        const uint32_t (&r)[16] = *reinterpret_cast<const uint32_t(*)[16]>(rr + 16 * (g & 1));
-        uint32_t pk[8];
+      for (int bb = 0; bb < C::HQ / BW; ++bb) {
+        uint32_t r0[4 * CB], r1[4 * CB];   // lane block 0 (rows R0, R1) and block 1 (rows R2, R3)
+        tmem_ld_16x256b<CB>(tm + bb * BW, r0);
+        tmem_ld_16x256b<CB>(tm + (16u << 16) + bb * BW, r1);
+        tmem_wait_ld_dep(r0);
+        tmem_wait_ld_dep(r1);
 #pragma unroll
-        for (int qd = 0; qd < 4; ++qd) {
-          const int j4 = c0 + 16 * g + 4 * qd;
-          const float4 b4 = *reinterpret_cast<const float4*>(bias + j4);
-          const float4 a4 = *reinterpret_cast<const float4*>(a + j4);
-          float4 c4 = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (TAIL == SAND_TAIL_MULT && prod) c4 = *reinterpret_cast<const float4*>(a1 + j4);
+        for (int i = 0; i < CB; ++i) {
+          const int jc = bb * BW + 8 * i;     // chunk column offset within this column quarter
+          const float2 b2 = *reinterpret_cast<const float2*>(bias + jc);
+          const float2 a2 = *reinterpret_cast<const float2*>(a + jc);
+          float2 c2 = make_float2(0.f, 0.f);
+          if (TAIL == SAND_TAIL_MULT && prod) c2 = *reinterpret_cast<const float2*>(a1 + jc);
+          const uint32_t u = (uint32_t)((c0 + jc) >> 3);
+          const uint32_t st_addr = aS + (u >> 3) * C::A_CHUNK + ((((u & 7u) ^ (uint32_t)quad)) << 4);
 #pragma unroll
-          for (int hp = 0; hp < 2; ++hp) {
-            const int pr = 2 * qd + hp;
-            const float2 b2 = hp ? make_float2(b4.z, b4.w) : make_float2(b4.x, b4.y);
-            const float2 acc = make_float2(__uint_as_float(r[2 * pr]), __uint_as_float(r[2 * pr + 1]));
+          for (int k = 0; k < 4; ++k) {
+            const uint32_t (&r)[4 * CB] = k < 2 ? r0 : r1;
+            const int o = 4 * i + 2 * (k & 1);
+            const float2 acc = make_float2(__uint_as_float(r[o]), __uint_as_float(r[o + 1]));
             float2 h;
-            if (2 * pr < NP) {
+            if (((bb * BW + 8 * i) & 31) < NP) {   // polynomial sine on the first NP of every 32 columns
               h = sin_poly2(__ffma2_rn(acc, SP2, b2));
             } else {
               const float2 z = __ffma2_rn(acc, SM2, b2);
               h = make_float2(__sinf(z.x), __sinf(z.y));
             }
-            yv = __ffma2_rn(hp ? make_float2(a4.z, a4.w) : make_float2(a4.x, a4.y), h, yv);
-            if (TAIL == SAND_TAIL_MULT)
-              yv1 = __ffma2_rn(hp ? make_float2(c4.z, c4.w) : make_float2(c4.x, c4.y), h, yv1);
-            pk[pr] = pack_bf16x2(h.x, h.y);
+            yv[k] = __ffma2_rn(a2, h, yv[k]);
+            if (TAIL == SAND_TAIL_MULT) yv1[k] = __ffma2_rn(c2, h, yv1[k]);
+            if (store) st_shared_b32(st_addr + (uint32_t)k * 1024, pack_bf16x2(h.x, h.y));
           }
-        }
-        if (store) {
-          const uint32_t u = (uint32_t)(c0 / 8 + 2 * g);
-          st_shared_v4(aS + (u >> 3) * C::A_CHUNK + (((u & 7u) ^ swz) << 4), pk[0], pk[1], pk[2], pk[3]);
-          st_shared_v4(aS + ((u + 1) >> 3) * C::A_CHUNK + ((((u + 1) & 7u) ^ swz) << 4), pk[4], pk[5], pk[6],
-                       pk[7]);
         }
       }
       if (prod) {
-        // Eq. 3: t_l = (a_l0 . h + c_l0)(a_l1 . h + c_l1) needs both full dot products of the row
+        // Eq. 3: t_l = (a_l0 . h + c_l0)(a_l1 . h + c_l1) needs both full dot products of the row:
+        // sum over the quad (4 column pairs), then over the 4 column quarters through shared memory
         float2* rb2 = red2 + ((s * 2 + e.kpar) * 4) * 128;
-        rb2[cq * 128 + row] = make_float2(yv.x + yv.y, yv1.x + yv1.y);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float s0 = quad_sum(yv[k].x + yv[k].y), s1 = quad_sum(yv1[k].x + yv1[k].y);
+          if (tq == 0) rb2[cq * 128 + 32 * q + quad + 8 * k] = make_float2(s0, s1);
+        }
         named_bar_sync(bar_q, 128);
         if (cq == 0) {
+          const int rowl = 32 * q + lane;
           float s0 = tc0[l - 1], s1 = tc1[l - 1];
 #pragma unroll
-          for (int k = 0; k < 4; ++k) { const float2 v = rb2[k * 128 + row]; s0 += v.x; s1 += v.y; }
+          for (int k = 0; k < 4; ++k) { const float2 v = rb2[k * 128 + rowl]; s0 += v.x; s1 += v.y; }
           e.yprod += s0 * s1;
         }
         e.kpar ^= 1u;
       } else {
-        e.ylin += yv.x + yv.y;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) e.ylin[k] += yv[k].x + yv[k].y;
       }
       if (l == d) {
-        // tile end: reduce the four column quarters of every row (per-quadrant barrier); column quarter
-        // 0 adds the tail-bias prefix sum and hands y_d to the IO warp.  Done before this step's
-        // publish, so the next tile's MMA (and its tile end) cannot overwrite `part` before it is read.
+        // tile end: reduce every row over its quad and over the four column quarters (per-quadrant
+        // barrier); column quarter 0 adds the tail-bias prefix sum (and, MULT, the Eq. 3 products) and
+        // hands y_d to the IO warp.  Done before this step's publish, so the next tile's MMA (and its
+        // tile end) cannot overwrite `part` before it is read.
         float* pq = part + s * 4 * 128;
-        pq[cq * 128 + row] = e.ylin + e.yprod;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float v = quad_sum(e.ylin[k]);
+          if (tq == 0) pq[cq * 128 + 32 * q + quad + 8 * k] = v;
+          e.ylin[k] = 0.f;
+        }
         named_bar_sync(bar_q, 128);
         if (cq == 0) {
           const int b = e.w.ti & 1;
-          out_y[(s * 2 + b) * 128 + row] = tcs[d] + pq[row] + pq[128 + row] + pq[256 + row] + pq[384 + row];
+          const int rowl = 32 * q + lane;
+          out_y[(s * 2 + b) * 128 + rowl] =
+              tcs[d] + e.yprod + pq[rowl] + pq[128 + rowl] + pq[256 + rowl] + pq[384 + rowl];
           __syncwarp();
           if (lane == 0) mbar_arrive(b_iodone + 8 * (s * 2 + b));
         }
-        e.ylin = 0.f;
         e.yprod = 0.f;
       }
       publish(s, store);
@@ -569,7 +581,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
     e0.w.start(pair, T, s_tile_end, L);
     e1.w.start(pair + npairs, T, s_tile_end, L);
     e0.pe = e1.pe = 0; e0.kpar = e1.kpar = 0;
-    e0.ylin = e1.ylin = e0.yprod = e1.yprod = 0.f;
+    e0.yprod = e1.yprod = 0.f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) e0.ylin[k] = e1.ylin[k] = 0.f;
     const long long t_start = p.prof ? clock64() : 0;
 #pragma unroll 1
     while (!(e0.w.done && e1.w.done)) {
@@ -614,13 +628,37 @@ static int pick_nst2(long long pt_floats, int L, int tail) {
 
 bool tc2_available(int H) { return H == 64 || H == 128 || H == 256; }
 
+void tc2_table_layout(int L, int H, int tail, MlpDev* m) {
+  auto al4 = [](long long v) { return (v + 3) & ~3ll; };
+  m->pt_off_l1 = 0;
+  m->pt_off_bias = 0;
+  m->pt_off_a = al4(m->pt_off_bias + (long long)L * H);
+  m->pt_off_a1 = al4(m->pt_off_a + (long long)L * H);
+  m->pt_off_c = al4(m->pt_off_a1 + (tail == SAND_TAIL_MULT ? (long long)(L - 1) * H : 0));
+  m->pt_off_c1 = al4(m->pt_off_c + L);
+  m->pt_off_csum = al4(m->pt_off_c1 + L);
+  m->pt_floats = al4(m->pt_off_csum + L + 1);
+}
+
+bool tc2_usable(int L, int H, int tail) {
+  if (!tc2_available(H)) return false;
+  MlpDev m{};
+  tc2_table_layout(L, H, tail, &m);
+  switch (H) {
+    case 64: return pick_nst2<64>(m.pt_floats, L, tail) > 0;
+    case 128: return pick_nst2<128>(m.pt_floats, L, tail) > 0;
+    case 256: return pick_nst2<256>(m.pt_floats, L, tail) > 0;
+    default: return false;
+  }
+}
+
 int tc2_npoly() {
   static int np = -1;
   if (np < 0) {
     np = kPairPolyDefault;
     if (const char* ev = getenv("SAND_NPOLY")) {
       const int v = atoi(ev);
-      if (v == 0 || v == 4 || v == 6 || v == 8) np = v;
+      if (v == 0 || v == 8 || v == 16) np = v;
     }
   }
   return np;
@@ -680,7 +718,7 @@ static cudaError_t prep_tc2_t() {
   return cudaFuncSetAttribute(k_tmlp_tc2<H, TAIL, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax2);
 }
 
-// The polynomial share is a template parameter; the bench configuration (H = 256, LINEAR) is built for
+// The polynomial share (columns per 32 on the FMA-pipe sine) is a template parameter; the bench configuration (H = 256, LINEAR) is built for
 // every supported share (tuning), the others for the default share only.
 #define SAND_TC2_DISPATCH(FN, ...)                                                                    \
   do {                                                                                                \
@@ -688,10 +726,9 @@ static cudaError_t prep_tc2_t() {
     const int np = m_np;                                                                              \
     if (m_H == 256 && !mult) {                                                                        \
       switch (np) {                                                                                   \
-        case 0: return FN<256, 0, 0>(__VA_ARGS__);                                                    \
-        case 4: return FN<256, 0, 4>(__VA_ARGS__);                                                    \
-        case 6: return FN<256, 0, 6>(__VA_ARGS__);                                                    \
-        default: return FN<256, 0, 8>(__VA_ARGS__);                                                   \
+        case 8: return FN<256, 0, 8>(__VA_ARGS__);                                                    \
+        case 16: return FN<256, 0, 16>(__VA_ARGS__);                                                  \
+        default: return FN<256, 0, 0>(__VA_ARGS__);                                                   \
       }                                                                                               \
     }                                                                                                 \
     if (np != kPairPolyDefault) return cudaErrorInvalidValue;                                          \
