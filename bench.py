@@ -134,6 +134,15 @@ def run_reference(args):
     return 0
 
 
+def _traffic():
+    """DRAM bytes per K3 launch from the committed ncu --set full capture (profiles/), or None."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "r01_k3_traffic.json")))
+        return t["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
 def _cores():
     try:
         from threadpoolctl import threadpool_info
@@ -164,7 +173,7 @@ def cpu_baseline(p, depthmap, pts, budget_s):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="sand", choices=["sand", "reference"])
     ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4"])
@@ -303,13 +312,14 @@ def main():
                        "global_points": summ["n_total"], "parallelism": f"dp{ws} (z-slab shards)",
                        "l2": f"inputs {12 * n / 1e9:.2f} GB per rank > 126 MB L2; no flush needed",
                        "full_depth_baseline": bool(args.full_depth)},
-            "roofline": {"bound": "tensor", "kernel": "k_tmlp_tc (K3 fused T-MLP)", "achieved": ach,
+            "roofline": {"bound": "tensor", "kernel": "k_tmlp_tc2 (K3 fused T-MLP, CTA pair)", "achieved": ach,
                          "peak": pk["bf16"], "unit": "TFLOP/s", "frac": ach / pk["bf16"],
                          "peak_source": pk["src"] + " bf16_tflops (burst)",
-                         "frac_vs_sustained": ach / pk["bf16_sus"], "traffic": None,
+                         "frac_vs_sustained": ach / pk["bf16_sus"], "traffic": _traffic(),
                          "algorithmic_flops_per_launch": f_exec_rank0,
                          "flops_formula": "executed H x H FLOPs sum_p (d_p - 1) * 2 H^2 (Eq. 2 reading R3)",
-                         "ms_per_launch": ms_mlp},
+                         "ms_per_launch": ms_mlp,
+                         "traffic_source": "profiles/r01_k3_traffic.json (ncu --set full, dram read+write per launch)"},
             "tensor_frac_step": f_exec / (ms_step / 1e3) / 1e12 / pk["bf16"],
             "tensor_frac_ns_formula": f_ns / (ms_step / 1e3) / 1e12 / pk["bf16"],
             "flops_exec_per_step": f_exec, "flops_ns_per_step": f_ns,
