@@ -447,7 +447,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
     constexpr int BW = 16;                        // columns per TMEM load batch (2 x 8 registers)
     constexpr int CB = BW / 8;                    // 8-column chunks per batch
     const uint32_t tm_q = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)c0;
-    const uint32_t a_q = sA + (uint32_t)(4 * q) * 1024 + quad * 128 + 4 * tq;
+    const uint32_t a_st = sA + (uint32_t)(4 * q + (lane >> 3)) * 1024 + (uint32_t)(lane & 7) * 128;
     const float2 SM2 = make_float2(p.m.omega0, p.m.omega0);
     const float2 SP2 = make_float2(p.m.omega0 * 0.31830988618379067f, p.m.omega0 * 0.31830988618379067f);
     const float* tb = tab + p.m.pt_off_bias;   // [L][H] (row 0 = 0: b_1 is inside the layer-1 MMA)
@@ -478,7 +478,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
     // one epilogue step (layer l of the current tile) of slot s
     auto step = [&](EpiSlot& e, const int s) {
       const int d = e.w.d, l = e.w.l;
-      const uint32_t aS = a_q + s * C::A_BYTES;
+      const uint32_t aSt = a_st + s * C::A_BYTES;
       float2 yv[4], yv1[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) { yv[k] = make_float2(0.f, 0.f); yv1[k] = make_float2(0.f, 0.f); }
@@ -508,7 +508,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
           float2 c2 = make_float2(0.f, 0.f);
           if (TAIL == SAND_TAIL_MULT && prod) c2 = *reinterpret_cast<const float2*>(a1 + jc);
           const uint32_t u = (uint32_t)((c0 + jc) >> 3);
-          const uint32_t st_addr = aS + (u >> 3) * C::A_CHUNK + ((((u & 7u) ^ (uint32_t)quad)) << 4);
+          uint32_t pk[4];
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const uint32_t (&r)[4 * CB] = k < 2 ? r0 : r1;
@@ -523,8 +523,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
             }
             yv[k] = __ffma2_rn(a2, h, yv[k]);
             if (TAIL == SAND_TAIL_MULT) yv1[k] = __ffma2_rn(c2, h, yv1[k]);
-            if (store) st_shared_b32(st_addr + (uint32_t)k * 1024, pack_bf16x2(h.x, h.y));
+            pk[k] = pack_bf16x2(h.x, h.y);
           }
+          // the 4 rows x 8 columns of this chunk are four 8x8 b16 matrices in the m8n8 fragment layout:
+          // one stmatrix.x4 (lane provides the address of row lane % 8 of matrix lane / 8)
+          if (store) stmatrix_x4(aSt + (u >> 3) * C::A_CHUNK + (((u & 7u) ^ (uint32_t)(lane & 7)) << 4), pk);
         }
       }
       if (prod) {
