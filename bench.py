@@ -326,7 +326,7 @@ def main():
             "stage_ms": {"lookup": ms_lookup, "bin": ms_bin, "mlp": ms_mlp},
             "per_depth": per_depth,
             "e2e": e2e, "cpu_baseline": cpu,
-            "gpu_launches": 4 * args.steps * ws,
+            "gpu_launches": 6 * args.steps * ws,   # lookup, scan x3, scatter, T-MLP per query
             "clocks": clocks,
             "hbm_lookup_gbs": (13.0 * n) / (ms_lookup / 1e3) / 1e9 if ms_lookup > 0 else None,
         }

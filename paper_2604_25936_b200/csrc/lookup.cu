@@ -147,50 +147,73 @@ __device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long
   return wpre + inc - v;
 }
 
-__global__ void __launch_bounds__(1024) k_scan(const uint32_t* __restrict__ hist, long long nblk, int L,
-                                               int tile_rows, uint32_t* __restrict__ offs,
-                                               QueryMeta* __restrict__ meta) {
-  __shared__ long long counts[kMaxBins];
-  const long long per = (nblk + blockDim.x - 1) / blockDim.x;
-  const long long b0 = threadIdx.x * per;
-  const long long b1 = (b0 + per < nblk) ? b0 + per : nblk;
-  unsigned long long running = 0;
-  // depth-0 and non-finite bins: totals only
-  for (int bin = 0; bin < L + 2; ++bin) {
-    unsigned long long s = 0;
-    for (long long b = b0; b < b1; ++b) s += hist[(long long)bin * nblk + b];
-    unsigned long long tot;
-    (void)block_excl_scan(s, &tot);
-    if (threadIdx.x == 0) counts[bin] = (long long)tot;
+// K2a, in three coalesced passes over the (L+2) x nblk histogram (bin-major):
+//   k_scan_partial: per (bin, chunk of kScanChunk blocks) sums
+//   k_scan_top    : bin totals, deepest-first starts, per-(depth, chunk) prefixes, the tile table
+//   k_scan_offs   : per block exclusive prefix within its chunk + chunk prefix -> offs[d][b]
+constexpr int kScanThreads = 1024;
+constexpr int kScanPer = 8;                           // histogram entries per thread
+constexpr int kScanChunk = kScanThreads * kScanPer;   // blocks per chunk
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_partial(const uint32_t* __restrict__ hist, long long nblk,
+                                                                unsigned long long* __restrict__ part, int nchunk) {
+  const int bin = blockIdx.y, c = blockIdx.x;
+  const long long b0 = (long long)c * kScanChunk + (long long)threadIdx.x * kScanPer;
+  unsigned long long s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k)
+    if (b0 + k < nblk) s += hist[(long long)bin * nblk + b0 + k];
+  unsigned long long tot;
+  (void)block_excl_scan(s, &tot);
+  if (threadIdx.x == 0) part[(long long)bin * nchunk + c] = tot;
+}
+
+__global__ void k_scan_top(const unsigned long long* __restrict__ part, int nchunk, int L, int tile_rows,
+                           unsigned long long* __restrict__ cpre, QueryMeta* __restrict__ meta) {
+  if (threadIdx.x != 0) return;
+  long long counts[kMaxBins];
+  for (int b = 0; b < kMaxBins; ++b) {
+    long long t = 0;
+    if (b < L + 2)
+      for (int c = 0; c < nchunk; ++c) t += (long long)part[(long long)b * nchunk + c];
+    counts[b] = t;
+    meta->count[b] = t;
+    meta->start[b] = 0;
+    meta->tile_begin[b] = meta->tile_end[b] = 0;
   }
-  __syncthreads();
-  // deepest-first scatter offsets
-  for (int d = L; d >= 1; --d) {
-    unsigned long long s = 0;
-    for (long long b = b0; b < b1; ++b) s += hist[(long long)d * nblk + b];
-    unsigned long long tot;
-    unsigned long long ex = block_excl_scan(s, &tot) + running;
-    for (long long b = b0; b < b1; ++b) {
-      offs[(long long)d * nblk + b] = (uint32_t)ex;
-      ex += hist[(long long)d * nblk + b];
+  long long running = 0, tb = 0;
+  for (int d = L; d >= 1; --d) {   // deepest first
+    meta->start[d] = running;
+    for (int c = 0; c < nchunk; ++c) {
+      cpre[(long long)d * nchunk + c] = (unsigned long long)running;
+      running += (long long)part[(long long)d * nchunk + c];
     }
-    if (threadIdx.x == 0) meta->start[d] = (long long)running;
-    running += tot;
+    meta->tile_begin[d] = tb;
+    tb += (counts[d] + tile_rows - 1) / tile_rows;
+    meta->tile_end[d] = tb;
   }
-  if (threadIdx.x == 0) {
-    long long tb = 0;
-    for (int b = 0; b < kMaxBins; ++b) {
-      meta->count[b] = (b < L + 2) ? counts[b] : 0;
-      meta->tile_begin[b] = meta->tile_end[b] = 0;
-    }
-    meta->start[0] = 0;
-    for (int d = L; d >= 1; --d) {
-      meta->tile_begin[d] = tb;
-      tb += (counts[d] + tile_rows - 1) / tile_rows;
-      meta->tile_end[d] = tb;
-    }
-    meta->total_tiles = tb;
-    meta->tile_rows = tile_rows;
+  meta->total_tiles = tb;
+  meta->tile_rows = tile_rows;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_offs(const uint32_t* __restrict__ hist, long long nblk,
+                                                             const unsigned long long* __restrict__ cpre,
+                                                             int nchunk, uint32_t* __restrict__ offs) {
+  const int d = blockIdx.y + 1, c = blockIdx.x;
+  const long long b0 = (long long)c * kScanChunk + (long long)threadIdx.x * kScanPer;
+  uint32_t v[kScanPer];
+  unsigned long long s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k) {
+    v[k] = (b0 + k < nblk) ? hist[(long long)d * nblk + b0 + k] : 0u;
+    s += v[k];
+  }
+  unsigned long long tot;
+  unsigned long long ex = block_excl_scan(s, &tot) + cpre[(long long)d * nchunk + c];
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k) {
+    if (b0 + k < nblk) offs[(long long)d * nblk + b0 + k] = (uint32_t)ex;
+    ex += v[k];
   }
 }
 
@@ -301,9 +324,19 @@ cudaError_t launch_lookup(const float* pts, long long n, const LookupParams& lp,
   return cudaGetLastError();
 }
 
+long long scan_scratch_words(long long nblk) {
+  const long long nchunk = (nblk + kScanChunk - 1) / kScanChunk;
+  return 2 * (long long)kMaxBins * (nchunk > 0 ? nchunk : 1);
+}
+
 cudaError_t launch_scan(const uint32_t* hist, long long nblk, int L, int tile_rows, uint32_t* offs,
-                        QueryMeta* meta, cudaStream_t st) {
-  k_scan<<<1, 1024, 0, st>>>(hist, nblk, L, tile_rows, offs, meta);
+                        QueryMeta* meta, unsigned long long* scratch, cudaStream_t st) {
+  const int nchunk = (int)((nblk + kScanChunk - 1) / kScanChunk);
+  unsigned long long* part = scratch;
+  unsigned long long* cpre = scratch + (long long)kMaxBins * nchunk;
+  k_scan_partial<<<dim3(nchunk, L + 2), kScanThreads, 0, st>>>(hist, nblk, part, nchunk);
+  k_scan_top<<<1, 32, 0, st>>>(part, nchunk, L, tile_rows, cpre, meta);
+  k_scan_offs<<<dim3(nchunk, L), kScanThreads, 0, st>>>(hist, nblk, cpre, nchunk, offs);
   return cudaGetLastError();
 }
 

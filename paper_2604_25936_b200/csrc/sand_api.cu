@@ -50,6 +50,7 @@ struct sand_ctx {
   long long cap_n = 0, cap_nblk = 0;
   uint32_t* d_hist = nullptr;
   uint32_t* d_offs = nullptr;
+  unsigned long long* d_scan = nullptr;
   uint32_t* d_perm = nullptr;
   QueryMeta* d_meta = nullptr;
   // timing: one event quad per query since the last sand_get_stats (grown on demand; never
@@ -146,7 +147,7 @@ extern "C" int sand_create(const sand_config* cfg, sand_ctx** out) {
 }
 
 static void free_workspace(sand_ctx* c) {
-  dfree(c->d_hist); dfree(c->d_offs); dfree(c->d_perm); dfree(c->d_meta);
+  dfree(c->d_hist); dfree(c->d_offs); dfree(c->d_scan); dfree(c->d_perm); dfree(c->d_meta);
   c->cap_n = c->cap_nblk = 0;
 }
 static void free_depthmap(sand_ctx* c) {
@@ -476,6 +477,7 @@ static int ensure_workspace(sand_ctx* ctx, long long n) {
   free_workspace(ctx);
   CU(cudaMalloc(&ctx->d_hist, sizeof(uint32_t) * (size_t)nblk * kMaxBins));
   CU(cudaMalloc(&ctx->d_offs, sizeof(uint32_t) * (size_t)nblk * kMaxBins));
+  CU(cudaMalloc(&ctx->d_scan, sizeof(unsigned long long) * (size_t)scan_scratch_words(nblk)));
   CU(cudaMalloc(&ctx->d_perm, sizeof(uint32_t) * (size_t)std::max(n, 1ll)));
   CU(cudaMalloc(&ctx->d_meta, sizeof(QueryMeta)));
   ctx->cap_n = n;
@@ -517,7 +519,7 @@ extern "C" int sand_query(sand_ctx* ctx, const float* d_points, int64_t n, float
   CU(launch_lookup(d_points, n, lp, d_depth, d_sdf, ctx->d_hist, nblk, st));
   CU(cudaEventRecord(ev[1], st));
   CU(launch_scan(ctx->d_hist, nblk, ctx->cfg.L, tmlp_tile_rows(ctx->cfg.H, ctx->cfg.prec, ctx->use_pair), ctx->d_offs,
-                 ctx->d_meta, st));
+                 ctx->d_meta, ctx->d_scan, st));
   CU(launch_scatter(d_depth, n, ctx->cfg.L, ctx->d_offs, ctx->d_perm, nblk, st));
   CU(cudaEventRecord(ev[2], st));
   if (ctx->cfg.prec == SAND_FP32)

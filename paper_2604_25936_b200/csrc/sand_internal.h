@@ -39,7 +39,8 @@ struct LookupParams {
 cudaError_t launch_lookup(const float* pts, long long n, const LookupParams& lp, uint8_t* out_depth,
                           float* out_sdf, uint32_t* hist, long long nblk, cudaStream_t st);
 cudaError_t launch_scan(const uint32_t* hist, long long nblk, int L, int tile_rows, uint32_t* offs,
-                        QueryMeta* meta, cudaStream_t st);
+                        QueryMeta* meta, unsigned long long* scratch, cudaStream_t st);
+long long scan_scratch_words(long long nblk);   // u64 words of scratch launch_scan needs
 cudaError_t launch_scatter(const uint8_t* depth, long long n, int L, const uint32_t* offs, uint32_t* perm,
                            long long nblk, cudaStream_t st);
 cudaError_t launch_bake_octree(const uint32_t* nodes, const uint8_t* leaf_depth, const float* leaf_far,
