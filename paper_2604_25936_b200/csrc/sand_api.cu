@@ -262,7 +262,7 @@ extern "C" int sand_load_weights(sand_ctx* ctx, const float* blob, size_t n_floa
   if (ctx->cfg.prec == SAND_BF16 && tc2_available(H)) {
     // CTA-pair kernel tables (layout in sand_internal.h MlpDev): per-column scale by sine path
     const int np = tc2_npoly();
-    const double kInvPi = 0.31830988618379067;
+    const double kInvPi = 0.15915494309189535;   // 1 / (2 pi): the polynomial takes z in turns
     // polynomial columns: the first np of every 32 within each epilogue thread's column quarter
     auto scale = [&](int j) { return ((j % (H / 4)) % 32) < np ? (double)w0 * kInvPi : (double)w0; };
     m.pt_npoly = np;

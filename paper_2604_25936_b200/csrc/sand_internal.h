@@ -64,7 +64,7 @@ struct MlpDev {
   const float* tables;
   long long off_w1, off_bias, off_a, off_c, off_a1, off_c1, tables_floats;
   // CTA-pair kernel tables (tmlp_tc2.cu), pre-scaled per column for its sine path: of every BW =
-  // min(32, H/4) columns the first min(pt_npoly, BW) use the FMA-pipe polynomial (scale w0/pi), the rest
+  // min(32, H/4) columns the first min(pt_npoly, BW) use the FMA-pipe polynomial (scale w0/(2 pi)), the rest
   // MUFU.SIN (scale w0):
   //   bias: [L][H] = scale(col) * b_i, row 0 (i = 1) zero: b_1 rides in the layer-1 MMA
   //   a: [L][H];  a1: [L-1][H] (MULT)

@@ -26,7 +26,7 @@
 // Sine split: of every 16 accumulator columns the first NP go through an odd
 // degree-7 polynomial on the FMA pipe (range reduction to [-pi/2, pi/2] by a magic-number round), the
 // rest through MUFU.SIN, so MUFU and FMA pipes share the transcendental load.  Bias tables are
-// pre-scaled on the host for the path their column takes (w0 or w0/pi).
+// pre-scaled on the host for the path their column takes (w0 or w0/(2 pi)).
 //
 // Tails: LINEAR tails sum linearly over layers, so every thread keeps a running partial over its columns;
 // the IO warp adds the four column quarters of a row and the tail-bias prefix sum csum[d] once per tile.
@@ -111,25 +111,20 @@ struct SlotWalk {
 };
 
 // ------------------------------------------------------------------------------ sine paths
-// Polynomial path: u = z / pi (pre-scaled), k = rint(u) by the 1.5 * 2^23 magic add, r = u - k in
-// [-1/2, 1/2], sin(z) = (-1)^k sin(pi r), sin(pi r) = r (C1 + C3 r^2 + C5 r^4 + C7 r^6)
-// (near-minimax on [-1/2, 1/2]; |error| < 8e-7 in FP32, below MUFU.SIN's).
+// Polynomial path (FMA pipe only): u = z / (2 pi) (pre-scaled), k = rint(u) by the 1.5 * 2^23 magic add,
+// r = u - k in [-1/2, 1/2], sin(z) = sin(2 pi r) = r (C1 + C3 r^2 + ... + C9 r^8), an odd degree-9
+// near-minimax fit on [-1/2, 1/2] (|error| < 7e-6 in FP32; the BF16 rounding of h is 2^-9 relative).
 __device__ __forceinline__ float2 sin_poly2(float2 u) {
   const float2 M = make_float2(12582912.0f, 12582912.0f);
   const float2 t = __fadd2_rn(u, M);
   const float2 k = __fadd2_rn(t, make_float2(-12582912.0f, -12582912.0f));
-  float2 r = __ffma2_rn(k, make_float2(-1.0f, -1.0f), u);
-  // odd k -> negate r (sin is odd): sign bit from the parity bit of t's mantissa
-  uint32_t sx, sy;
-  asm("shf.l.wrap.b32 %0, %1, %1, 31;" : "=r"(sx) : "r"(__float_as_uint(t.x)));
-  asm("shf.l.wrap.b32 %0, %1, %1, 31;" : "=r"(sy) : "r"(__float_as_uint(t.y)));
-  r.x = __uint_as_float(__float_as_uint(r.x) ^ (sx & 0x80000000u));
-  r.y = __uint_as_float(__float_as_uint(r.y) ^ (sy & 0x80000000u));
+  const float2 r = __ffma2_rn(k, make_float2(-1.0f, -1.0f), u);
   const float2 r2 = __fmul2_rn(r, r);
-  float2 p = __ffma2_rn(r2, make_float2(-0.5546384453773499f, -0.5546384453773499f),
-                        make_float2(2.5418999195098877f, 2.5418999195098877f));
-  p = __ffma2_rn(p, r2, make_float2(-5.167142868041992f, -5.167142868041992f));
-  p = __ffma2_rn(p, r2, make_float2(3.1415820121765137f, 3.1415820121765137f));
+  float2 p = __ffma2_rn(r2, make_float2(32.783390045166016f, 32.783390045166016f),
+                        make_float2(-74.4790267944336f, -74.4790267944336f));
+  p = __ffma2_rn(p, r2, make_float2(81.36698913574219f, 81.36698913574219f));
+  p = __ffma2_rn(p, r2, make_float2(-41.33122634887695f, -41.33122634887695f));
+  p = __ffma2_rn(p, r2, make_float2(6.283055782318115f, 6.283055782318115f));
   return __fmul2_rn(p, r);
 }
 
@@ -449,7 +444,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
     const uint32_t tm_q = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)c0;
     const uint32_t a_st = sA + (uint32_t)(4 * q + (lane >> 3)) * 1024 + (uint32_t)(lane & 7) * 128;
     const float2 SM2 = make_float2(p.m.omega0, p.m.omega0);
-    const float2 SP2 = make_float2(p.m.omega0 * 0.31830988618379067f, p.m.omega0 * 0.31830988618379067f);
+    const float2 SP2 = make_float2(p.m.omega0 * 0.15915494309189535f, p.m.omega0 * 0.15915494309189535f);
     const float* tb = tab + p.m.pt_off_bias;   // [L][H] (row 0 = 0: b_1 is inside the layer-1 MMA)
     const float* ta = tab + p.m.pt_off_a;      // [L][H]
     const float* ta1 = tab + p.m.pt_off_a1;    // [L-1][H] (MULT)
