@@ -163,12 +163,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
   const uint32_t sA1 = sW1 + C::W1_HALF;                          // [slot] layer-1 A operand
   float* tab = reinterpret_cast<float*>(gbase + ((sA1 + NSLOT * C::A1_BYTES) - base));
   const long long ntab = p.m.pt_floats;
-  float* part = tab + ((ntab + 3) & ~3ll);                        // [slot][cq][128] tile-end partials
-  float* out_y = part + NSLOT * 4 * 128;                          // [slot][buf][128] finished y_d
-  float2* red2 = reinterpret_cast<float2*>(out_y + NSLOT * 2 * 128);   // MULT: [slot][kpar][cq][128]
+  constexpr int NPL = TAIL == SAND_TAIL_MULT ? 5 : 4;   // partial planes: 4 column quarters (+ Eq. 3 products)
+  float* part = tab + ((ntab + 3) & ~3ll);                        // [slot][plane][128] tile-end partials
+  float2* red2 = reinterpret_cast<float2*>(part + NSLOT * NPL * 128);   // MULT: [slot][kpar][cq][128]
   const int red2_floats = (TAIL == SAND_TAIL_MULT) ? NSLOT * 2 * 4 * 128 * 2 : 0;
   const int nb = L + 2;
-  long long* meta_s = reinterpret_cast<long long*>(out_y + NSLOT * 2 * 128 + red2_floats);
+  long long* meta_s = reinterpret_cast<long long*>(part + NSLOT * NPL * 128 + red2_floats);
   long long* s_tile_end = meta_s;
   long long* s_tile_begin = meta_s + nb;
   long long* s_start = meta_s + 2 * nb;
@@ -181,8 +181,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
   const uint32_t b_accfull = b_afull + 8 * NSLOT;       // [slot]  accumulator ready
   const uint32_t b_a1full = b_accfull + 8 * NSLOT;      // [slot]  layer-1 A written (leader: 2 arrivals)
   const uint32_t b_a1free = b_a1full + 8 * NSLOT;       // [slot]  layer-1 MMA done with the A1 buffer
-  const uint32_t b_iodone = b_a1free + 8 * NSLOT;       // [slot][buf] y_d of a tile in out_y
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * nst + 7 * NSLOT);
+  const uint32_t b_iodone = b_a1free + 8 * NSLOT;       // [slot]  all epilogue warps wrote their partials
+  const uint32_t b_partfree = b_iodone + 8 * NSLOT;     // [slot]  IO warp has read the partials
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * nst + 7 * NSLOT);   // (3 nst + 7 NSLOT) barriers
 #ifdef SAND_HANG_DEBUG
   if (blockIdx.x == 0 && threadIdx.x == 0)
     printf("[bars] wfull 0x%x wempty 0x%x wpeer 0x%x afull 0x%x accfull 0x%x a1full 0x%x a1free 0x%x iodone 0x%x\n",
@@ -216,7 +217,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
     // a_full: one arrive per epilogue warp of both CTAs
     for (int s = 0; s < NSLOT; ++s) { mbar_init(b_afull + 8 * s, 2 * kEpiWarps); mbar_init(b_accfull + 8 * s, 1); }
     for (int s = 0; s < NSLOT; ++s) { mbar_init(b_a1full + 8 * s, 2); mbar_init(b_a1free + 8 * s, 1); }
-    for (int i = 0; i < 2 * NSLOT; ++i) mbar_init(b_iodone + 8 * i, 4);   // the 4 column-quarter-0 warps
+    for (int s = 0; s < NSLOT; ++s) { mbar_init(b_iodone + 8 * s, kEpiWarps); mbar_init(b_partfree + 8 * s, 1); }
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc_cg2(smem_u32(tmem_slot), C::TMEM_COLS);
@@ -335,6 +336,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
     // sdf[perm[row]].  Perm rows live in registers: cur (tile being computed), nxt (next tile, in A1
     // once filled), pre (the tile after).
     const uint32_t a1full_dst = rank == 0 ? b_a1full : mapa_shared(b_a1full, 0);
+    const float* tcs = tab + p.m.pt_off_csum;
     unsigned long long io_wait = 0, io_busy = 0;
     auto load_perm = [&](long long t, uint32_t (&ix)[4]) {
       const int d = tile_depth2(t, s_tile_end, L);
@@ -408,14 +410,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
         }
       }
       if (w.l == w.d) {
-        const int b = w.ti & 1;
         const long long c1_ = p.prof ? clock64() : 0;
-        mbar_wait(b_iodone + 8 * (s * 2 + b), (uint32_t)((w.ti >> 1) & 1));
+        mbar_wait(b_iodone + 8 * s, (uint32_t)(w.ti & 1));
         if (p.prof) waited += clock64() - c1_;
-        const float* yb = out_y + (s * 2 + b) * 128;
+        const float* pl = part + s * NPL * 128;
+        const float cs = tcs[w.d];
+        float y[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int r = lane + 32 * k;
+          y[k] = cs + pl[r] + pl[128 + r] + pl[256 + r] + pl[384 + r];
+          if (NPL == 5) y[k] += pl[512 + r];
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(b_partfree + 8 * s);
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          if (q.cur[k] != 0xFFFFFFFFu) p.out[q.cur[k]] = yb[lane + 32 * k];
+          if (q.cur[k] != 0xFFFFFFFFu) p.out[q.cur[k]] = y[k];
         __syncwarp();
 #pragma unroll
         for (int k = 0; k < 4; ++k) { q.cur[k] = q.nxt[k]; q.nxt[k] = q.pre[k]; }
@@ -450,7 +461,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
     const float* ta1 = tab + p.m.pt_off_a1;    // [L-1][H] (MULT)
     const float* tc0 = tab + p.m.pt_off_c;     // [L]
     const float* tc1 = tab + p.m.pt_off_c1;    // [L] (MULT, index l-1)
-    const float* tcs = tab + p.m.pt_off_csum;  // [L+1]
     const uint32_t bar_q = 1 + q;              // per-quadrant named barrier (tile-end / MULT reductions)
     const uint32_t afull_dst0 = rank == 0 ? b_afull : mapa_shared(b_afull, 0);
     unsigned long long ep_wait = 0, ep_busy = 0, ep_steps = 0;
@@ -547,30 +557,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
 #pragma unroll
         for (int k = 0; k < 4; ++k) e.ylin[k] += yv[k].x + yv[k].y;
       }
+      publish(s, store);
       if (l == d) {
-        // tile end: reduce every row over its quad and over the four column quarters (per-quadrant
-        // barrier); column quarter 0 adds the tail-bias prefix sum (and, MULT, the Eq. 3 products) and
-        // hands y_d to the IO warp.  Done before this step's publish, so the next tile's MMA (and its
-        // tile end) cannot overwrite `part` before it is read.
-        float* pq = part + s * 4 * 128;
+        // tile end: every row reduced over its quad (shuffles); each warp hands its column quarter's
+        // partials to the IO warp (which adds the 4 quarters and the tail-bias prefix sum).  No barrier
+        // among the epilogue warps; part[s] is reused once the IO warp has read it (part_free).
+        mbar_wait(b_partfree + 8 * s, (uint32_t)((e.w.ti & 1) ^ 1));
+        float* pq = part + s * NPL * 128;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const float v = quad_sum(e.ylin[k]);
           if (tq == 0) pq[cq * 128 + 32 * q + quad + 8 * k] = v;
           e.ylin[k] = 0.f;
         }
-        named_bar_sync(bar_q, 128);
-        if (cq == 0) {
-          const int b = e.w.ti & 1;
-          const int rowl = 32 * q + lane;
-          out_y[(s * 2 + b) * 128 + rowl] =
-              tcs[d] + e.yprod + pq[rowl] + pq[128 + rowl] + pq[256 + rowl] + pq[384 + rowl];
-          __syncwarp();
-          if (lane == 0) mbar_arrive(b_iodone + 8 * (s * 2 + b));
-        }
+        if (NPL == 5 && cq == 0) pq[4 * 128 + 32 * q + lane] = e.yprod;
         e.yprod = 0.f;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(b_iodone + 8 * s);
       }
-      publish(s, store);
       e.w.advance(tstride, T, s_tile_end, L);
       if (p.prof) { ep_wait += c1_ - c0_; ep_busy += clock64() - c1_; ep_steps += 1; }
     };
@@ -607,7 +611,7 @@ template <int H>
 static size_t smem_for2(long long pt_floats, int L, int tail, int nst) {
   using C = Tc2Shape<H>;
   const size_t tab_bytes = (size_t)((pt_floats + 3) & ~3ll) * 4;
-  const size_t io_bytes = (size_t)C::NSLOT * 4 * 128 * 4 + (size_t)C::NSLOT * 2 * 128 * 4;
+  const size_t io_bytes = (size_t)C::NSLOT * (tail == SAND_TAIL_MULT ? 5 : 4) * 128 * 4;
   const size_t red_bytes = tail == SAND_TAIL_MULT ? (size_t)C::NSLOT * 2 * 4 * 128 * 8 : 0;
   return (size_t)C::NSLOT * C::A_BYTES + (size_t)nst * C::STAGE + C::W1_HALF + (size_t)C::NSLOT * C::A1_BYTES +
          tab_bytes + io_bytes + red_bytes + 4 * (size_t)(L + 2) * sizeof(long long) + (3 * nst + 7 * C::NSLOT) * 8 +

@@ -1,0 +1,78 @@
+// Epilogue compute microbenchmark: the K3 per-chunk math (z = acc*w0 + b, sine, tail FFMA2, bf16 pack,
+// stmatrix) on register data, 16 warps x 148 CTAs, for several polynomial shares.  Measures cycles per
+// element per SM.  No TMEM / MMA: isolates the MUFU / FMA / issue balance.
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ float2 sin_poly2(float2 u) {
+  const float2 M = make_float2(12582912.0f, 12582912.0f);
+  const float2 t = __fadd2_rn(u, M);
+  const float2 k = __fadd2_rn(t, make_float2(-12582912.0f, -12582912.0f));
+  const float2 r = __ffma2_rn(k, make_float2(-1.0f, -1.0f), u);
+  const float2 r2 = __fmul2_rn(r, r);
+  float2 p = __ffma2_rn(r2, make_float2(32.78339f, 32.78339f), make_float2(-74.479027f, -74.479027f));
+  p = __ffma2_rn(p, r2, make_float2(81.366989f, 81.366989f));
+  p = __ffma2_rn(p, r2, make_float2(-41.331226f, -41.331226f));
+  p = __ffma2_rn(p, r2, make_float2(6.2830558f, 6.2830558f));
+  return __fmul2_rn(p, r);
+}
+__device__ __forceinline__ uint32_t pack(float lo, float hi) {
+  uint32_t r; asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo)); return r;
+}
+template <int NPCH>   // polynomial chunks per 4 chunks
+__global__ void __launch_bounds__(512, 1) k(int iters, float w0, unsigned long long* cyc, float* sink) {
+  __shared__ __align__(16) float tab[2][256];
+  __shared__ __align__(1024) uint8_t abuf[16 * 1024];
+  for (int i = threadIdx.x; i < 512; i += blockDim.x) tab[i / 256][i % 256] = 0.001f * i;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tq = lane & 3;
+  float acc[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) acc[i] = 0.01f * (threadIdx.x + i);
+  float2 yv[4] = {};
+  const float2 SM2 = make_float2(w0, w0), SP2 = make_float2(w0 * 0.15915f, w0 * 0.15915f);
+  const uint32_t abase = (uint32_t)__cvta_generic_to_shared(abuf) + (lane & 7) * 128 + (lane >> 3) * 1024;
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {   // 4 chunks of 8 columns x 4 rows per thread
+      const float2 b2 = *reinterpret_cast<const float2*>(&tab[0][(8 * i + 2 * tq + 2 * it) & 255]);
+      const float2 a2 = *reinterpret_cast<const float2*>(&tab[1][(8 * i + 2 * tq + 2 * it) & 255]);
+      uint32_t pk[4];
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const float2 a = make_float2(acc[8 * i + 2 * kk], acc[8 * i + 2 * kk + 1]);
+        float2 h;
+        if (i < NPCH) h = sin_poly2(__ffma2_rn(a, SP2, b2));
+        else { const float2 z = __ffma2_rn(a, SM2, b2); h = make_float2(__sinf(z.x), __sinf(z.y)); }
+        yv[kk] = __ffma2_rn(a2, h, yv[kk]);
+        pk[kk] = pack(h.x, h.y);
+      }
+      asm volatile("stmatrix.sync.aligned.m8n8.x4.shared.b16 [%0], {%1, %2, %3, %4};" ::"r"(abase + ((i ^ (lane & 7)) << 4)),
+                   "r"(pk[0]), "r"(pk[1]), "r"(pk[2]), "r"(pk[3]) : "memory");
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) acc[i] += 1e-3f;   // new "accumulators" each iteration
+  }
+  long long t1 = clock64();
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+  float s = 0; for (int kk = 0; kk < 4; ++kk) s += yv[kk].x + yv[kk].y;
+  if (s == 123.f) sink[0] = s;
+}
+int main() {
+  unsigned long long* c; cudaMalloc(&c, 148 * 8); float* sink; cudaMalloc(&sink, 8);
+  unsigned long long h[148];
+  const int iters = 2000;
+  auto run = [&](auto kern, const char* name) {
+    kern<<<148, 512>>>(iters, 30.f, c, sink);
+    cudaError_t e = cudaDeviceSynchronize(); if (e) { printf("%s\n", cudaGetErrorString(e)); return; }
+    kern<<<148, 512>>>(iters, 30.f, c, sink); cudaDeviceSynchronize();
+    cudaMemcpy(h, c, sizeof h, cudaMemcpyDeviceToHost);
+    double el = (double)iters * 512 * 32;   // elements per SM
+    printf("%s: %.4f cycles per element per SM (MUFU floor %.4f)\n", name, (double)h[0] / el, 1.0 / 16);
+  };
+  run(k<0>, "poly 0/4"); run(k<1>, "poly 1/4"); run(k<2>, "poly 2/4"); run(k<3>, "poly 3/4"); run(k<4>, "poly 4/4");
+  return 0;
+}
