@@ -62,6 +62,22 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 }
 
 #endif
+// Wait for roles off the critical path (weight producer, IO warp, relay): poll with __nanosleep
+// back-off instead of try_wait so the waiting warp does not steal issue slots from the epilogue warps
+// on its SM sub-partition.
+__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred P1;\nmbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\nselp.u32 %0, 1, 0, P1;\n}\n"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_lazy(uint32_t bar, uint32_t parity, uint32_t ns = 256) {
+  while (!mbar_test(bar, parity)) __nanosleep(ns);
+}
+
 // Same wait with cluster-scope acquire (pairs with a release.cluster arrive from the peer CTA).
 #ifdef SAND_HANG_DEBUG
 __device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {

@@ -275,7 +275,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
           const uint8_t* src = img + (size_t)(l - 2) * 2 * C::KC * C::WH_CHUNK;
           for (int j = 0; j < C::NSJ; ++j) {
             const long long c0_ = p.prof ? clock64() : 0;
-            mbar_wait(b_wempty + 8 * st, ph ^ 1u);
+            mbar_wait_lazy(b_wempty + 8 * st, ph ^ 1u);
             if (p.prof) { pc[4] += clock64() - c0_; pc[5] += 1; }
             mbar_arrive_expect_tx(b_wfull + 8 * st, C::STAGE);
             bulk_g2s(sW + st * C::STAGE, src + (size_t)j * C::STAGE, C::STAGE, b_wfull + 8 * st);
@@ -403,7 +403,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
       if (w.l == 1) {
         const long long t1 = w.t + tstride;
         if (t1 < T) {
-          mbar_wait(b_a1free + 8 * s, (uint32_t)(w.ti & 1));   // this tile's layer-1 MMA read A1
+          mbar_wait_lazy(b_a1free + 8 * s, (uint32_t)(w.ti & 1));   // this tile's layer-1 MMA read A1
           if (p.prof) waited += clock64() - c0_;
           fill(s, q.nxt);
           if (t1 + tstride < T) load_perm(t1 + tstride, q.pre);
@@ -411,7 +411,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
       }
       if (w.l == w.d) {
         const long long c1_ = p.prof ? clock64() : 0;
-        mbar_wait(b_iodone + 8 * s, (uint32_t)(w.ti & 1));
+        mbar_wait_lazy(b_iodone + 8 * s, (uint32_t)(w.ti & 1));
         if (p.prof) waited += clock64() - c1_;
         const float* pl = part + s * NPL * 128;
         const float cs = tcs[w.d];
