@@ -197,10 +197,18 @@ def main():
     from paper_2604_25936_b200 import SAND_BF16, SandContext, partition
 
     ws, rank, local = _dist()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # one process per GPU; SAND_BENCH_SHARE_GPU=1 (test only) maps several ranks onto the visible GPUs
+    # round-robin and uses gloo, to exercise the N > 1 path on a single-GPU box (the ranks' kernels are
+    # independent: no kernel waits on another rank)
+    share = os.environ.get("SAND_BENCH_SHARE_GPU") == "1"
+    dev_index = local % torch.cuda.device_count() if share else local
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     c = g.make_config(args.config)
     p = c.params()
@@ -222,7 +230,7 @@ def main():
     sdf = torch.empty(n, dtype=torch.float32, device=dev)
     dep = torch.empty(n, dtype=torch.uint8, device=dev)
 
-    ctx = SandContext(c.spec.L, c.spec.H, c.spec.omega0, SAND_BF16, c.spec.tail, local)
+    ctx = SandContext(c.spec.L, c.spec.H, c.spec.omega0, SAND_BF16, c.spec.tail, dev_index)
     ctx.sand_load_weights(g.pack_blob(p))
     ctx.sand_load_depthmap(dm)
     ctx.sand_reserve(n)
@@ -233,7 +241,7 @@ def main():
         ctx.sand_query(pts.data_ptr(), n, sdf.data_ptr(), dep.data_ptr())
     st0 = ctx.sand_get_stats()          # synchronises; resets the per-query event sums
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    clk = ClockSampler(local)
+    clk = ClockSampler(dev_index)
     torch.cuda.synchronize(dev)
     if ws > 1:
         dist.barrier()
@@ -257,8 +265,9 @@ def main():
     dhash = float((dep.to(torch.int64) * (torch.arange(n, device=dev, dtype=torch.int64) % 8191 + 1)).sum().item())
     rec = partition.make_record(n, st["per_depth"], ms_total, sdf_sum, dhash, k0, k1, st["queries"])
     if ws > 1:
-        t = torch.from_numpy(rec).to(dev)
-        allr = torch.empty(ws * t.numel(), dtype=t.dtype, device=dev)
+        cdev = torch.device("cpu") if share else dev   # gloo gathers host tensors
+        t = torch.from_numpy(rec).to(cdev)
+        allr = torch.empty(ws * t.numel(), dtype=t.dtype, device=cdev)
         dist.all_gather_into_tensor(allr, t)
         summ = partition.summarize(allr.cpu().numpy())
     else:
@@ -280,7 +289,7 @@ def main():
             ts.append(time.perf_counter() - t0)
         t_e2e = float(np.mean(ts))
         if ws > 1:
-            tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
+            tt = torch.tensor([t_e2e], dtype=torch.float64, device="cpu" if share else dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             t_e2e = float(tt.item())
         e2e = {"value": summ["n_total"] / t_e2e, "unit": UNIT, "h2d_bytes_per_step": 12 * summ["n_total"],

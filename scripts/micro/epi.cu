@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(512, 1) k(int iters, float w0, unsigned long l
       for (int kk = 0; kk < 4; ++kk) {
         const float2 a = make_float2(acc[8 * i + 2 * kk], acc[8 * i + 2 * kk + 1]);
         float2 h;
-        if (i < NPCH) h = sin_poly2(__ffma2_rn(a, SP2, b2));
+        if ((NPCH < 0 && kk < -NPCH) || (i < NPCH)) h = sin_poly2(__ffma2_rn(a, SP2, b2));
         else { const float2 z = __ffma2_rn(a, SM2, b2); h = make_float2(__sinf(z.x), __sinf(z.y)); }
         yv[kk] = __ffma2_rn(a2, h, yv[kk]);
         pk[kk] = pack(h.x, h.y);
@@ -73,6 +73,7 @@ int main() {
     double el = (double)iters * 512 * 32;   // elements per SM
     printf("%s: %.4f cycles per element per SM (MUFU floor %.4f)\n", name, (double)h[0] / el, 1.0 / 16);
   };
-  run(k<0>, "poly 0/4"); run(k<1>, "poly 1/4"); run(k<2>, "poly 2/4"); run(k<3>, "poly 3/4"); run(k<4>, "poly 4/4");
+  run(k<0>, "poly 0/4"); run(k<1>, "poly 1/4 (chunk)"); run(k<-1>, "poly 1/4 (row k=0)"); run(k<2>, "poly 2/4");
+  run(k<-2>, "poly 2/4 (rows)");
   return 0;
 }
