@@ -16,10 +16,11 @@ Parity unpinned: nothing in this module.
 """
 from .sand_oracle import (
     cell_coords, lookup_voxel, lookup_octree, lookup_bruteforce, lookup,
-    tmlp_forward, tmlp_trace, query, query_full, NONFINITE_DEPTH,
+    tmlp_forward, tmlp_trace, query, query_full, NONFINITE_DEPTH, required_depth, populate_leaf_depths,
 )
 
 __all__ = [
     "cell_coords", "lookup_voxel", "lookup_octree", "lookup_bruteforce", "lookup",
-    "tmlp_forward", "tmlp_trace", "query", "query_full", "NONFINITE_DEPTH",
+    "tmlp_forward", "tmlp_trace", "query", "query_full", "NONFINITE_DEPTH", "required_depth",
+    "populate_leaf_depths",
 ]

@@ -199,3 +199,29 @@ def query(params, depthmap, points, lod_cap=None):
 def query_full(params, points):
     """Uniform full-depth evaluation y_L for every point (Eq. 2 at i = L; SPEC query_full S:374)."""
     return tmlp_forward(params, np.asarray(points, np.float32), params.spec.L)
+
+
+# --------------------------------------------------------------------------------------------
+# Volumetric network-depth map population   (PAPER.md P:209-233, Sec. 3.2, Eq. 5 and Eq. 6)
+# --------------------------------------------------------------------------------------------
+def required_depth(params, x, r, near=True):
+    """Eq. 5:  d(x) = min{ i : |y_L(x) - y_i(x)| < r  and  S_i(x) }  for near-surface points
+    (delta = 1), d(x) = min{ i : S_i(x) } for far points (delta = 0), with
+    S_i(x) := sign(y_i(x)) = sign(y_L(x)).  i runs over 1..L; i = L always qualifies.
+    Evaluated in float64 (R14).  Returns int64 [n]."""
+    _, _, ys = tmlp_trace(params, x)           # ys[i-1] = y_i, shape [L][n]
+    yL = ys[-1]
+    ok = np.sign(ys) == np.sign(yL)[None, :]
+    if near:
+        ok &= np.abs(yL[None, :] - ys) < r
+    ok[-1, :] = True
+    return np.argmax(ok, axis=0).astype(np.int64) + 1
+
+
+def populate_leaf_depths(params, samples, r):
+    """Eq. 6: d(N) = max over the leaf's sample points x of d(x) (near branch of Eq. 5).
+    samples: [n_leaves, spl, 3] (the sample set is an input; R21).  Returns int64 [n_leaves]."""
+    s = np.asarray(samples, np.float32)
+    n, spl = s.shape[0], s.shape[1]
+    d = required_depth(params, s.reshape(-1, 3), r, near=True).reshape(n, spl)
+    return d.max(axis=1)

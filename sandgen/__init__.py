@@ -14,7 +14,7 @@ from .rng import splitmix64, u01, uniform, normal
 from .weights import TMlpSpec, make_weights, pack_blob, unpack_blob, blob_len
 from .geometry import SphereSet, make_spheres, single_sphere, union_sdf
 from .depthmaps import VoxelMap, Octree, build_voxel_map, build_octree, bands_depth
-from .points import grid_axis, grid_points, cloud_points, grid_points_slab
+from .points import grid_axis, grid_points, cloud_points, grid_points_slab, leaf_samples
 from .configs import CONFIGS, make_config
 
 __all__ = [
@@ -22,6 +22,6 @@ __all__ = [
     "TMlpSpec", "make_weights", "pack_blob", "unpack_blob", "blob_len",
     "SphereSet", "make_spheres", "single_sphere", "union_sdf",
     "VoxelMap", "Octree", "build_voxel_map", "build_octree", "bands_depth",
-    "grid_axis", "grid_points", "cloud_points", "grid_points_slab",
+    "grid_axis", "grid_points", "cloud_points", "grid_points_slab", "leaf_samples",
     "CONFIGS", "make_config",
 ]

@@ -43,3 +43,26 @@ def cloud_points(spheres: SphereSet, seed: int, n_uniform: int, n_near: int,
     eps = normal(seed, 2004, 3 * n_near).reshape(n_near, 3) * sigma
     near = spheres.centres[s] + spheres.radii[s, None] * u + eps
     return np.concatenate([uni, near], axis=0).astype(np.float32)
+
+
+def leaf_samples(leaf_level, leaf_ijk, k: int, seed: int) -> np.ndarray:
+    """Eq. 6 sample set of octree leaves (SPEC S:289 design decision; reading R21): per leaf,
+    the 8 cell corners, the cell centre and k seeded interior points U[lo, hi)^3 (counter stream
+    3001, counter = leaf * k * 3 + sample * 3 + axis).  Returns float32 [n_leaves, 9 + k, 3]."""
+    lev = np.asarray(leaf_level, np.int64)
+    ijk = np.asarray(leaf_ijk, np.int64).reshape(-1, 3)
+    n = lev.size
+    side = 2.0 / (2.0 ** lev)                          # float64
+    lo = -1.0 + ijk * side[:, None]
+    out = np.empty((n, 9 + k, 3), np.float64)
+    for c in range(8):
+        off = np.array([(c >> 0) & 1, (c >> 1) & 1, (c >> 2) & 1], np.float64)
+        out[:, c, :] = lo + off[None, :] * side[:, None]
+    out[:, 8, :] = lo + 0.5 * side[:, None]
+    if k:
+        cnt = (np.arange(n, dtype=np.uint64)[:, None, None] * np.uint64(3 * k)
+               + np.arange(k, dtype=np.uint64)[None, :, None] * np.uint64(3)
+               + np.arange(3, dtype=np.uint64)[None, None, :])
+        u = u01(seed, 3001, cnt.reshape(-1)).reshape(n, k, 3)
+        out[:, 9:, :] = lo[:, None, :] + u * side[:, None, None]
+    return out.astype(np.float32)
