@@ -157,6 +157,27 @@ int sand_get_stats(sand_ctx* ctx, sand_stats* out);
  * NULL to query the count only.  Synchronizes ctx's stream. */
 int sand_debug_perm(sand_ctx* ctx, uint32_t* host_perm, int64_t cap, int64_t* n_binned);
 
+/* ---------------------------------------------------------------------------------------------------
+ * Volumetric network-depth map population (the step before the query path; Sec. 3.2).
+ * Both calls evaluate the full L-layer T-MLP in FP32 (accurate sine) whatever ctx's precision, because
+ * Eq. 5 compares cumulative outputs against r (1.5e-4 in the paper).  Only the weights must be
+ * loaded.  Asynchronous on ctx's stream.  Errors: SAND_ERR_ARG, SAND_ERR_STATE, SAND_ERR_UNSUPPORTED
+ * (H not in {16, 32, 64, 128, 256, 336}), SAND_ERR_CUDA, SAND_ERR_OOM.                              */
+
+/* Required depth (Eq. 5) of each of n points (d_points: n x 3 float32 AoS, device):
+ *   near != 0: d(x) = min{ i : |y_L(x) - y_i(x)| < r and sign(y_i(x)) = sign(y_L(x)) }  (delta = 1)
+ *   near == 0: d(x) = min{ i : sign(y_i(x)) = sign(y_L(x)) }                             (delta = 0)
+ * written to d_out_depth[n] (1..L; i = L always qualifies). */
+int sand_required_depth(sand_ctx* ctx, const float* d_points, int64_t n, float r, int near,
+                        uint8_t* d_out_depth);
+
+/* Leaf depths (Eq. 6): d_samples holds n_leaves x samples_per_leaf points (leaf-major,
+ * float32 AoS, device; the sample set is the caller's, e.g. corners + centre + seeded interior points);
+ * d_leaf_depth[N] = max over leaf N's samples of the near-branch d(x).  Far leaves (Eq. 7) are not
+ * passed: their payload is the cached SDF, not a depth. */
+int sand_populate_leaf_depths(sand_ctx* ctx, const float* d_samples, int64_t n_leaves, int samples_per_leaf,
+                              float r, uint8_t* d_leaf_depth);
+
 /* Message for the last error on ctx (or of the last failed sand_create if ctx is NULL).
  * Valid until the next call on ctx.  Never NULL. */
 const char* sand_last_error(const sand_ctx* ctx);

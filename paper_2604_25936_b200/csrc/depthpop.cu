@@ -1,0 +1,204 @@
+// depthpop.cu -- volumetric network-depth map population on the GPU.
+//
+// PAPER.md Sec. 3.2: the required network depth of a point (Eq. 5)
+//     d(x) = min{ i : |y_L(x) - y_i(x)| < r  and  sign(y_i(x)) = sign(y_L(x)) }      (near, delta = 1)
+//     d(x) = min{ i : sign(y_i(x)) = sign(y_L(x)) }                                   (far,  delta = 0)
+// and the leaf depth (Eq. 6) d(N) = max over the leaf's sample points of d(x).
+//
+// Eq. 5 compares cumulative outputs against r (1.5e-4 in the paper), far below the BF16 path's
+// error, so the full-depth evaluation here is FP32 (accurate sinf), whatever the context's precision.
+// k_required_depth: persistent blocks of 256 threads over tiles of 64 points; every layer is a register-
+// blocked FP32 GEMM (thread = 8 points x ceil(H/32) units, W^T staged in shared memory 16 rows at a
+// time, activations transposed [unit][point] in shared memory) with the sine, tail and running y_i
+// fused; after layer L each point's d(x) is decided from its y_1..y_L.  k_leaf_max: Eq. 6 pooling.
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "sand_internal.h"
+
+namespace sand {
+
+constexpr int kDpP = 64;          // points per tile
+constexpr int kDpThreads = 256;   // 8 point groups x 32 unit lanes
+constexpr int kDpKC = 16;         // W^T rows staged per step
+
+template <int H>
+struct DpShape {
+  static constexpr int U = (H + 31) / 32;                    // units per thread
+  static constexpr int HP = U * 32;                          // padded unit count
+  static constexpr size_t SMEM = (size_t)2 * HP * kDpP * 4   // h ping-pong, [unit][point]
+                                 + (size_t)kDpKC * HP * 4;   // W^T stage
+};
+
+template <int H, int TAIL>
+__global__ void __launch_bounds__(kDpThreads, 1) k_required_depth(MlpDev m, const float* __restrict__ w_t,
+                                                                  const float* __restrict__ pts, long long n,
+                                                                  float r, int near, uint8_t* __restrict__ out) {
+  using C = DpShape<H>;
+  extern __shared__ __align__(16) float sm[];
+  float* hA = sm;                               // [HP][kDpP]
+  float* hB = hA + C::HP * kDpP;
+  float* ws = hB + C::HP * kDpP;                // [kDpKC][HP]
+  __shared__ float ys[32][kDpP];                // y_i per point (L <= 32)
+  __shared__ float px[3][kDpP];
+  const int L = m.L;
+  const float w0 = m.omega0;
+  const int tid = threadIdx.x, tj = tid & 31, tp = tid >> 5;   // warp = point group
+  const float4* w1 = reinterpret_cast<const float4*>(m.tables + m.off_w1);
+  const float* bias_t = m.tables + m.off_bias;   // [L-1][H], w0 * b_i
+  const float* a_t = m.tables + m.off_a;         // [L][H]
+  const float* a1_t = m.tables + m.off_a1;       // [L-1][H] (MULT)
+  const float* c_t = m.tables + m.off_c;         // [L]
+  const float* c1_t = m.tables + m.off_c1;       // [L-1] (MULT)
+  const long long ntiles = (n + kDpP - 1) / kDpP;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long long p0 = tile * kDpP;
+    for (int i = tid; i < 3 * kDpP; i += kDpThreads) {
+      const int p = i / 3, c = i % 3;
+      px[c][p] = (p0 + p < n) ? pts[3 * (p0 + p) + c] : 0.f;
+    }
+    __syncthreads();
+    // ---- layer 1 (K = 3) + tail 1
+    for (int i = tid; i < C::HP * kDpP; i += kDpThreads) {
+      const int j = i / kDpP, p = i % kDpP;
+      float h = 0.f;
+      if (j < H) {
+        const float4 w = w1[j];
+        h = sinf(fmaf(w.z, px[2][p], fmaf(w.y, px[1][p], fmaf(w.x, px[0][p], w.w))));
+      }
+      hA[j * kDpP + p] = h;
+    }
+    __syncthreads();
+    auto tails = [&](int l, const float* hcur) {
+      // t_l per point: warp tp reduces its 8 points over all H units (lane = unit residue)
+      for (int pp = 0; pp < 8; ++pp) {
+        const int p = tp * 8 + pp;
+        float s0 = 0.f, s1 = 0.f;
+        for (int j = tj; j < H; j += 32) {
+          const float h = hcur[j * kDpP + p];
+          s0 = fmaf(a_t[(l - 1) * H + j], h, s0);
+          if (TAIL == SAND_TAIL_MULT && l >= 2) s1 = fmaf(a1_t[(l - 2) * H + j], h, s1);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+          s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        }
+        if (tj == 0) {
+          float t = s0 + c_t[l - 1];
+          if (TAIL == SAND_TAIL_MULT && l >= 2) t *= s1 + c1_t[l - 2];
+          ys[l - 1][p] = (l == 1 ? 0.f : ys[l - 2][p]) + t;
+        }
+      }
+    };
+    tails(1, hA);
+    // ---- hidden layers: h_out[j][p] = sin(w0 * (W_l h_in)[j][p] + w0 b_l[j])
+    float* hin = hA;
+    float* hout = hB;
+    for (int l = 2; l <= L; ++l) {
+      const float* W = w_t + (size_t)(l - 2) * H * H;   // W^T [k][j]
+      float acc[8][C::U];
+#pragma unroll
+      for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int u = 0; u < C::U; ++u) acc[a][u] = 0.f;
+      for (int k0 = 0; k0 < H; k0 += kDpKC) {
+        __syncthreads();
+        for (int i = tid; i < kDpKC * C::HP; i += kDpThreads) {
+          const int kk = i / C::HP, j = i % C::HP;
+          ws[i] = (k0 + kk < H && j < H) ? W[(size_t)(k0 + kk) * H + j] : 0.f;
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int kk = 0; kk < kDpKC && k0 + kk < H; ++kk) {
+          const float4 h0 = *reinterpret_cast<const float4*>(hin + (k0 + kk) * kDpP + tp * 8);
+          const float4 h1 = *reinterpret_cast<const float4*>(hin + (k0 + kk) * kDpP + tp * 8 + 4);
+          const float hv[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+#pragma unroll
+          for (int u = 0; u < C::U; ++u) {
+            const float w = ws[kk * C::HP + tj + 32 * u];
+#pragma unroll
+            for (int a = 0; a < 8; ++a) acc[a][u] = fmaf(w, hv[a], acc[a][u]);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < C::U; ++u) {
+        const int j = tj + 32 * u;
+        const float b = j < H ? bias_t[(l - 2) * H + j] : 0.f;
+#pragma unroll
+        for (int a = 0; a < 8; ++a) hout[j * kDpP + tp * 8 + a] = j < H ? sinf(fmaf(acc[a][u], w0, b)) : 0.f;
+      }
+      __syncthreads();
+      tails(l, hout);
+      float* t = hin; hin = hout; hout = t;
+    }
+    __syncthreads();
+    // ---- Eq. 5 decision per point
+    if (tid < kDpP && p0 + tid < n) {
+      const float yL = ys[L - 1][tid];
+      const float sL = (yL > 0.f) - (yL < 0.f);
+      int d = L;
+      for (int i = 1; i < L; ++i) {
+        const float yi = ys[i - 1][tid];
+        const float si = (yi > 0.f) - (yi < 0.f);
+        if (si == sL && (!near || fabsf(yL - yi) < r)) { d = i; break; }
+      }
+      out[p0 + tid] = (uint8_t)d;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_leaf_max(const uint8_t* __restrict__ d, long long n_leaves, int spl, uint8_t* __restrict__ out) {
+  const long long leaf = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (leaf >= n_leaves) return;
+  uint32_t mx = 0;
+  for (int s = 0; s < spl; ++s) mx = max(mx, (uint32_t)d[leaf * spl + s]);
+  out[leaf] = (uint8_t)mx;
+}
+
+template <int H, int TAIL>
+static cudaError_t launch_rd_t(const MlpDev& m, const float* w_t, const float* pts, long long n, float r, int near,
+                               uint8_t* out, int num_sms, cudaStream_t st) {
+  const size_t sm = DpShape<H>::SMEM;
+  cudaError_t e = cudaFuncSetAttribute(k_required_depth<H, TAIL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)sm);
+  if (e != cudaSuccess) return e;
+  const long long ntiles = (n + kDpP - 1) / kDpP;
+  const int grid = (int)(ntiles < num_sms ? ntiles : num_sms);
+  k_required_depth<H, TAIL><<<grid, kDpThreads, sm, st>>>(m, w_t, pts, n, r, near, out);
+  return cudaGetLastError();
+}
+
+bool depthpop_supported(int H) {
+  return H == 16 || H == 32 || H == 64 || H == 128 || H == 256 || H == 336;
+}
+
+cudaError_t launch_required_depth(const MlpDev& m, const float* w_t, const float* pts, long long n, float r,
+                                  int near, uint8_t* out, int num_sms, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const bool mult = m.tail == SAND_TAIL_MULT;
+#define SAND_DP_CASE(HH)                                                                          \
+  case HH:                                                                                        \
+    return mult ? launch_rd_t<HH, 1>(m, w_t, pts, n, r, near, out, num_sms, st)                   \
+                : launch_rd_t<HH, 0>(m, w_t, pts, n, r, near, out, num_sms, st);
+  switch (m.H) {
+    SAND_DP_CASE(16)
+    SAND_DP_CASE(32)
+    SAND_DP_CASE(64)
+    SAND_DP_CASE(128)
+    SAND_DP_CASE(256)
+    SAND_DP_CASE(336)
+    default: return cudaErrorInvalidValue;
+  }
+#undef SAND_DP_CASE
+}
+
+cudaError_t launch_leaf_max(const uint8_t* d, long long n_leaves, int spl, uint8_t* out, cudaStream_t st) {
+  if (n_leaves <= 0) return cudaSuccess;
+  k_leaf_max<<<(unsigned)((n_leaves + 255) / 256), 256, 0, st>>>(d, n_leaves, spl, out);
+  return cudaGetLastError();
+}
+
+}  // namespace sand

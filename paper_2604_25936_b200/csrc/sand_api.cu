@@ -37,6 +37,9 @@ struct sand_ctx {
   void* d_wimage = nullptr;
   void* d_wimage_pair = nullptr;
   float* d_whidden = nullptr;
+  float* d_wt_f32 = nullptr;      // FP32 hidden weights transposed [L-1][k][j] (depth-map population)
+  uint8_t* d_dp_tmp = nullptr;    // per-sample depths of sand_populate_leaf_depths
+  long long cap_dp = 0;
   MlpDev mlp{};
   // depth map
   bool have_dm = false;
@@ -155,7 +158,7 @@ static void free_depthmap(sand_ctx* c) {
   c->have_dm = false;
 }
 static void free_weights(sand_ctx* c) {
-  dfree(c->d_tables); dfree(c->d_pair_tables); dfree(c->d_w1_image); dfree(c->d_wimage); dfree(c->d_wimage_pair); dfree(c->d_whidden);
+  dfree(c->d_tables); dfree(c->d_pair_tables); dfree(c->d_w1_image); dfree(c->d_wimage); dfree(c->d_wimage_pair); dfree(c->d_whidden); dfree(c->d_wt_f32);
   c->have_w = false;
 }
 static void free_hostpipe(sand_ctx* c) {
@@ -182,6 +185,7 @@ extern "C" int sand_destroy(sand_ctx* ctx) {
   free_depthmap(ctx);
   free_weights(ctx);
   free_hostpipe(ctx);
+  dfree(ctx->d_dp_tmp);
   for (auto& q : ctx->evq)
     for (auto& v : q)
       if (v) cudaEventDestroy(v);
@@ -351,6 +355,15 @@ extern "C" int sand_load_weights(sand_ctx* ctx, const float* blob, size_t n_floa
         CU(cudaMemcpy(ctx->d_wimage_pair, pimg.data(), pimg.size(), cudaMemcpyHostToDevice));
       }
     }
+  }
+  if (L >= 2) {
+    // FP32 W^T for the depth-map population kernels (Eq. 5 needs FP32 whatever the query precision)
+    std::vector<float> wt((size_t)(L - 1) * H * H);
+    for (int i = 1; i < L; ++i)
+      for (int j = 0; j < H; ++j)
+        for (int k = 0; k < H; ++k) wt[(size_t)(i - 1) * H * H + (size_t)k * H + j] = W[i][(size_t)j * H + k];
+    CU(cudaMalloc(&ctx->d_wt_f32, sizeof(float) * wt.size()));
+    CU(cudaMemcpy(ctx->d_wt_f32, wt.data(), sizeof(float) * wt.size(), cudaMemcpyHostToDevice));
   }
   m.w_hidden = ctx->d_whidden;
   m.w_image = ctx->d_wimage;
@@ -650,5 +663,42 @@ extern "C" int sand_debug_perm(sand_ctx* ctx, uint32_t* host_perm, int64_t cap, 
   for (int d = 1; d <= ctx->cfg.L; ++d) nb += m.count[d];
   *n_binned = nb;
   if (host_perm && cap > 0) CU(cudaMemcpy(host_perm, ctx->d_perm, sizeof(uint32_t) * (size_t)std::min<long long>(cap, nb), cudaMemcpyDeviceToHost));
+  return SAND_OK;
+}
+
+// ------------------------------------------------------------------------------- depth-map population
+extern "C" int sand_required_depth(sand_ctx* ctx, const float* d_points, int64_t n, float r, int near,
+                                   uint8_t* d_out_depth) {
+  if (!ctx) return fail(ctx, SAND_ERR_ARG, "NULL ctx");
+  if (n < 0 || !(r >= 0.0f)) return fail(ctx, SAND_ERR_ARG, "sand_required_depth: n < 0 or r < 0");
+  if (!ctx->have_w) return fail(ctx, SAND_ERR_STATE, "load weights before sand_required_depth");
+  if (n == 0) return SAND_OK;
+  if (!d_points || !d_out_depth) return fail(ctx, SAND_ERR_ARG, "NULL buffer");
+  if (!depthpop_supported(ctx->cfg.H)) return fail(ctx, SAND_ERR_UNSUPPORTED, "H = %d", ctx->cfg.H);
+  CU(cudaSetDevice(ctx->cfg.device));
+  CU(launch_required_depth(ctx->mlp, ctx->d_wt_f32, d_points, n, r, near ? 1 : 0, d_out_depth, ctx->num_sms,
+                           ctx->stream));
+  return SAND_OK;
+}
+
+extern "C" int sand_populate_leaf_depths(sand_ctx* ctx, const float* d_samples, int64_t n_leaves,
+                                         int samples_per_leaf, float r, uint8_t* d_leaf_depth) {
+  if (!ctx) return fail(ctx, SAND_ERR_ARG, "NULL ctx");
+  if (n_leaves < 0 || samples_per_leaf < 1 || !(r >= 0.0f))
+    return fail(ctx, SAND_ERR_ARG, "sand_populate_leaf_depths: bad size or r");
+  if (!ctx->have_w) return fail(ctx, SAND_ERR_STATE, "load weights before sand_populate_leaf_depths");
+  if (n_leaves == 0) return SAND_OK;
+  if (!d_samples || !d_leaf_depth) return fail(ctx, SAND_ERR_ARG, "NULL buffer");
+  if (!depthpop_supported(ctx->cfg.H)) return fail(ctx, SAND_ERR_UNSUPPORTED, "H = %d", ctx->cfg.H);
+  CU(cudaSetDevice(ctx->cfg.device));
+  const long long ns = n_leaves * (long long)samples_per_leaf;
+  if (ns > ctx->cap_dp) {
+    CU(cudaStreamSynchronize(ctx->stream));
+    dfree(ctx->d_dp_tmp);
+    CU(cudaMalloc(&ctx->d_dp_tmp, (size_t)ns));
+    ctx->cap_dp = ns;
+  }
+  CU(launch_required_depth(ctx->mlp, ctx->d_wt_f32, d_samples, ns, r, 1, ctx->d_dp_tmp, ctx->num_sms, ctx->stream));
+  CU(launch_leaf_max(ctx->d_dp_tmp, n_leaves, samples_per_leaf, d_leaf_depth, ctx->stream));
   return SAND_OK;
 }

@@ -50,7 +50,8 @@ class sand_stats(ctypes.Structure):
 
 EXPORTS = ("sand_create", "sand_destroy", "sand_load_weights", "sand_load_depthmap", "sand_set_stream",
            "sand_set_lod_cap", "sand_reserve", "sand_query", "sand_query_host", "sand_get_stats",
-           "sand_debug_perm", "sand_last_error", "sand_abi_version")
+           "sand_debug_perm", "sand_last_error", "sand_abi_version", "sand_required_depth",
+           "sand_populate_leaf_depths")
 
 _lib = None
 
@@ -79,6 +80,8 @@ def load_library(path=None):
     lib.sand_last_error.argtypes = [vp]
     lib.sand_last_error.restype = ctypes.c_char_p
     lib.sand_abi_version.argtypes = []
+    lib.sand_required_depth.argtypes = [vp, vp, i64, ctypes.c_float, ctypes.c_int, vp]
+    lib.sand_populate_leaf_depths.argtypes = [vp, vp, i64, ctypes.c_int, ctypes.c_float, vp]
     for f in EXPORTS:
         if f not in ("sand_last_error",):
             getattr(lib, f).restype = ctypes.c_int
@@ -180,6 +183,15 @@ class SandContext:
         out = np.empty(nb.value, np.uint32)
         self._chk(self.lib.sand_debug_perm(self.h, out.ctypes.data_as(ctypes.c_void_p), out.size, ctypes.byref(nb)))
         return out
+
+    # -- depth-map population (Eq. 5 / Eq. 6) --------------------------------------------------------
+    def sand_required_depth(self, d_points, n, r, near, d_out_depth):
+        self._chk(self.lib.sand_required_depth(self.h, ctypes.c_void_p(d_points), int(n), float(r), int(bool(near)),
+                                               ctypes.c_void_p(d_out_depth)))
+
+    def sand_populate_leaf_depths(self, d_samples, n_leaves, samples_per_leaf, r, d_leaf_depth):
+        self._chk(self.lib.sand_populate_leaf_depths(self.h, ctypes.c_void_p(d_samples), int(n_leaves),
+                                                     int(samples_per_leaf), float(r), ctypes.c_void_p(d_leaf_depth)))
 
     # -- torch convenience (device tensors in, device tensors out) -----------------------------------
     def query_tensor(self, pts, sdf=None, depth=None):
