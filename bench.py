@@ -170,6 +170,73 @@ def cpu_baseline(p, depthmap, pts, budget_s):
             "sample": f"{done} seeded random points of the workload ({t_used:.1f} s of oracle time)"}
 
 
+def run_populate(args):
+    """Depth-map population (Eq. 5 + Eq. 6): every finest leaf of the config's octree, 25 samples
+    each (8 corners + centre + 16 seeded interior points, R21), r = 1.5e-4.  One step =
+    sand_populate_leaf_depths over all of them.  Single GPU (rank 0 of any launch)."""
+    import torch
+    import sandgen as g
+    from paper_2604_25936_b200 import SAND_BF16, SandContext
+    ws, rank, local = _dist()
+    if rank != 0:
+        return 0
+    c = g.make_config(args.config if args.config != "C1" else "C2")
+    p = c.params()
+    oc = c.depthmap
+    sel = np.nonzero(oc.leaf_level == oc.level)[0]
+    samples = g.leaf_samples(oc.leaf_level[sel], oc.leaf_ijk[sel], 16, seed=5)
+    n, spl = samples.shape[0], samples.shape[1]
+    dev = torch.device("cuda", 0)
+    ts = torch.from_numpy(np.ascontiguousarray(samples.reshape(-1, 3))).to(dev)
+    out = torch.empty(n, dtype=torch.uint8, device=dev)
+    r = 1.5e-4
+    with SandContext(c.spec.L, c.spec.H, c.spec.omega0, SAND_BF16, c.spec.tail, 0) as ctx:
+        ctx.sand_load_weights(g.pack_blob(p))
+        st = torch.cuda.current_stream(dev)
+        ctx.sand_set_stream(st.cuda_stream)
+        for _ in range(args.warmup):
+            ctx.sand_populate_leaf_depths(ts.data_ptr(), n, spl, r, out.data_ptr())
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        clk = ClockSampler(0)
+        clk.start()
+        e0.record(st)
+        for _ in range(args.steps):
+            ctx.sand_populate_leaf_depths(ts.data_ptr(), n, spl, r, out.data_ptr())
+        e1.record(st)
+        torch.cuda.synchronize(dev)
+        clocks = clk.stop()
+        ms = e0.elapsed_time(e1) / args.steps
+    H, L = c.spec.H, c.spec.L
+    ns = n * spl
+    flops = ns * (6.0 * H + (L - 1) * 2.0 * H * H + L * 2.0 * H)
+    sm_mhz = (clocks or {}).get("sm_mhz") or 1965.0
+    peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12   # FP32 FMA lanes x 2 FLOP x clock (B200_PROFILING.md units)
+    ach = flops / (ms / 1e3) / 1e12
+    cpu = None
+    if not args.no_cpu:
+        import oracle
+        k = min(n, 2000)
+        t0 = time.perf_counter()
+        oracle.populate_leaf_depths(p, samples[:k], r)
+        dt = time.perf_counter() - t0
+        cpu = {"value": k * spl / dt, "unit": "samples/s", "cores": _cores(), "kind": "oracle",
+               "sample": f"first {k} leaves x {spl} samples"}
+    line = {"task": "populate", "metric": "depth-map population samples/sec (Eq. 5 + Eq. 6)",
+            "value": ns / (ms / 1e3), "unit": "samples/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{c.name} octree finest leaves: {n} leaves x {spl} samples, r = 1.5e-4",
+                       "model": f"{L}x{H} SIREN T-MLP (seeded init)"},
+            "roofline": {"bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                         "peak_source": "derived: 148 SM x 128 FP32 FMA lanes x 2 FLOP x median SM clock",
+                         "traffic": None},
+            "cpu_baseline": cpu, "clocks": clocks,
+            "depth_hist": np.bincount(out.cpu().numpy(), minlength=L + 1).tolist()}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -184,11 +251,16 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-sample", type=int, default=1 << 15)
     ap.add_argument("--full-depth", action="store_true", help="all-L depth map (non-adaptive GPU baseline)")
+    ap.add_argument("--task", default="query", choices=["query", "populate"],
+                    help="query: the adaptive SDF query path (BASELINE metric); populate: depth-map "
+                         "population (Eq. 5/6, SURVEY 8(f) NEXT #1) on the config's finest octree leaves")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: at least 3 warm-up steps
     if args.impl == "reference":
         return run_reference(args)
+    if args.task == "populate":
+        return run_populate(args)
 
     import torch
     import torch.distributed as dist
