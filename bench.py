@@ -388,15 +388,15 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": wl_desc if ws == 1 else f"{args.config} weak-scaled: 512x512x{Rz} grid, "
-                       "work-balanced z-slabs", "model": "8x256 SIREN T-MLP (seeded SIREN init), linear tails",
+                       "work-balanced z-slabs", "model": f"{c.spec.L}x{c.spec.H} SIREN T-MLP (seeded SIREN init), linear tails",
                        "depth_map": "level-7 sphere-union octree (baked 128^3)" if args.config == "C2" else args.config,
                        "global_points": summ["n_total"], "parallelism": f"dp{ws} (z-slab shards)",
                        "l2": f"inputs {12 * n / 1e9:.2f} GB per rank > 126 MB L2; no flush needed",
                        "full_depth_baseline": bool(args.full_depth)},
-            "roofline": {"bound": "tensor", "kernel": "k_tmlp_tc2 (K3 fused T-MLP, CTA pair)", "achieved": ach,
+            "roofline": {"bound": "tensor", "kernel": ("k_tmlp_wide (K3 fused T-MLP, CTA pair, N-halves)" if c.spec.H == 336 else "k_tmlp_tc2 (K3 fused T-MLP, CTA pair)"), "achieved": ach,
                          "peak": pk["bf16"], "unit": "TFLOP/s", "frac": ach / pk["bf16"],
                          "peak_source": pk["src"] + " bf16_tflops (burst)",
-                         "frac_vs_sustained": ach / pk["bf16_sus"], "traffic": _traffic(),
+                         "frac_vs_sustained": ach / pk["bf16_sus"], "traffic": _traffic() if args.config == "C2" else None,
                          "algorithmic_flops_per_launch": f_exec_rank0,
                          "flops_formula": "executed H x H FLOPs sum_p (d_p - 1) * 2 H^2 (Eq. 2 reading R3)",
                          "ms_per_launch": ms_mlp,

@@ -101,7 +101,8 @@ static void dfree(T*& p) {
 static bool supported(const sand_config& c) {
   if (c.prec == SAND_FP32) return simt_supported_H(c.H) && simt_smem_bytes(c.L, c.H, c.tail) <= 232448;
   if (c.prec == SAND_BF16)
-    return tc_supported_H(c.H) && (tc2_usable(c.L, c.H, c.tail) || tc_smem_bytes(c.L, c.H, c.tail) > 0);
+    return tc_supported_H(c.H) && (tc2_usable(c.L, c.H, c.tail) || tc3_usable(c.L, c.H, c.tail) ||
+                                   tc_smem_bytes(c.L, c.H, c.tail) > 0);
   return false;
 }
 
@@ -142,7 +143,8 @@ extern "C" int sand_create(const sand_config* cfg, sand_ctx** out) {
   ctx->num_sms = prop.multiProcessorCount;
   if (const char* ev = getenv("SAND_PAIR")) ctx->use_pair = std::atoi(ev) != 0;
   // the CTA-pair kernel keeps its per-column tables in shared memory: large L falls back to the 1-CTA kernel
-  if (cfg->prec == SAND_BF16) ctx->use_pair = ctx->use_pair && tc2_usable(cfg->L, cfg->H, cfg->tail);
+  if (cfg->prec == SAND_BF16)
+    ctx->use_pair = ctx->use_pair && (tc2_usable(cfg->L, cfg->H, cfg->tail) || tc3_usable(cfg->L, cfg->H, cfg->tail));
   cudaError_t e = prepare_tmlp_kernels(cfg->L, cfg->H, cfg->tail, cfg->prec);
   if (e != cudaSuccess) { fail(ctx, SAND_ERR_CUDA, "kernel attribute setup: %s", cudaGetErrorString(e)); return bail(SAND_ERR_CUDA); }
   *out = ctx;
@@ -315,6 +317,23 @@ extern "C" int sand_load_weights(sand_ctx* ctx, const float* blob, size_t n_floa
     CU(cudaMalloc(&ctx->d_pair_tables, sizeof(float) * pt.size()));
     CU(cudaMemcpy(ctx->d_pair_tables, pt.data(), sizeof(float) * pt.size(), cudaMemcpyHostToDevice));
     m.pair_tables = ctx->d_pair_tables;
+  }
+  if (ctx->cfg.prec == SAND_BF16 && tc3_available(H, tail)) {
+    // wide CTA-pair kernel: padded-width tables, layer-1 and hidden-layer images (tmlp_tc3.cu)
+    std::vector<float> pt;
+    std::vector<uint16_t> w1img;
+    std::vector<uint8_t> wimg;
+    tc3_build_host(L, H, w0, W.data(), b.data(), a.data(), c.data(), &m, &pt, &w1img, &wimg);
+    CU(cudaMalloc(&ctx->d_pair_tables, sizeof(float) * pt.size()));
+    CU(cudaMemcpy(ctx->d_pair_tables, pt.data(), sizeof(float) * pt.size(), cudaMemcpyHostToDevice));
+    m.pair_tables = ctx->d_pair_tables;
+    CU(cudaMalloc(&ctx->d_w1_image, w1img.size() * 2));
+    CU(cudaMemcpy(ctx->d_w1_image, w1img.data(), w1img.size() * 2, cudaMemcpyHostToDevice));
+    m.w1_image = ctx->d_w1_image;
+    if (!wimg.empty()) {
+      CU(cudaMalloc(&ctx->d_wimage_pair, wimg.size()));
+      CU(cudaMemcpy(ctx->d_wimage_pair, wimg.data(), wimg.size(), cudaMemcpyHostToDevice));
+    }
   }
   if (L >= 2) {
     if (ctx->cfg.prec == SAND_FP32) {

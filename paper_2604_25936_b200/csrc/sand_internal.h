@@ -3,6 +3,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <vector>
+
 #include "../../include/sand.h"
 
 namespace sand {
@@ -104,5 +106,15 @@ cudaError_t launch_tmlp_tc2(const MlpDev& m, const float* pts, const uint32_t* p
                             float* out, int num_sms, cudaStream_t st);
 cudaError_t prepare_tc2(int H, int tail);
 size_t tc2_w1_offset(int H, int n, int k);   // byte offset of (unit n, column k) in MlpDev::w1_image
+// Wide CTA-pair kernel (tmlp_tc3.cu): H = 336, LINEAR; one 256-row tile split into two N-halves.  It reuses
+// MlpDev::pair_tables / w1_image / w_image_pair with its own (padded-width) layouts, built by tc3_build_host.
+bool tc3_available(int H, int tail);
+bool tc3_usable(int L, int H, int tail);
+void tc3_build_host(int L, int H, float w0, const float* const* W, const float* const* b, const float* const* a,
+                    const float* c, MlpDev* m, std::vector<float>* tables, std::vector<uint16_t>* w1img,
+                    std::vector<uint8_t>* img);
+cudaError_t launch_tmlp_tc3(const MlpDev& m, const float* pts, const uint32_t* perm, const QueryMeta* meta,
+                            float* out, int num_sms, cudaStream_t st);
+cudaError_t prepare_tc3();
 
 }  // namespace sand

@@ -43,6 +43,20 @@ def test_bf16_random_depths_small(H, tail):
     assert_parity(sdf, dep, sdf_or, dep_or, TOL_BF16)
 
 
+@pytest.mark.parametrize("L", [1, 2, 8])
+def test_bf16_wide_pair_kernel(L):
+    """H = 336 (configs[3] width) on the wide CTA-pair kernel: single-layer and two-layer edge cases and
+    the full L = 8 net, many 256-row tiles per depth with ragged tails."""
+    spec = g.TMlpSpec(L=L, H=336, omega0=30.0, tail=0, seed=40 + L)
+    p = g.make_weights(spec)
+    dm = _random_voxel_map(3, L, 11)
+    pts = _pts(60007, 12)
+    with make_ctx(spec, BF16) as ctx:
+        sdf, dep = run_engine(ctx, p, dm, pts)
+    sdf_or, dep_or = oracle.query(p, dm, pts)
+    assert_parity(sdf, dep, sdf_or, dep_or, TOL_BF16)
+
+
 @pytest.mark.parametrize("H", [16, 32, 64])
 @pytest.mark.parametrize("tail", [0, 1])
 def test_fp32_random_depths_small(H, tail):
