@@ -52,7 +52,16 @@ struct Tc3Params {
   const QueryMeta* meta;
   float* out;
   int nst;
+  int prof;   // diagnostic (env SAND_KPROF=1): clock64 wait counters per role -> g_kprof3
 };
+
+// Diagnostic counters per CTA (written only when prof != 0): 0 MMA wait a_full[A], 1 MMA wait a_full[B]
+// (mid-job), 2 MMA wait weights, 3 MMA wait layer-1 (a_full + a1_full), 4 MMA loop total, 5 producer
+// wait w_empty, 6 epi wait acc[A], 7 epi wait acc[B] (step B), 8 epi wait acc[B] (before A stores),
+// 9 epi total, 10 epi steps, 11 IO wait, 12 epi wait part_free.
+constexpr int kProf3 = 13;
+__device__ unsigned long long g_kprof3[160][kProf3];
+#define P3T() (p.prof ? clock64() : 0ll)
 
 __device__ __forceinline__ int tile_depth3(long long t, const long long* te, int L) {
   for (int d = L; d >= 1; --d)
@@ -123,6 +132,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc3Shape<H>::THREADS
   const uint32_t b_a1free = b_a1full + 8;          // layer-1 MMAs done with A1
   const uint32_t b_iodone = b_a1free + 8;          // all epilogue warps wrote their tile partials
   const uint32_t b_partfree = b_iodone + 8;        // IO warp read the partials
+  const uint32_t b_bhead = b_partfree + 8;         // job (B, l >= 2) has read K-chunks 0..2 (A cols 0..191)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * nst + 10);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -154,6 +164,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc3Shape<H>::THREADS
     mbar_init(b_a1free, 1);
     mbar_init(b_iodone, kEpiWarps);
     mbar_init(b_partfree, 1);
+    mbar_init(b_bhead, 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc_cg2(smem_u32(tmem_slot), 512);
@@ -181,6 +192,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc3Shape<H>::THREADS
       int st = 0;
       uint32_t ph = 0;
       bool first_a = true, first_b = true;
+      unsigned long long pc[kProf3] = {};
+      const long long t_start = P3T();
 #pragma unroll 1
       while (!w.done) {
         const int l = w.l, hf = w.half;
@@ -189,6 +202,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc3Shape<H>::THREADS
         const uint32_t ID = hf ? IDB : IDA;
         if (l == 1) {
           if (warp == 1 && rank == 0) {
+            const long long t0_ = P3T();
             // acc of this half free: the epilogue finished the previous tile's last step of this half
             if (hf == 0) {
               if (!first_a) { mbar_wait_cluster(b_afull, paA); paA ^= 1u; }
@@ -199,6 +213,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc3Shape<H>::THREADS
               if (!first_b) { mbar_wait_cluster(b_afull + 8, paB); paB ^= 1u; }
               first_b = false;
             }
+            if (p.prof) pc[3] += clock64() - t0_;
             tc_fence_after();
             mma_bf16_cg2(acc, desc_nosw(sA1, 128, 256), desc_nosw(sW1 + (hf ? C::RA * 32 : 0), 128, 256), ID, 0u);
             if (hf) mma_commit_cg2_mc(b_a1free, 0x3);
@@ -208,40 +223,62 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc3Shape<H>::THREADS
           const uint8_t* src = img + (size_t)(l - 2) * layer_bytes + (hf ? (size_t)C::KC * C::RA * 128 : 0);
           const uint32_t chunk = (uint32_t)rows * 128;
           if (warp == 0) {
-            for (int j = 0; j < C::NSJ; ++j) {
+            for (int j = 0; j < C::NSJ && p.prof != 3; ++j) {
               const int nch = (2 * j + 1 < C::KC) ? 2 : 1;
+              const long long t0_ = P3T();
               mbar_wait_lazy(b_wempty + 8 * st, ph ^ 1u);
+              if (p.prof) pc[5] += clock64() - t0_;
               mbar_arrive_expect_tx(b_wfull + 8 * st, nch * chunk);
               bulk_g2s(sW + st * C::STAGE, src + (size_t)(2 * j) * chunk, nch * chunk, b_wfull + 8 * st);
               if (++st == nst) { st = 0; ph ^= 1u; }
             }
           } else if (rank == 0) {
             // job (A, l): K-chunks 0..2 need epilogue (A, l-1), K-chunks 3.. need (B, l-1)
+            long long t0_ = P3T();
             if (hf == 0) { mbar_wait_cluster(b_afull, paA); paA ^= 1u; }
+            if (p.prof) pc[0] += clock64() - t0_;
             tc_fence_after();
-            int ks = 0;
+            // descriptors precomputed (the single issuing thread's scalar work per MMA would otherwise
+            // exceed the tensor pipe's N/2 clk per instruction); K-step k of a chunk = +32 B = +2
+            const uint64_t a_d0 = desc_sw128(sA);
+            const uint32_t chunk16 = (uint32_t)rows * 8;   // chunk bytes >> 4
+#pragma unroll
             for (int j = 0; j < C::NSJ; ++j) {
-              mbar_wait(b_wfull + 8 * st, ph);
-              mbar_wait_cluster(b_wpeer + 8 * st, ph);
+              t0_ = P3T();
+              if (p.prof != 3) {   // diagnostic 3: no weight streaming (stale ring contents)
+                mbar_wait(b_wfull + 8 * st, ph);
+                mbar_wait_cluster(b_wpeer + 8 * st, ph);
+              }
+              if (p.prof) pc[2] += clock64() - t0_;
               tc_fence_after();
-              for (int c = 0; c < 2 && 2 * j + c < C::KC; ++c) {
+              const uint64_t w_d = desc_sw128(sW + st * C::STAGE);
+#pragma unroll
+              for (int c = 0; c < 2; ++c) {
                 const int kc = 2 * j + c;
+                if (kc >= C::KC) break;
                 if (hf == 0 && kc == 3) {
+                  t0_ = P3T();
                   mbar_wait_cluster(b_afull + 8, paB);
+                  if (p.prof) pc[1] += clock64() - t0_;
                   paB ^= 1u;
                   tc_fence_after();
                 }
+                const uint64_t wc = w_d + (uint64_t)(c * chunk16);
                 const int nk = (kc * 64 + 64 <= HP) ? 4 : (HP - kc * 64) / 16;
-                for (int k = 0; k < nk; ++k, ++ks)
-                  mma_bf16_cg2(acc, desc_sw128(sA + kc * C::A_CHUNK + 32 * k),
-                               desc_sw128(sW + st * C::STAGE + c * chunk + 32 * k), ID, ks ? 1u : 0u);
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                  if (k < nk)
+                    mma_bf16_cg2(acc, a_d0 + (uint64_t)(kc * (C::A_CHUNK >> 4) + 2 * k), wc + (uint64_t)(2 * k), ID,
+                                 (kc | k) ? 1u : 0u);
+                // half A of the operand may be overwritten (epilogue (A, l)) once job B is past it
+                if (hf == 1 && kc == 2) mma_commit_cg2_mc(b_bhead, 0x3);
               }
               mma_commit_cg2_mc(b_wempty + 8 * st, 0x3);
               if (++st == nst) { st = 0; ph ^= 1u; }
             }
             mma_commit_cg2_mc(b_accfull + 8 * hf, 0x3);
           } else {
-            for (int j = 0; j < C::NSJ; ++j) {
+            for (int j = 0; j < C::NSJ && p.prof != 3; ++j) {
               mbar_wait(b_wfull + 8 * st, ph);
               mbar_arrive_remote(peer_wpeer + 8 * st);
               if (++st == nst) { st = 0; ph ^= 1u; }
@@ -249,6 +286,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc3Shape<H>::THREADS
           }
         }
         w.advance(tstride, T, s_tile_end, L);
+      }
+      if (p.prof) {
+        pc[4] = clock64() - t_start;
+        if (warp == 1) for (int k = 0; k < 5; ++k) g_kprof3[blockIdx.x][k] = pc[k];
+        else g_kprof3[blockIdx.x][5] = pc[5];
       }
     }
   } else if (warp == 2) {
@@ -300,6 +342,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc3Shape<H>::THREADS
     if (!w.done) { load_perm(w.t, cur); fill(cur); }
     if (w.t + tstride < T) load_perm(w.t + tstride, nxt);
     uint32_t pa1f = 0, piod = 0;
+    unsigned long long io_wait = 0;
 #pragma unroll 1
     while (!w.done) {
       if (w.l == 1 && w.half == 1) {
@@ -316,7 +359,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc3Shape<H>::THREADS
         }
       }
       if (w.l == w.d && w.half == 1) {
+        const long long t0_ = P3T();
         mbar_wait_lazy(b_iodone, piod);
+        if (p.prof) io_wait += clock64() - t0_;
         piod ^= 1u;
         const float cs = tcs[w.d];
         float y[4];
@@ -336,6 +381,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc3Shape<H>::THREADS
       }
       w.advance(tstride, T, s_tile_end, L);
     }
+    if (p.prof && lane == 0) g_kprof3[blockIdx.x][11] = io_wait;
   } else if (warp >= 3) {
     // =========================== epilogue (16 warps; steps (A, l), (B, l) of the current tile)
     const int ew = warp - 3;
@@ -356,10 +402,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc3Shape<H>::THREADS
     float ylin[4] = {0.f, 0.f, 0.f, 0.f};
     uint32_t pe[2] = {0u, 0u};
     uint32_t ppf = 1u;   // part_free parity: first tile passes immediately
-    bool b_seen = false;   // acc_full[B] of this layer already consumed by the half-A stores
+    uint32_t pbh = 0;      // b_bhead parity (one phase per hidden-layer job B)
+    unsigned long long ep[5] = {};
+    const long long t_start = P3T();
     // Columns [c0, c0 + NCH * 8) of one half: TMEM -> sin -> tail partials, h packed to BF16 in registers.
-    // The A-operand stores of half A must wait until job (B, l) -- issued after job (A, l) and reading
-    // all of H_{l-1} -- has completed (acc_full[B]); half B's job is then complete by construction.
+    // The A-operand stores of half A (l >= 2) must wait until job (B, l) -- issued after job (A, l) and
+    // reading all of H_{l-1} -- is past K-chunks 0..2 (b_bhead); half B's job is complete by then
+    // (acc_full[B]).  Layer-1 jobs read the A1 buffer, not the A operand.
     auto half_cols = [&](auto nch_c, int c0, int l, bool store, bool wait_b) {
       constexpr int NCH = decltype(nch_c)::value;
       const float* bias = tb + (l - 1) * HP + c0 + 2 * tq;
@@ -368,6 +417,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc3Shape<H>::THREADS
       uint32_t pk[NCH][4];
 #pragma unroll
       for (int i0 = 0; i0 < NCH; i0 += 2) {
+        if (p.prof >= 2) break;   // diagnostic: MMA / weight-stream throughput without epilogue work
         uint32_t r0[8], r1[8];
         if (i0 + 1 < NCH) {
           tmem_ld_16x256b<2>(tm_q + c0 + 8 * i0, r0);
@@ -404,9 +454,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc3Shape<H>::THREADS
       for (int k = 0; k < 4; ++k) ylin[k] += yv[k].x + yv[k].y;
       if (store) {
         if (wait_b) {
-          mbar_wait(b_accfull + 8, pe[1]);
-          pe[1] ^= 1u;
-          b_seen = true;
+          const long long t0_ = P3T();
+          mbar_wait(b_bhead, pbh);
+          if (p.prof) ep[2] += clock64() - t0_;
+          pbh ^= 1u;
         }
 #pragma unroll
         for (int i = 0; i < NCH; ++i) {
@@ -421,14 +472,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc3Shape<H>::THREADS
 #pragma unroll 1
     while (!w.done) {
       const int hf = w.half, l = w.l, d = w.d;
-      if (hf == 0 || !b_seen) {
+      {
+        const long long t0_ = P3T();
         mbar_wait(b_accfull + 8 * hf, pe[hf]);
         pe[hf] ^= 1u;
+        if (p.prof) ep[hf] += clock64() - t0_;
       }
-      if (hf == 1) b_seen = false;
-      tc_fence_after();
+      ep[4] += 1;
       const bool store = l != d;
-      if (hf == 0) half_cols(std::integral_constant<int, C::NA / 32>{}, cq * (C::NA / 4), l, store, true);
+      // every hidden-layer job B completes one b_bhead phase: consumed by the half-A stores, or here
+      if (hf == 1 && l >= 2 && !store) { mbar_wait(b_bhead, pbh); pbh ^= 1u; }
+      tc_fence_after();
+      if (hf == 0) half_cols(std::integral_constant<int, C::NA / 32>{}, cq * (C::NA / 4), l, store, l >= 2);
       else half_cols(std::integral_constant<int, C::NB / 32>{}, C::NA + cq * (C::NB / 4), l, store, false);
       if (store) fence_proxy_async_smem();
       tc_fence_before();
@@ -438,8 +493,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc3Shape<H>::THREADS
         else mbar_arrive_remote(afull_dst0 + 8 * hf);
       }
       if (l == d && hf == 1) {
+        const long long t0_ = P3T();
         mbar_wait(b_partfree, ppf);
         ppf ^= 1u;
+        if (p.prof) ep[3] += clock64() - t0_;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const float v = quad_sum(ylin[k]);
@@ -450,6 +507,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc3Shape<H>::THREADS
         if (lane == 0) mbar_arrive(b_iodone);
       }
       w.advance(tstride, T, s_tile_end, L);
+    }
+    if (p.prof && warp == 3 && lane == 0) {
+      g_kprof3[blockIdx.x][6] = ep[0];
+      g_kprof3[blockIdx.x][7] = ep[1];
+      g_kprof3[blockIdx.x][8] = ep[2];
+      g_kprof3[blockIdx.x][9] = clock64() - t_start;
+      g_kprof3[blockIdx.x][10] = ep[4];
+      g_kprof3[blockIdx.x][12] = ep[3];
     }
   }
   tc_fence_before();
@@ -566,9 +631,32 @@ cudaError_t launch_tmlp_tc3(const MlpDev& m, const float* pts, const uint32_t* p
     if (smem_for3<336>(m.pt_floats, m.L, n) <= kSmemMax3) nst = n;
   if (!nst) return cudaErrorInvalidConfiguration;
   const size_t sm = smem_for3<336>(m.pt_floats, m.L, nst);
-  Tc3Params p{m, pts, perm, meta, out, nst};
-  k_tmlp_wide<336><<<num_sms & ~1, Tc3Shape<336>::THREADS, sm, st>>>(p);
-  return cudaGetLastError();
+  static const int prof = getenv("SAND_KPROF") ? atoi(getenv("SAND_KPROF")) : 0;
+  Tc3Params p{m, pts, perm, meta, out, nst, prof};
+  const int grid = num_sms & ~1;
+  k_tmlp_wide<336><<<grid, Tc3Shape<336>::THREADS, sm, st>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (prof && e == cudaSuccess) {
+    static unsigned long long h[160][kProf3];
+    e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) e = cudaMemcpyFromSymbol(h, g_kprof3, sizeof h);
+    if (e == cudaSuccess) {
+      double a[kProf3] = {0};
+      int nl = 0;
+      for (int b = 0; b < grid; ++b) {
+        for (int k = 0; k < kProf3; ++k)
+          if (k > 4 || (b & 1) == 0) a[k] += (double)h[b][k];
+        nl += (b & 1) == 0;
+      }
+      for (int k = 0; k < kProf3; ++k) a[k] /= (k <= 4 ? nl : grid);
+      fprintf(stderr,
+              "[kprof3] nst %d | MMA total %.0f wait_aA %.0f wait_aB %.0f wait_W %.0f wait_l1 %.0f | prod wait_empty "
+              "%.0f | epi total %.0f steps %.0f wait_accA %.0f wait_accB %.0f wait_accB_store %.0f wait_part %.0f | "
+              "IO wait %.0f\n",
+              nst, a[4], a[0], a[1], a[2], a[3], a[5], a[9], a[10], a[6], a[7], a[8], a[12], a[11]);
+    }
+  }
+  return e;
 }
 
 cudaError_t prepare_tc3() {
