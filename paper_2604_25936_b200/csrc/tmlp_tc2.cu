@@ -77,7 +77,7 @@ struct Tc2Params {
 //  4 producer wait w_empty  5 producer loads
 //  6 epi wait acc_full  7 epi busy (steps excl. waits)  8 epi loop total  9 epi steps
 //  10 IO wait  11 IO busy
-constexpr int kProfSlots = 12;
+constexpr int kProfSlots = 14;   // + 12 epi publish, 13 epi tile end
 __device__ unsigned long long g_kprof[160][kProfSlots];
 
 // ------------------------------------------------------------------------------ step sequence
@@ -273,7 +273,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
         }
         if (warp == 0) {
           const uint8_t* src = img + (size_t)(l - 2) * 2 * C::KC * C::WH_CHUNK;
-          for (int j = 0; j < C::NSJ; ++j) {
+          for (int j = 0; j < C::NSJ && p.prof != 3; ++j) {
             const long long c0_ = p.prof ? clock64() : 0;
             mbar_wait_lazy(b_wempty + 8 * st, ph ^ 1u);
             if (p.prof) { pc[4] += clock64() - c0_; pc[5] += 1; }
@@ -286,28 +286,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
           long long c0_ = 0;
           tc_fence_after();
           const uint32_t acc = tmem_base + (uint32_t)(s * H);
-          const uint32_t a_base = sA + s * C::A_BYTES;
+          // descriptors precomputed once per job / stage: a K-step of 32 B is +2 in the address field.
+          // (Computing them per MMA costs the single issuing thread more than the tensor pipe's time.)
+          const uint64_t a_d = desc_sw128(sA + s * C::A_BYTES);
+#pragma unroll
           for (int j = 0; j < C::NSJ; ++j) {
             c0_ = p.prof ? clock64() : 0;
-            mbar_wait(b_wfull + 8 * st, ph);
-            mbar_wait_cluster(b_wpeer + 8 * st, ph);
+            if (p.prof != 3) { mbar_wait(b_wfull + 8 * st, ph);
+            mbar_wait_cluster(b_wpeer + 8 * st, ph); }   // diagnostic 3: no weight streaming
             if (p.prof) pc[1] += clock64() - c0_;
             tc_fence_after();
+            const uint64_t w_d = desc_sw128(sW + st * C::STAGE);
 #pragma unroll
             for (int c = 0; c < C::SC; ++c) {
               const int kc = j * C::SC + c;
-              const uint32_t w_base = sW + st * C::STAGE + c * C::WH_CHUNK;
 #pragma unroll
               for (int k = 0; k < 4; ++k)
-                mma_bf16_cg2(acc, desc_sw128(a_base + kc * C::A_CHUNK + 32 * k), desc_sw128(w_base + 32 * k), ID,
-                             (kc | k) ? 1u : 0u);
+                mma_bf16_cg2(acc, a_d + (uint64_t)(kc * (C::A_CHUNK >> 4) + 2 * k),
+                             w_d + (uint64_t)(c * (C::WH_CHUNK >> 4) + 2 * k), ID, (kc | k) ? 1u : 0u);
             }
             mma_commit_cg2_mc(b_wempty + 8 * st, 0x3);
             if (++st == nst) { st = 0; ph ^= 1u; }
           }
           mma_commit_cg2_mc(b_accfull + 8 * s, 0x3);
         } else {
-          for (int j = 0; j < C::NSJ; ++j) {
+          for (int j = 0; j < C::NSJ && p.prof != 3; ++j) {
             mbar_wait(b_wfull + 8 * st, ph);
             mbar_arrive_remote(peer_wpeer + 8 * st);
             if (++st == nst) { st = 0; ph ^= 1u; }
@@ -463,7 +466,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
     const float* tc1 = tab + p.m.pt_off_c1;    // [L] (MULT, index l-1)
     const uint32_t bar_q = 1 + q;              // per-quadrant named barrier (tile-end / MULT reductions)
     const uint32_t afull_dst0 = rank == 0 ? b_afull : mapa_shared(b_afull, 0);
-    unsigned long long ep_wait = 0, ep_busy = 0, ep_steps = 0;
+    unsigned long long ep_wait = 0, ep_busy = 0, ep_steps = 0, ep_pub = 0, ep_tend = 0;
 
     auto publish = [&](int s, bool wrote_a) {
       if (wrote_a) fence_proxy_async_smem();
@@ -498,6 +501,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
       const float* a1 = ta1 + (l - 2) * H + c0 + 2 * tq;
       const bool prod = TAIL == SAND_TAIL_MULT && l >= 2;
       const uint32_t tm = tm_q + (uint32_t)(s * H);
+      if (p.prof < 2)   // diagnostic 2/3: no epilogue math
 #pragma unroll
       for (int bb = 0; bb < C::HQ / BW; ++bb) {
         uint32_t r0[4 * CB], r1[4 * CB];   // lane block 0 (rows R0, R1) and block 1 (rows R2, R3)
@@ -557,7 +561,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
 #pragma unroll
         for (int k = 0; k < 4; ++k) e.ylin[k] += yv[k].x + yv[k].y;
       }
+      const long long cp_ = p.prof ? clock64() : 0;
       publish(s, store);
+      if (p.prof) ep_pub += clock64() - cp_;
+      const long long ct_ = p.prof ? clock64() : 0;
       if (l == d) {
         // tile end: every row reduced over its quad (shuffles); each warp hands its column quarter's
         // partials to the IO warp (which adds the 4 quarters and the tail-bias prefix sum).  No barrier
@@ -575,6 +582,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
         __syncwarp();
         if (lane == 0) mbar_arrive(b_iodone + 8 * s);
       }
+      if (p.prof) ep_tend += clock64() - ct_;
       e.w.advance(tstride, T, s_tile_end, L);
       if (p.prof) { ep_wait += c1_ - c0_; ep_busy += clock64() - c1_; ep_steps += 1; }
     };
@@ -597,6 +605,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
       g_kprof[blockIdx.x][7] = ep_busy;
       g_kprof[blockIdx.x][8] = clock64() - t_start;
       g_kprof[blockIdx.x][9] = ep_steps;
+      g_kprof[blockIdx.x][12] = ep_pub;
+      g_kprof[blockIdx.x][13] = ep_tend;
     }
   }
   tc_fence_before();
@@ -708,8 +718,8 @@ static cudaError_t launch_tc2_t(const MlpDev& m, const float* pts, const uint32_
         for (int k = 0; k < kProfSlots; ++k) a[k] += (double)h[b][k] / (k < 4 ? grid / 2 : grid);
       fprintf(stderr,
               "[kprof] nst %d | MMA: total %.0f wait_A %.0f wait_W %.0f jobs %.0f | producer: wait_empty %.0f "
-              "loads %.0f | epilogue(w4): total %.0f wait_acc %.0f busy %.0f steps %.0f | IO: wait %.0f busy %.0f\n",
-              nst, a[2], a[0], a[1], a[3], a[4], a[5], a[8], a[6], a[7], a[9], a[10], a[11]);
+              "loads %.0f | epilogue(w4): total %.0f wait_acc %.0f busy %.0f steps %.0f publish %.0f tile_end %.0f | IO: wait %.0f busy %.0f\n",
+              nst, a[2], a[0], a[1], a[3], a[4], a[5], a[8], a[6], a[7], a[9], a[12], a[13], a[10], a[11]);
     }
   }
   return e;

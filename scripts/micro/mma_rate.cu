@@ -13,7 +13,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
     k_rate(int N, int ksteps, int jobs, int ldtm, int cevery, int tcol, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t sm[];
   const uint32_t base = (smem_u32(sm) + 1023) & ~1023u;
-  __shared__ uint64_t bar[3];
+  __shared__ uint64_t bar[4];
   __shared__ uint32_t tslot;
   const uint32_t rank = cluster_ctarank();
   const int warp = threadIdx.x >> 5;
@@ -21,6 +21,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
     mbar_init(smem_u32(&bar[0]), 1);
     mbar_init(smem_u32(&bar[1]), 1);
     mbar_init(smem_u32(&bar[2]), 1);
+    mbar_init(smem_u32(&bar[3]), 1);
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc_cg2(smem_u32(&tslot), 512);
@@ -45,12 +46,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
         const uint64_t a0 = desc_sw128(sA), b0 = desc_sw128(sB);
         const uint64_t bstep = (uint64_t)((N / 2) * 128 >> 4);
 #pragma unroll
-        for (int k = 0; k < 22; ++k)
+        for (int k = 0; k < 22; ++k) {
           mma_bf16_cg2(tm, a0 + (uint64_t)((k >> 2) * (16384 >> 4) + 2 * (k & 3)), b0 + (uint64_t)(k >> 2) * bstep + 2 * (k & 3),
                        id, k ? 1u : 0u);
+          if (tcol == 8 && (k & 7) == 7) mma_commit_cg2_mc(smem_u32(&bar[2]), 0x3);
+          if (tcol == 9 && (k & 7) == 7) mma_commit_cg2_mc(smem_u32(&bar[2 + ((k >> 3) & 1)]), 0x3);
+        }
       } else {
       for (int k = 0; k < ksteps; ++k) {
-        mma_bf16_cg2(tm + (uint32_t)tcol, desc_sw128(sA + (k >> 2) * 16384 + 32 * (k & 3)),
+        mma_bf16_cg2(tm, desc_sw128(sA + (k >> 2) * 16384 + 32 * (k & 3)),
                      desc_sw128(sB + (k >> 2) * (N / 2) * 128 + 32 * (k & 3)), id, k ? 1u : 0u);
         if (cevery > 0 && (k % cevery) == cevery - 1) mma_commit_cg2_mc(smem_u32(&bar[2]), 0x3);
       }
@@ -102,7 +106,7 @@ int main() {
   cudaFuncSetAttribute(k_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int Ns[] = {128, 192, 256};
   struct Cfg { int N, ldtm, cevery, tcol; };
-  const Cfg cfgs[] = {{192, 0, 0, 0}, {192, 0, 100, 0}, {160, 0, 100, 0}, {128, 0, 100, 0}, {256, 0, 100, 0}, {256, 0, 0, 0}};
+  const Cfg cfgs[] = {{256, 0, 100, 0}, {256, 0, 100, 8}, {256, 0, 100, 9}, {192, 0, 100, 0}, {192, 0, 100, 8}};
   for (int rep = 0; rep < 2; ++rep)
   for (const Cfg& c : cfgs) {
       const int N = c.N, ldtm = c.ldtm;
