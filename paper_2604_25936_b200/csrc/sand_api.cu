@@ -272,12 +272,14 @@ extern "C" int sand_load_weights(sand_ctx* ctx, const float* blob, size_t n_floa
     // polynomial columns: the first np of every 32 within each epilogue thread's column quarter
     auto scale = [&](int j) { return ((j % (H / 4)) % 32) < np ? (double)w0 * kInvPi : (double)w0; };
     m.pt_npoly = np;
-    tc2_table_layout(L, H, tail, &m);
+    tc2_table_layout(L, H, tail, &m, true);
     std::vector<float> pt((size_t)m.pt_floats, 0.f);
+    // interleaved per column pair: [i][j/2] = (bias_j, bias_j+1, a_j, a_j+1)
+    auto ba = [&](int i, int j) { return m.pt_off_bias + (size_t)i * 2 * H + (size_t)(j / 2) * 4 + (j & 1); };
     for (int i = 1; i < L; ++i)
-      for (int j = 0; j < H; ++j) pt[m.pt_off_bias + (size_t)i * H + j] = (float)(scale(j) * b[i][j]);
+      for (int j = 0; j < H; ++j) pt[ba(i, j)] = (float)(scale(j) * b[i][j]);
     for (int i = 0; i < L; ++i) {
-      std::memcpy(&pt[m.pt_off_a + (size_t)i * H], a[i], sizeof(float) * H);
+      for (int j = 0; j < H; ++j) pt[ba(i, j) + 2] = a[i][j];
       pt[m.pt_off_c + i] = c[i];
       pt[m.pt_off_c1 + i] = c1[i];
     }

@@ -100,7 +100,7 @@ cudaError_t launch_leaf_max(const uint8_t* d, long long n_leaves, int spl, uint8
 // CTA-pair kernel (tmlp_tc2.cu)
 bool tc2_available(int H);
 bool tc2_usable(int L, int H, int tail);           // H supported and the kernel's shared memory fits
-void tc2_table_layout(int L, int H, int tail, MlpDev* m);   // pair-table offsets (pt_off_*, pt_floats)
+void tc2_table_layout(int L, int H, int tail, MlpDev* m, bool interleave);   // pair-table offsets (pt_off_*, pt_floats)
 int tc2_npoly();   // polynomial columns per 32 in use (SAND_NPOLY env override: 0, 8, 16)
 cudaError_t launch_tmlp_tc2(const MlpDev& m, const float* pts, const uint32_t* perm, const QueryMeta* meta,
                             float* out, int num_sms, cudaStream_t st);

@@ -459,8 +459,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
     const uint32_t a_st = sA + (uint32_t)(4 * q + (lane >> 3)) * 1024 + (uint32_t)(lane & 7) * 128;
     const float2 SM2 = make_float2(p.m.omega0, p.m.omega0);
     const float2 SP2 = make_float2(p.m.omega0 * 0.15915494309189535f, p.m.omega0 * 0.15915494309189535f);
-    const float* tb = tab + p.m.pt_off_bias;   // [L][H] (row 0 = 0: b_1 is inside the layer-1 MMA)
-    const float* ta = tab + p.m.pt_off_a;      // [L][H]
+    const float* tba = tab + p.m.pt_off_bias;  // [L][H/2][bias pair, a pair] (row 0 bias = 0: b_1 is in the layer-1 MMA)
     const float* ta1 = tab + p.m.pt_off_a1;    // [L-1][H] (MULT)
     const float* tc0 = tab + p.m.pt_off_c;     // [L]
     const float* tc1 = tab + p.m.pt_off_c1;    // [L] (MULT, index l-1)
@@ -496,8 +495,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
       e.pe ^= 1u;
       tc_fence_after();
       const bool store = l != d;
-      const float* bias = tb + (l - 1) * H + c0 + 2 * tq;
-      const float* a = ta + (l - 1) * H + c0 + 2 * tq;
+      const float* ba = tba + (l - 1) * 2 * H + (c0 + 2 * tq) * 2;
       const float* a1 = ta1 + (l - 2) * H + c0 + 2 * tq;
       const bool prod = TAIL == SAND_TAIL_MULT && l >= 2;
       const uint32_t tm = tm_q + (uint32_t)(s * H);
@@ -512,8 +510,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
 #pragma unroll
         for (int i = 0; i < CB; ++i) {
           const int jc = bb * BW + 8 * i;     // chunk column offset within this column quarter
-          const float2 b2 = *reinterpret_cast<const float2*>(bias + jc);
-          const float2 a2 = *reinterpret_cast<const float2*>(a + jc);
+          const float4 ba4 = *reinterpret_cast<const float4*>(ba + 2 * jc);
+          const float2 b2 = make_float2(ba4.x, ba4.y), a2 = make_float2(ba4.z, ba4.w);
           float2 c2 = make_float2(0.f, 0.f);
           if (TAIL == SAND_TAIL_MULT && prod) c2 = *reinterpret_cast<const float2*>(a1 + jc);
           const uint32_t u = (uint32_t)((c0 + jc) >> 3);
@@ -640,12 +638,14 @@ static int pick_nst2(long long pt_floats, int L, int tail) {
 
 bool tc2_available(int H) { return H == 64 || H == 128 || H == 256; }
 
-void tc2_table_layout(int L, int H, int tail, MlpDev* m) {
+void tc2_table_layout(int L, int H, int tail, MlpDev* m, bool interleave) {
   auto al4 = [](long long v) { return (v + 3) & ~3ll; };
   m->pt_off_l1 = 0;
   m->pt_off_bias = 0;
-  m->pt_off_a = al4(m->pt_off_bias + (long long)L * H);
-  m->pt_off_a1 = al4(m->pt_off_a + (long long)L * H);
+  // interleaved (this kernel): [L][H/2][4] = (bias_c, bias_c+1, a_c, a_c+1) per column pair, one 16-byte
+  // shared load per 8-column chunk; separate (wide kernel): bias [L][H], a [L][H]
+  m->pt_off_a = interleave ? m->pt_off_bias + 2 : al4(m->pt_off_bias + (long long)L * H);
+  m->pt_off_a1 = interleave ? al4(m->pt_off_bias + 2ll * L * H) : al4(m->pt_off_a + (long long)L * H);
   m->pt_off_c = al4(m->pt_off_a1 + (tail == SAND_TAIL_MULT ? (long long)(L - 1) * H : 0));
   m->pt_off_c1 = al4(m->pt_off_c + L);
   m->pt_off_csum = al4(m->pt_off_c1 + L);
@@ -655,7 +655,7 @@ void tc2_table_layout(int L, int H, int tail, MlpDev* m) {
 bool tc2_usable(int L, int H, int tail) {
   if (!tc2_available(H)) return false;
   MlpDev m{};
-  tc2_table_layout(L, H, tail, &m);
+  tc2_table_layout(L, H, tail, &m, true);
   switch (H) {
     case 64: return pick_nst2<64>(m.pt_floats, L, tail) > 0;
     case 128: return pick_nst2<128>(m.pt_floats, L, tail) > 0;

@@ -541,7 +541,7 @@ int tc3_padded_width(int H) { return (H + 31) / 32 * 32; }
 bool tc3_usable(int L, int H, int tail) {
   if (!tc3_available(H, tail)) return false;
   MlpDev m{};
-  tc2_table_layout(L, tc3_padded_width(H), tail, &m);
+  tc2_table_layout(L, tc3_padded_width(H), tail, &m, false);
   return smem_for3<336>(m.pt_floats, L, 2) <= kSmemMax3;
 }
 
@@ -550,7 +550,7 @@ void tc3_build_host(int L, int H, float w0, const float* const* W, const float* 
                     std::vector<uint8_t>* img) {
   using C = Tc3Shape<336>;
   const int HP = C::HP;
-  tc2_table_layout(L, HP, SAND_TAIL_LINEAR, m);
+  tc2_table_layout(L, HP, SAND_TAIL_LINEAR, m, false);
   m->pt_npoly = 0;
   tables->assign((size_t)m->pt_floats, 0.f);
   for (int i = 1; i < L; ++i)
