@@ -409,12 +409,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc3Shape<H>::THREADS
     // The A-operand stores of half A (l >= 2) must wait until job (B, l) -- issued after job (A, l) and
     // reading all of H_{l-1} -- is past K-chunks 0..2 (b_bhead); half B's job is complete by then
     // (acc_full[B]).  Layer-1 jobs read the A1 buffer, not the A operand.
+    // Chunks are stored as they are computed, except that with wait_b the first HOLD chunks are held in
+    // registers until b_bhead (by then job B is normally past K-chunk 2).
     auto half_cols = [&](auto nch_c, int c0, int l, bool store, bool wait_b) {
       constexpr int NCH = decltype(nch_c)::value;
+      constexpr int HOLD = 4;
       const float* bias = tb + (l - 1) * HP + c0 + 2 * tq;
       const float* a = ta + (l - 1) * HP + c0 + 2 * tq;
       float2 yv[4] = {};
-      uint32_t pk[NCH][4];
+      uint32_t held[HOLD][4];
+      auto put = [&](int ci, const uint32_t (&pk)[4]) {
+        const uint32_t u = (uint32_t)((c0 + 8 * ci) >> 3);
+        stmatrix_x4(a_st + (u >> 3) * C::A_CHUNK + (((u & 7u) ^ (uint32_t)(lane & 7)) << 4), pk);
+      };
+      auto release = [&]() {
+        const long long t0_ = P3T();
+        mbar_wait(b_bhead, pbh);
+        if (p.prof) ep[2] += clock64() - t0_;
+        pbh ^= 1u;
+#pragma unroll
+        for (int ci = 0; ci < HOLD; ++ci)
+          if (ci < NCH) put(ci, held[ci]);
+      };
 #pragma unroll
       for (int i0 = 0; i0 < NCH; i0 += 2) {
         if (p.prof >= 2) break;   // diagnostic: MMA / weight-stream throughput without epilogue work
@@ -436,35 +452,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc3Shape<H>::THREADS
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
           if (i0 + i < NCH) {
-            const int jc = 8 * (i0 + i);
+            const int ci = i0 + i;
+            const int jc = 8 * ci;
             const float2 b2 = *reinterpret_cast<const float2*>(bias + jc);
             const float2 a2 = *reinterpret_cast<const float2*>(a + jc);
+            uint32_t pk[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const uint32_t* r = k < 2 ? r0 : r1;
               const int o = 4 * i + 2 * (k & 1);
               const float2 h = sin_mufu2(__ffma2_rn(make_float2(__uint_as_float(r[o]), __uint_as_float(r[o + 1])), SM2, b2));
               yv[k] = __ffma2_rn(a2, h, yv[k]);
-              pk[i0 + i][k] = pack_bf16x2(h.x, h.y);
+              pk[k] = pack_bf16x2(h.x, h.y);
+            }
+            if (store) {
+              if (ci < HOLD) {
+                if (wait_b) {
+#pragma unroll
+                  for (int k = 0; k < 4; ++k) held[ci][k] = pk[k];
+                } else {
+                  put(ci, pk);
+                }
+              } else {
+                if (ci == HOLD && wait_b) release();
+                put(ci, pk);
+              }
             }
           }
         }
       }
+      if (store && wait_b && (NCH <= HOLD || p.prof >= 2)) release();   // (diagnostic modes skip the loop)
 #pragma unroll
       for (int k = 0; k < 4; ++k) ylin[k] += yv[k].x + yv[k].y;
-      if (store) {
-        if (wait_b) {
-          const long long t0_ = P3T();
-          mbar_wait(b_bhead, pbh);
-          if (p.prof) ep[2] += clock64() - t0_;
-          pbh ^= 1u;
-        }
-#pragma unroll
-        for (int i = 0; i < NCH; ++i) {
-          const uint32_t u = (uint32_t)((c0 + 8 * i) >> 3);
-          stmatrix_x4(a_st + (u >> 3) * C::A_CHUNK + (((u & 7u) ^ (uint32_t)(lane & 7)) << 4), pk[i]);
-        }
-      }
     };
     WideWalk w;
     w.ti = 0;
