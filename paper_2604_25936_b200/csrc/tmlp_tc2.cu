@@ -39,6 +39,10 @@
 #include "ptx.cuh"
 #include "sand_internal.h"
 
+#ifndef SAND_ABL
+#define SAND_ABL 0   // ablation builds for timing studies (scripts/abl.sh); 0 = the product kernel
+#endif
+
 namespace sand {
 
 template <int H>
@@ -229,8 +233,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
   const long long T = p.meta->total_tiles;
   const long long tstride = 2ll * npairs;
 
-  if (warp == 0 || warp == 1) {
-    if (lane == 0) {
+  if ((warp == 0 && lane == 0) || warp == 1) {
+    {
+      // warp 0: producer (lane 0); warp 1: MMA issuer (leader CTA) / relay (odd CTA), all 32 lanes converged,
+      // side effects by one elected lane
       // producer / MMA issuer / relay: one job per epilogue step, in the epilogue's order
       SlotWalk w0, w1;
       w0.start(pair, T, s_tile_end, L);
@@ -265,10 +271,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
           mbar_wait_cluster(b_a1full + 8 * s, (uint32_t)(w.ti & 1));
           if (p.prof) { pc[0] += clock64() - c0_; pc[3] += 1; }
           tc_fence_after();
-          mma_bf16_cg2(tmem_base + (uint32_t)(s * H), desc_nosw(sA1 + s * C::A1_BYTES, 128, 256),
+          mma_bf16_cg2_w(tmem_base + (uint32_t)(s * H), desc_nosw(sA1 + s * C::A1_BYTES, 128, 256),
                        desc_nosw(sW1, 128, 256), ID, 0u);
-          mma_commit_cg2_mc(b_a1free + 8 * s, 0x3);
-          mma_commit_cg2_mc(b_accfull + 8 * s, 0x3);
+          mma_commit_cg2_mc_w(b_a1free + 8 * s, 0x3);
+          mma_commit_cg2_mc_w(b_accfull + 8 * s, 0x3);
           return;
         }
         if (warp == 0) {
@@ -300,19 +306,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
 #pragma unroll
             for (int c = 0; c < C::SC; ++c) {
               const int kc = j * C::SC + c;
-#pragma unroll
-              for (int k = 0; k < 4; ++k)
-                mma_bf16_cg2(acc, a_d + (uint64_t)(kc * (C::A_CHUNK >> 4) + 2 * k),
-                             w_d + (uint64_t)(c * (C::WH_CHUNK >> 4) + 2 * k), ID, (kc | k) ? 1u : 0u);
+              mma4_bf16_cg2_w(acc, a_d + (uint64_t)(kc * (C::A_CHUNK >> 4)), w_d + (uint64_t)(c * (C::WH_CHUNK >> 4)), ID,
+                              kc ? 1u : 0u);
             }
-            mma_commit_cg2_mc(b_wempty + 8 * st, 0x3);
+            mma_commit_cg2_mc_w(b_wempty + 8 * st, 0x3);
             if (++st == nst) { st = 0; ph ^= 1u; }
           }
-          mma_commit_cg2_mc(b_accfull + 8 * s, 0x3);
+          mma_commit_cg2_mc_w(b_accfull + 8 * s, 0x3);
         } else {
           for (int j = 0; j < C::NSJ && p.prof != 3; ++j) {
             mbar_wait(b_wfull + 8 * st, ph);
-            mbar_arrive_remote(peer_wpeer + 8 * st);
+            if (lane == 0) mbar_arrive_remote(peer_wpeer + 8 * st);
+            __syncwarp();
             if (++st == nst) { st = 0; ph ^= 1u; }
           }
         }
@@ -324,7 +329,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
       }
       if (p.prof) {
         pc[2] = clock64() - t_start;
-        if (warp == 1 && rank == 0)
+        if (warp == 1 && rank == 0 && lane == 0)
           for (int k = 0; k < 4; ++k) g_kprof[blockIdx.x][k] = pc[k];
         if (warp == 0)
           for (int k = 4; k < 6; ++k) g_kprof[blockIdx.x][k] = pc[k];
@@ -503,14 +508,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
 #pragma unroll
       for (int bb = 0; bb < C::HQ / BW; ++bb) {
         uint32_t r0[4 * CB], r1[4 * CB];   // lane block 0 (rows R0, R1) and block 1 (rows R2, R3)
+#if SAND_ABL == 3   // ablation build (timing only): no TMEM loads
+#pragma unroll
+        for (int q_ = 0; q_ < 4 * CB; ++q_) { r0[q_] = __float_as_uint(0.01f * (lane + q_ + bb)); r1[q_] = r0[q_] ^ 1u; }
+#else
         tmem_ld_16x256b<CB>(tm + bb * BW, r0);
         tmem_ld_16x256b<CB>(tm + (16u << 16) + bb * BW, r1);
         tmem_wait_ld_dep(r0);
         tmem_wait_ld_dep(r1);
+#endif
 #pragma unroll
         for (int i = 0; i < CB; ++i) {
           const int jc = bb * BW + 8 * i;     // chunk column offset within this column quarter
+#if SAND_ABL == 2   // ablation build (timing only): no table loads
+          const float4 ba4 = make_float4(0.1f * jc, 0.2f, 0.3f, 0.4f * jc);
+#else
           const float4 ba4 = *reinterpret_cast<const float4*>(ba + 2 * jc);
+#endif
           const float2 b2 = make_float2(ba4.x, ba4.y), a2 = make_float2(ba4.z, ba4.w);
           float2 c2 = make_float2(0.f, 0.f);
           if (TAIL == SAND_TAIL_MULT && prod) c2 = *reinterpret_cast<const float2*>(a1 + jc);
@@ -526,7 +540,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
               h = sin_poly2(__ffma2_rn(acc, SP2, b2));
             } else {
               const float2 z = __ffma2_rn(acc, SM2, b2);
+#if SAND_ABL == 4   // ablation build (timing only): no sine
+              h = z;
+#else
               h = make_float2(__sinf(z.x), __sinf(z.y));
+#endif
             }
             yv[k] = __ffma2_rn(a2, h, yv[k]);
             if (TAIL == SAND_TAIL_MULT) yv1[k] = __ffma2_rn(c2, h, yv1[k]);
@@ -534,7 +552,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
           }
           // the 4 rows x 8 columns of this chunk are four 8x8 b16 matrices in the m8n8 fragment layout:
           // one stmatrix.x4 (lane provides the address of row lane % 8 of matrix lane / 8)
+#if SAND_ABL == 1   // ablation build (timing only): no A-operand stores
+          if (store && pk[0] == 0x12345678u && pk[1] == 0x9u) stmatrix_x4(aSt, pk);
+#else
           if (store) stmatrix_x4(aSt + (u >> 3) * C::A_CHUNK + (((u & 7u) ^ (uint32_t)(lane & 7)) << 4), pk);
+#endif
         }
       }
       if (prod) {

@@ -61,7 +61,7 @@ def load_library(path=None):
     global _lib
     if _lib is not None:
         return _lib
-    path = path or _LIB_PATH
+    path = path or os.environ.get("SAND_LIB") or _LIB_PATH   # SAND_LIB: diagnostic A/B builds
     if not os.path.exists(path):
         raise ImportError(f"libsand.so not found at {path}; run `python -m paper_2604_25936_b200.build`")
     lib = ctypes.CDLL(path)

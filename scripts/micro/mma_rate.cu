@@ -24,6 +24,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
     mbar_init(smem_u32(&bar[3]), 1);
     fence_mbar_init();
   }
+  for (int i = threadIdx.x; i < 196608 / 4; i += blockDim.x)
+    reinterpret_cast<uint32_t*>(sm + (base - smem_u32(sm)))[i] = 0x3c003c00u ^ (uint32_t)(i * 2654435761u & 0x007f007fu);
+  fence_proxy_async_smem();
   if (warp == 0) tmem_alloc_cg2(smem_u32(&tslot), 512);
   tc_fence_before();
   __syncthreads();
@@ -41,7 +44,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
       if (j >= 2) { mbar_wait(smem_u32(&bar[s]), ph[s]); ph[s] ^= 1u; }
       tc_fence_after();
       const long long ti0 = clock64();
-      if (cevery == 100) {
+      if (cevery == 200) {
+        // tc2-like: A alternates between two 64 KB slot buffers, B rotates over two 32 KB ring stages,
+        // accumulator alternates TMEM columns 0 / 256, commit per stage; 16 MMAs (K = 256) per job
+        const uint64_t a0 = desc_sw128(sA + (uint32_t)s * 65536u);
+        const uint32_t acc = tm + (uint32_t)(s * 256);
+#pragma unroll
+        for (int st = 0; st < 2; ++st) {
+          const uint64_t b0 = desc_sw128(sA + 131072u + (uint32_t)st * 32768u);
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            mma_bf16_cg2(acc, a0 + (uint64_t)((st * 2 + (k >> 2)) * (16384 >> 4) + 2 * (k & 3)),
+                         b0 + (uint64_t)((k >> 2) * (16384 >> 4) + 2 * (k & 3)), id, (st | k) ? 1u : 0u);
+          mma_commit_cg2_mc(smem_u32(&bar[2]), 0x3);
+        }
+      } else if (cevery == 100) {
         // precomputed descriptors, fully unrolled (22 K-steps: 5 chunks of 4 + 2)
         const uint64_t a0 = desc_sw128(sA), b0 = desc_sw128(sB);
         const uint64_t bstep = (uint64_t)((N / 2) * 128 >> 4);
@@ -65,6 +82,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
     for (int s = 0; s < 2; ++s) { mbar_wait(smem_u32(&bar[(jobs + s) & 1]), ph[(jobs + s) & 1]); }
     out[blockIdx.x] = clock64() - t0;
     out[200 + blockIdx.x] = tissue;
+  } else if (ldtm == 3 && warp >= 1) {
+    // compute-bound competing warps (MUFU + FMA), like the epilogue
+    float x = 0.001f * threadIdx.x, y = 0.f;
+    for (int i = 0; i < jobs * 40; ++i) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) { x = __sinf(x * 1.0001f + 0.1f); y = fmaf(x, 0.5f, y); }
+    }
+    if (y == 0.12345f) out[1000] = 1;
   } else if (ldtm >= 2 && warp >= 1) {
     // concurrent shared-memory traffic from 15 warps (both CTAs): 2 = 16 B stores, 3 = 16 B loads
     const uint32_t reg = base + 6 * 16384 + 6 * 128 * 128 + (uint32_t)(warp * 512 + (threadIdx.x & 31) * 16);
@@ -102,15 +127,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
 int main() {
   unsigned long long* d;
   cudaMalloc(&d, 2000 * 8);
-  const int smem = 6 * 16384 + 6 * 128 * 128 + 1024 + 16 * 512;
+  const int smem = 196608 + 1024 + 16 * 512;
   cudaFuncSetAttribute(k_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int Ns[] = {128, 192, 256};
   struct Cfg { int N, ldtm, cevery, tcol; };
-  const Cfg cfgs[] = {{256, 0, 100, 0}, {256, 0, 100, 8}, {256, 0, 100, 9}, {192, 0, 100, 0}, {192, 0, 100, 8}};
+  const Cfg cfgs[] = {{256, 0, 200, 0}, {256, 3, 200, 0}, {256, 3, 0, 0}};
   for (int rep = 0; rep < 2; ++rep)
   for (const Cfg& c : cfgs) {
       const int N = c.N, ldtm = c.ldtm;
-      const int ks = 22, jobs = 2000;
+      const int ks = (c.cevery == 200 ? 16 : 22), jobs = 2000;
       cudaEvent_t e0, e1;
       cudaEventCreate(&e0); cudaEventCreate(&e1);
       cudaEventRecord(e0);
