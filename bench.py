@@ -237,6 +237,79 @@ def run_populate(args):
     return 0
 
 
+def run_sweep(args):
+    """octree max level 6..10 (C2's spheres, bands and score bump; Sec. 3.2 / Tab. 8 of the
+    paper sweeps the octree depth) and a paper-like far-field map (depth 0 = cached SDF, Eq. 7, for
+    every leaf farther than 0.04 from the surface: most of the grid) on C2's 512^3 grid with C2's 8x256 net.
+    Levels <= 8 are baked into a dense grid on load, 9-10 are descended on the device.  One JSON line with
+    one entry per map: points/s, per-stage ms, K1 achieved HBM GB/s (13 B/pt algorithmic; + 4 B/pt far SDF
+    for depth-0 points), depth histogram.  Single GPU."""
+    import torch
+    import sandgen as g
+    from sandgen import configs as gc
+    from paper_2604_25936_b200 import SAND_BF16, SandContext
+    ws, rank, local = _dist()
+    if rank != 0:
+        return 0
+    c = g.make_config("C2")
+    p = c.params()
+    sph = g.make_spheres(gc.SPHERE_SEED)
+    dev = torch.device("cuda", 0)
+    pts_np = g.grid_points(c.grid_R)
+    n = pts_np.shape[0]
+    pts = torch.from_numpy(pts_np).to(dev)
+    sdf = torch.empty(n, dtype=torch.float32, device=dev)
+    dep = torch.empty(n, dtype=torch.uint8, device=dev)
+    maps = [(f"octree level {lev}", lev, gc.BANDS_8, False) for lev in (6, 7, 8, 9, 10)]
+    maps.append(("far-field octree level 7 (|d| >= 0.04 -> depth 0)", 7, (0.005, 0.01, 0.02, 0.04), True))
+    entries = []
+    pk = _peaks()
+    with SandContext(c.spec.L, c.spec.H, c.spec.omega0, SAND_BF16, c.spec.tail, 0) as ctx:
+        ctx.sand_load_weights(g.pack_blob(p))
+        ctx.sand_reserve(n)
+        st = torch.cuda.current_stream(dev)
+        ctx.sand_set_stream(st.cuda_stream)
+        for name, lev, bands, far in maps:
+            oc = g.build_octree(sph, lev, bands, c.spec.L, score_seed=gc.SCORE_SEED, far_band=far)
+            ctx.sand_load_depthmap(oc)
+            for _ in range(args.warmup):
+                ctx.sand_query(pts.data_ptr(), n, sdf.data_ptr(), dep.data_ptr())
+            ctx.sand_get_stats()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize(dev)
+            e0.record(st)
+            for _ in range(args.steps):
+                ctx.sand_query(pts.data_ptr(), n, sdf.data_ptr(), dep.data_ptr())
+            e1.record(st)
+            torch.cuda.synchronize(dev)
+            ms = e0.elapsed_time(e1) / args.steps
+            s2 = ctx.sand_get_stats()
+            q = max(s2["queries"], 1)
+            pd = [int(v) for v in s2["per_depth"][:c.spec.L + 1]]   # last query's histogram
+            ms_lk = s2["ms_lookup_sum"] / q
+            k1_bytes = 13.0 * n + 4.0 * pd[0]
+            f_exec = sum(pd[d] * (d - 1) * 2.0 * c.spec.H ** 2 for d in range(1, c.spec.L + 1))
+            ms_mlp = s2["ms_mlp_sum"] / q
+            entries.append({"map": name, "max_level": lev, "n_nodes": int(oc.nodes.size),
+                            "n_leaves": int(oc.leaf_depth.size), "baked": lev <= 8,
+                            "value": n / (ms / 1e3), "unit": UNIT, "ms_per_step": ms,
+                            "stage_ms": {"lookup": ms_lk, "bin": s2["ms_bin_sum"] / q, "mlp": ms_mlp},
+                            "depth0_frac": pd[0] / n, "mean_depth": sum(d * pd[d] for d in range(len(pd))) / n,
+                            "k1_hbm_gbs": k1_bytes / (ms_lk / 1e3) / 1e9, "k1_hbm_frac": k1_bytes / (ms_lk / 1e3) / 1e9 / pk["hbm"],
+                            "k3_tensor_frac": (f_exec / (ms_mlp / 1e3) / 1e12 / pk["bf16"]) if ms_mlp > 0 else None,
+                            "per_depth": pd})
+            print(f"[sweep] {name}: {n / (ms / 1e3) / 1e9:.2f} G points/s, lookup {ms_lk:.3f} ms, "
+                  f"depth-0 {pd[0] / n:.3f}", file=sys.stderr, flush=True)
+    line = {"task": "sweep", "metric": "adaptive T-MLP SDF queries/sec vs octree max level and far-field share",
+            "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"C2 512^3 grid ({n} points), 8x256 SIREN T-MLP, C2 spheres",
+                       "hbm_peak_gbs": pk["hbm"], "bf16_peak_tflops": pk["bf16"]},
+            "entries": entries}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -251,7 +324,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-sample", type=int, default=1 << 15)
     ap.add_argument("--full-depth", action="store_true", help="all-L depth map (non-adaptive GPU baseline)")
-    ap.add_argument("--task", default="query", choices=["query", "populate"],
+    ap.add_argument("--task", default="query", choices=["query", "populate", "sweep"],
                     help="query: the adaptive SDF query path (BASELINE metric); populate: depth-map "
                          "population (Eq. 5/6, SURVEY 8(f) NEXT #1) on the config's finest octree leaves")
     args = ap.parse_args()
@@ -261,6 +334,8 @@ def main():
         return run_reference(args)
     if args.task == "populate":
         return run_populate(args)
+    if args.task == "sweep":
+        return run_sweep(args)
 
     import torch
     import torch.distributed as dist

@@ -147,8 +147,8 @@ def test_far_field_and_lod_caps(prec, H):
 
 
 def test_octree_descent_and_baked_paths():
-    """Octree level 9 (device descent, no baking) and level 6 (baked dense grid), far-field leaves
-    included; out-of-domain and face points."""
+    """Octree levels 9 and 10 (device descent, no baking) and level 6 (baked dense grid), far-field
+    leaves included; out-of-domain and face points."""
     L = 6
     spec = g.TMlpSpec(L=L, H=64, omega0=30.0, seed=9)
     p = g.make_weights(spec)
@@ -156,7 +156,7 @@ def test_octree_descent_and_baked_paths():
     rng = np.random.default_rng(0)
     pts = np.concatenate([rng.uniform(-1.2, 1.2, (20000, 3)),
                           -1 + rng.integers(0, 513, (2000, 3)) * (2.0 / 512)]).astype(np.float32)
-    for lev in (6, 9):
+    for lev in (6, 9, 10):
         oc = g.build_octree(sph, lev, g.configs.BANDS_8, L, score_seed=1, far_band=True,
                             subdivide_factor=0.3)
         with make_ctx(spec, BF16) as ctx:
