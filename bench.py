@@ -318,7 +318,7 @@ def main():
     ap.add_argument("--impl", default="sand", choices=["sand", "reference"])
     ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4"])
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--e2e-chunk", type=int, default=1 << 24)
+    ap.add_argument("--e2e-chunk", type=int, default=0, help="points per host-pipeline chunk (0: library default)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -440,7 +440,8 @@ def main():
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             t_e2e = float(tt.item())
         e2e = {"value": summ["n_total"] / t_e2e, "unit": UNIT, "h2d_bytes_per_step": 12 * summ["n_total"],
-               "d2h_bytes_per_step": 5 * summ["n_total"], "chunk_points": args.e2e_chunk,
+               "d2h_bytes_per_step": 5 * summ["n_total"],
+               "chunk_points": args.e2e_chunk or min(max(n // 8, 1 << 21), 1 << 23),
                "timing": "host wall clock around the synchronous sand_query_host, max over ranks"}
         ctx.sand_get_stats()
 

@@ -128,9 +128,11 @@ int sand_query(sand_ctx* ctx, const float* d_points, int64_t n,
                float* d_out_sdf, uint8_t* d_out_exit_depth);
 
 /* End-to-end variant with HOST buffers: copies points host->device, runs sand_query, copies the
- * results device->host, in chunks of at most chunk_points (0 = whole array) double-buffered over
- * two streams.  Host buffers should be pinned for full bandwidth.  Returns after the results are
- * in host memory (synchronous). */
+ * results device->host, in chunks of at most chunk_points double-buffered over two streams, so the
+ * copies of one chunk overlap the kernels of the next.  chunk_points = 0 lets the library choose:
+ * n / 8 clamped to [2^21, 2^23] points (measured on B200: the pipeline fill / drain of a large first
+ * and last chunk dominates otherwise; too small chunks under-fill the 148 SMs).  Host buffers should
+ * be pinned for full bandwidth.  Returns after the results are in host memory (synchronous). */
 int sand_query_host(sand_ctx* ctx, const float* h_points, int64_t n,
                     float* h_out_sdf, uint8_t* h_out_exit_depth, int64_t chunk_points);
 

@@ -593,7 +593,9 @@ extern "C" int sand_query_host(sand_ctx* ctx, const float* h_points, int64_t n, 
   if (n == 0) return SAND_OK;
   if (!h_points || !h_sdf || !h_depth) return fail(ctx, SAND_ERR_ARG, "NULL buffer");
   CU(cudaSetDevice(ctx->cfg.device));
-  long long chunk = chunk_points ? std::min<long long>(chunk_points, n) : n;
+  long long chunk = chunk_points;
+  if (chunk == 0) chunk = std::min<long long>(std::max<long long>(n / 8, 1ll << 21), 1ll << 23);   // sand.h
+  chunk = std::min<long long>(chunk, n);
   chunk = (chunk + 3) & ~3ll;
   int rc = ensure_hostpipe(ctx, chunk);
   if (rc) return rc;

@@ -227,9 +227,12 @@ def test_determinism_and_host_e2e():
         hp = torch.from_numpy(pts).pin_memory()
         hs = torch.empty(n, dtype=torch.float32).pin_memory()
         hd = torch.empty(n, dtype=torch.uint8).pin_memory()
-        ctx.sand_query_host(hp.data_ptr(), n, hs.data_ptr(), hd.data_ptr(), chunk_points=1 << 20)
-        np.testing.assert_array_equal(hs.numpy(), s1)
-        np.testing.assert_array_equal(hd.numpy(), d1)
+        for chunk in (1 << 20, 0, 12345):   # explicit, library default, ragged chunks
+            hs.zero_()
+            hd.zero_()
+            ctx.sand_query_host(hp.data_ptr(), n, hs.data_ptr(), hd.data_ptr(), chunk_points=chunk)
+            np.testing.assert_array_equal(hs.numpy(), s1)
+            np.testing.assert_array_equal(hd.numpy(), d1)
 
 
 def test_all_max_depth_equals_full_depth():
