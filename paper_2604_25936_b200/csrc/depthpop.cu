@@ -8,7 +8,7 @@
 // Eq. 5 compares cumulative outputs against r (1.5e-4 in the paper), far below the BF16 path's
 // error, so the full-depth evaluation here is FP32 (accurate sinf), whatever the context's precision.
 // k_required_depth: persistent blocks of 256 threads over tiles of 64 points; every layer is a register-
-// blocked FP32 GEMM (thread = 8 points x ceil(H/32) units, W^T staged in shared memory 16 rows at a
+// blocked FP32 GEMM (thread = 8 points x ceil(H/32) units, W^T double-buffered in shared memory by cp.async, 16 rows at a
 // time, activations transposed [unit][point] in shared memory) with the sine, tail and running y_i
 // fused; after layer L each point's d(x) is decided from its y_1..y_L.  k_leaf_max: Eq. 6 pooling.
 #include <cstdint>
@@ -19,16 +19,29 @@
 namespace sand {
 
 constexpr int kDpP = 64;          // points per tile
-constexpr int kDpThreads = 256;   // 8 point groups x 32 unit lanes
+constexpr int kDpS = 68;          // row stride of the [unit][point] activations: 16-byte rows, 4-way (not
+                                  // 32-way) bank conflicts when the 32 lanes of a warp touch 32 units
+constexpr int kDpThreads = 256;   // 8 point groups (warps) x 32 unit lanes (512 measured slower: more loads per FMA)
+constexpr int kDpPPW = kDpP / (kDpThreads / 32);   // points per warp
 constexpr int kDpKC = 16;         // W^T rows staged per step
 
 template <int H>
 struct DpShape {
   static constexpr int U = (H + 31) / 32;                    // units per thread
   static constexpr int HP = U * 32;                          // padded unit count
-  static constexpr size_t SMEM = (size_t)2 * HP * kDpP * 4   // h ping-pong, [unit][point]
-                                 + (size_t)kDpKC * HP * 4;   // W^T stage
+  static constexpr int KC = H > 256 ? kDpKC / 2 : kDpKC;     // W^T rows per stage (H = 336: fit 227 KB)
+  static constexpr size_t SMEM = (size_t)2 * HP * kDpS * 4   // h ping-pong, [unit][point]
+                                 + (size_t)2 * KC * HP * 4;  // W^T stages, double-buffered
 };
+
+// 16-byte global -> shared async copy (no register staging), completion by commit / wait groups
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 template <int H, int TAIL>
 __global__ void __launch_bounds__(kDpThreads, 1) k_required_depth(MlpDev m, const float* __restrict__ w_t,
@@ -36,9 +49,9 @@ __global__ void __launch_bounds__(kDpThreads, 1) k_required_depth(MlpDev m, cons
                                                                   float r, int near, uint8_t* __restrict__ out) {
   using C = DpShape<H>;
   extern __shared__ __align__(16) float sm[];
-  float* hA = sm;                               // [HP][kDpP]
-  float* hB = hA + C::HP * kDpP;
-  float* ws = hB + C::HP * kDpP;                // [kDpKC][HP]
+  float* hA = sm;                               // [HP][kDpS]
+  float* hB = hA + C::HP * kDpS;
+  float* ws = hB + C::HP * kDpS;                // [2][C::KC][HP] (columns >= H stay zero)
   __shared__ float ys[32][kDpP];                // y_i per point (L <= 32)
   __shared__ float px[3][kDpP];
   const int L = m.L;
@@ -51,6 +64,17 @@ __global__ void __launch_bounds__(kDpThreads, 1) k_required_depth(MlpDev m, cons
   const float* c_t = m.tables + m.off_c;         // [L]
   const float* c1_t = m.tables + m.off_c1;       // [L-1] (MULT)
   const long long ntiles = (n + kDpP - 1) / kDpP;
+  for (int i = tid; i < 2 * C::KC * C::HP; i += kDpThreads) ws[i] = 0.f;
+  __syncthreads();
+  // W^T rows [k0, k0 + C::KC) of layer matrix W -> stage buffer b (H % 16 == 0: rows are whole float4s)
+  auto stage = [&](const float* W, int k0, int b) {
+    constexpr int RV = H / 4;   // float4 per row
+    for (int i = tid; i < C::KC * RV; i += kDpThreads) {
+      const int kk = i / RV, j4 = i % RV;
+      cp_async16(ws + (b * C::KC + kk) * C::HP + 4 * j4, W + (size_t)(k0 + kk) * H + 4 * j4);
+    }
+    cp_async_commit();
+  };
   for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const long long p0 = tile * kDpP;
     for (int i = tid; i < 3 * kDpP; i += kDpThreads) {
@@ -66,16 +90,16 @@ __global__ void __launch_bounds__(kDpThreads, 1) k_required_depth(MlpDev m, cons
         const float4 w = w1[j];
         h = sinf(fmaf(w.z, px[2][p], fmaf(w.y, px[1][p], fmaf(w.x, px[0][p], w.w))));
       }
-      hA[j * kDpP + p] = h;
+      hA[j * kDpS + p] = h;
     }
     __syncthreads();
     auto tails = [&](int l, const float* hcur) {
-      // t_l per point: warp tp reduces its 8 points over all H units (lane = unit residue)
-      for (int pp = 0; pp < 8; ++pp) {
-        const int p = tp * 8 + pp;
+      // t_l per point: warp tp reduces its kDpPPW points over all H units (lane = unit residue)
+      for (int pp = 0; pp < kDpPPW; ++pp) {
+        const int p = tp * kDpPPW + pp;
         float s0 = 0.f, s1 = 0.f;
         for (int j = tj; j < H; j += 32) {
-          const float h = hcur[j * kDpP + p];
+          const float h = hcur[j * kDpS + p];
           s0 = fmaf(a_t[(l - 1) * H + j], h, s0);
           if (TAIL == SAND_TAIL_MULT && l >= 2) s1 = fmaf(a1_t[(l - 2) * H + j], h, s1);
         }
@@ -97,37 +121,47 @@ __global__ void __launch_bounds__(kDpThreads, 1) k_required_depth(MlpDev m, cons
     float* hout = hB;
     for (int l = 2; l <= L; ++l) {
       const float* W = w_t + (size_t)(l - 2) * H * H;   // W^T [k][j]
-      float acc[8][C::U];
+      float acc[kDpPPW][C::U];
 #pragma unroll
-      for (int a = 0; a < 8; ++a)
+      for (int a = 0; a < kDpPPW; ++a)
 #pragma unroll
         for (int u = 0; u < C::U; ++u) acc[a][u] = 0.f;
-      for (int k0 = 0; k0 < H; k0 += kDpKC) {
-        __syncthreads();
-        for (int i = tid; i < kDpKC * C::HP; i += kDpThreads) {
-          const int kk = i / C::HP, j = i % C::HP;
-          ws[i] = (k0 + kk < H && j < H) ? W[(size_t)(k0 + kk) * H + j] : 0.f;
+      // W^T streamed through two shared-memory stages: the copy of rows k0 + 16 .. overlaps the FMAs on
+      // rows k0 .. (cp.async, no register staging)
+      __syncthreads();   // previous users of both stage buffers are done
+      stage(W, 0, 0);
+      for (int k0 = 0, b = 0; k0 < H; k0 += C::KC, b ^= 1) {
+        if (k0 + C::KC < H) {
+          stage(W, k0 + C::KC, b ^ 1);
+          cp_async_wait<1>();
+        } else {
+          cp_async_wait<0>();
         }
         __syncthreads();
+        const float* wsb = ws + b * C::KC * C::HP;
 #pragma unroll 4
-        for (int kk = 0; kk < kDpKC && k0 + kk < H; ++kk) {
-          const float4 h0 = *reinterpret_cast<const float4*>(hin + (k0 + kk) * kDpP + tp * 8);
-          const float4 h1 = *reinterpret_cast<const float4*>(hin + (k0 + kk) * kDpP + tp * 8 + 4);
-          const float hv[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+        for (int kk = 0; kk < C::KC; ++kk) {
+          float hv[kDpPPW];
+#pragma unroll
+          for (int q4 = 0; q4 < kDpPPW / 4; ++q4) {
+            const float4 hq = *reinterpret_cast<const float4*>(hin + (k0 + kk) * kDpS + tp * kDpPPW + 4 * q4);
+            hv[4 * q4] = hq.x; hv[4 * q4 + 1] = hq.y; hv[4 * q4 + 2] = hq.z; hv[4 * q4 + 3] = hq.w;
+          }
 #pragma unroll
           for (int u = 0; u < C::U; ++u) {
-            const float w = ws[kk * C::HP + tj + 32 * u];
+            const float w = wsb[kk * C::HP + tj + 32 * u];
 #pragma unroll
-            for (int a = 0; a < 8; ++a) acc[a][u] = fmaf(w, hv[a], acc[a][u]);
+            for (int a = 0; a < kDpPPW; ++a) acc[a][u] = fmaf(w, hv[a], acc[a][u]);
           }
         }
+        __syncthreads();   // stage b is overwritten by the copy issued next iteration
       }
 #pragma unroll
       for (int u = 0; u < C::U; ++u) {
         const int j = tj + 32 * u;
         const float b = j < H ? bias_t[(l - 2) * H + j] : 0.f;
 #pragma unroll
-        for (int a = 0; a < 8; ++a) hout[j * kDpP + tp * 8 + a] = j < H ? sinf(fmaf(acc[a][u], w0, b)) : 0.f;
+        for (int a = 0; a < kDpPPW; ++a) hout[j * kDpS + tp * kDpPPW + a] = j < H ? sinf(fmaf(acc[a][u], w0, b)) : 0.f;
       }
       __syncthreads();
       tails(l, hout);
