@@ -37,6 +37,10 @@
 #include <cuda_runtime.h>
 
 #include "ptx.cuh"
+
+#ifndef SAND_DIAG
+#define SAND_DIAG 0   // 1: diagnostic modes SAND_KPROF=2/3 (timing studies; build with SAND_BUILD_DEFS=-DSAND_DIAG=1)
+#endif
 #include "sand_internal.h"
 
 #ifndef SAND_ABL
@@ -279,7 +283,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
         }
         if (warp == 0) {
           const uint8_t* src = img + (size_t)(l - 2) * 2 * C::KC * C::WH_CHUNK;
-          for (int j = 0; j < C::NSJ && p.prof != 3; ++j) {
+          for (int j = 0; j < C::NSJ && !(SAND_DIAG && p.prof == 3); ++j) {
             const long long c0_ = p.prof ? clock64() : 0;
             mbar_wait_lazy(b_wempty + 8 * st, ph ^ 1u);
             if (p.prof) { pc[4] += clock64() - c0_; pc[5] += 1; }
@@ -298,7 +302,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
 #pragma unroll
           for (int j = 0; j < C::NSJ; ++j) {
             c0_ = p.prof ? clock64() : 0;
-            if (p.prof != 3) { mbar_wait(b_wfull + 8 * st, ph);
+            if (!(SAND_DIAG && p.prof == 3)) { mbar_wait(b_wfull + 8 * st, ph);
             mbar_wait_cluster(b_wpeer + 8 * st, ph); }   // diagnostic 3: no weight streaming
             if (p.prof) pc[1] += clock64() - c0_;
             tc_fence_after();
@@ -314,7 +318,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
           }
           mma_commit_cg2_mc_w(b_accfull + 8 * s, 0x3);
         } else {
-          for (int j = 0; j < C::NSJ && p.prof != 3; ++j) {
+          for (int j = 0; j < C::NSJ && !(SAND_DIAG && p.prof == 3); ++j) {
             mbar_wait(b_wfull + 8 * st, ph);
             if (lane == 0) mbar_arrive_remote(peer_wpeer + 8 * st);
             __syncwarp();
@@ -504,7 +508,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
       const float* a1 = ta1 + (l - 2) * H + c0 + 2 * tq;
       const bool prod = TAIL == SAND_TAIL_MULT && l >= 2;
       const uint32_t tm = tm_q + (uint32_t)(s * H);
-      if (p.prof < 2)   // diagnostic 2/3: no epilogue math
+      if (!(SAND_DIAG && p.prof >= 2))   // diagnostic 2/3 (SAND_DIAG builds): no epilogue math
 #pragma unroll
       for (int bb = 0; bb < C::HQ / BW; ++bb) {
         uint32_t r0[4 * CB], r1[4 * CB];   // lane block 0 (rows R0, R1) and block 1 (rows R2, R3)

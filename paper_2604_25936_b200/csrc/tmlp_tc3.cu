@@ -22,6 +22,10 @@
 #include <vector>
 
 #include "ptx.cuh"
+
+#ifndef SAND_DIAG
+#define SAND_DIAG 0   // 1: diagnostic modes SAND_KPROF=2/3 (timing studies; build with SAND_BUILD_DEFS=-DSAND_DIAG=1)
+#endif
 #include "sand_internal.h"
 
 namespace sand {
@@ -223,7 +227,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc3Shape<H>::THREADS
           const uint8_t* src = img + (size_t)(l - 2) * layer_bytes + (hf ? (size_t)C::KC * C::RA * 128 : 0);
           const uint32_t chunk = (uint32_t)rows * 128;
           if (warp == 0) {
-            for (int j = 0; j < C::NSJ && p.prof != 3; ++j) {
+            for (int j = 0; j < C::NSJ && !(SAND_DIAG && p.prof == 3); ++j) {
               const int nch = (2 * j + 1 < C::KC) ? 2 : 1;
               const long long t0_ = P3T();
               mbar_wait_lazy(b_wempty + 8 * st, ph ^ 1u);
@@ -245,7 +249,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc3Shape<H>::THREADS
 #pragma unroll
             for (int j = 0; j < C::NSJ; ++j) {
               t0_ = P3T();
-              if (p.prof != 3) {   // diagnostic 3: no weight streaming (stale ring contents)
+              if (!(SAND_DIAG && p.prof == 3)) {   // diagnostic 3: no weight streaming (stale ring contents)
                 mbar_wait(b_wfull + 8 * st, ph);
                 mbar_wait_cluster(b_wpeer + 8 * st, ph);
               }
@@ -278,7 +282,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc3Shape<H>::THREADS
             }
             mma_commit_cg2_mc(b_accfull + 8 * hf, 0x3);
           } else {
-            for (int j = 0; j < C::NSJ && p.prof != 3; ++j) {
+            for (int j = 0; j < C::NSJ && !(SAND_DIAG && p.prof == 3); ++j) {
               mbar_wait(b_wfull + 8 * st, ph);
               mbar_arrive_remote(peer_wpeer + 8 * st);
               if (++st == nst) { st = 0; ph ^= 1u; }
@@ -433,7 +437,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc3Shape<H>::THREADS
       };
 #pragma unroll
       for (int i0 = 0; i0 < NCH; i0 += 2) {
-        if (p.prof >= 2) break;   // diagnostic: MMA / weight-stream throughput without epilogue work
+        if (SAND_DIAG && p.prof >= 2) break;   // diagnostic (SAND_DIAG builds): no epilogue work
         uint32_t r0[8], r1[8];
         if (i0 + 1 < NCH) {
           tmem_ld_16x256b<2>(tm_q + c0 + 8 * i0, r0);
@@ -481,7 +485,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc3Shape<H>::THREADS
           }
         }
       }
-      if (store && wait_b && (NCH <= HOLD || p.prof >= 2)) release();   // (diagnostic modes skip the loop)
+      if (store && wait_b && (NCH <= HOLD || (SAND_DIAG && p.prof >= 2))) release();   // (diagnostic modes skip the loop)
 #pragma unroll
       for (int k = 0; k < 4; ++k) ylin[k] += yv[k].x + yv[k].y;
     };
