@@ -43,8 +43,20 @@ __device__ __forceinline__ LookupResult lookup_one(float x, float y, float z, co
     d = __ldg(lp.grid + lin);
     if (d == 0 && lp.grid_far) far = __ldg(lp.grid_far + lin);
   } else {
-    uint32_t node = 0, v = __ldg(lp.nodes);
-    for (int bit = lp.level - 1; !(v >> 31) && bit >= 0; --bit) {
+    uint32_t node = 0, v;
+    int bit = lp.level - 1;
+    if (lp.top) {
+      // resume the descent at level top_level from the dense start table (one L2-resident load
+      // replaces the top_level pointer-chasing steps; entries may already be leaves)
+      const int sh = lp.level - lp.top_level;
+      const uint64_t t = (uint64_t)(cx >> sh) + ((uint64_t)(cy >> sh) << lp.top_level) +
+                         ((uint64_t)(cz >> sh) << (2 * lp.top_level));
+      v = __ldg(lp.top + t);
+      bit = sh - 1;
+    } else {
+      v = __ldg(lp.nodes);
+    }
+    for (; !(v >> 31) && bit >= 0; --bit) {
       const uint32_t oct = ((cx >> bit) & 1u) | (((cy >> bit) & 1u) << 1) | (((cz >> bit) & 1u) << 2);
       node = v + oct;
       v = __ldg(lp.nodes + node);
@@ -313,6 +325,28 @@ __global__ void k_bake(const uint32_t* __restrict__ nodes, const uint8_t* __rest
     grid[lin] = leaf_depth[leaf];
     if (grid_far) grid_far[lin] = leaf_far ? leaf_far[leaf] : 0.0f;
   }
+}
+
+// Start table for deep octrees: top[cell] = node payload after descending top_level levels (or the
+// leaf payload met earlier) -- the same octant walk as the lookup's own descent.
+__global__ void k_bake_top(const uint32_t* __restrict__ nodes, int top_level, uint32_t* __restrict__ top) {
+  const long long G = 1ll << top_level;
+  for (long long lin = blockIdx.x * (long long)blockDim.x + threadIdx.x; lin < G * G * G;
+       lin += (long long)gridDim.x * blockDim.x) {
+    const uint32_t cx = (uint32_t)(lin & (G - 1)), cy = (uint32_t)((lin >> top_level) & (G - 1)),
+                   cz = (uint32_t)(lin >> (2 * top_level));
+    uint32_t v = nodes[0];
+    for (int bit = top_level - 1; !(v >> 31) && bit >= 0; --bit) {
+      const uint32_t oct = ((cx >> bit) & 1u) | (((cy >> bit) & 1u) << 1) | (((cz >> bit) & 1u) << 2);
+      v = nodes[v + oct];
+    }
+    top[lin] = v;
+  }
+}
+
+cudaError_t launch_bake_top(const uint32_t* nodes, int top_level, uint32_t* top, cudaStream_t st) {
+  k_bake_top<<<148 * 8, 256, 0, st>>>(nodes, top_level, top);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_lookup(const float* pts, long long n, const LookupParams& lp, uint8_t* out_depth,

@@ -46,6 +46,7 @@ struct sand_ctx {
   LookupParams lp{};
   uint8_t* d_grid = nullptr;
   float* d_grid_far = nullptr;
+  uint32_t* d_top = nullptr;   // octree start table (levels > 8)
   uint32_t* d_nodes = nullptr;
   uint8_t* d_leaf_depth = nullptr;
   float* d_leaf_far = nullptr;
@@ -156,7 +157,7 @@ static void free_workspace(sand_ctx* c) {
   c->cap_n = c->cap_nblk = 0;
 }
 static void free_depthmap(sand_ctx* c) {
-  dfree(c->d_grid); dfree(c->d_grid_far); dfree(c->d_nodes); dfree(c->d_leaf_depth); dfree(c->d_leaf_far);
+  dfree(c->d_grid); dfree(c->d_grid_far); dfree(c->d_top); dfree(c->d_nodes); dfree(c->d_leaf_depth); dfree(c->d_leaf_far);
   c->have_dm = false;
 }
 static void free_weights(sand_ctx* c) {
@@ -480,6 +481,13 @@ extern "C" int sand_load_depthmap(sand_ctx* ctx, const sand_depthmap* dm) {
       cudaFree(d_err);
       if (herr) return fail(ctx, SAND_ERR_DEPTHMAP, "octree bake failed (descent exceeded level)");
       lp.dense = 1;
+    } else {
+      // deeper octrees keep the descent, started from a dense table of the level-7 nodes (8 MB)
+      lp.top_level = 7;
+      CU(cudaMalloc(&ctx->d_top, sizeof(uint32_t) << (3 * lp.top_level)));
+      CU(launch_bake_top(ctx->d_nodes, lp.top_level, ctx->d_top, ctx->stream));
+      CU(cudaStreamSynchronize(ctx->stream));
+      lp.top = ctx->d_top;
     }
   } else {
     return fail(ctx, SAND_ERR_ARG, "depth map kind %d (0 = voxel, 1 = octree)", dm->kind);

@@ -35,6 +35,8 @@ struct LookupParams {
   const uint32_t* nodes;  // octree
   const uint8_t* leaf_depth;
   const float* leaf_far;
+  const uint32_t* top;    // octree descent: node payload reached at level top_level per 2^top_level cell
+  int top_level;          // (a dense 8 MB start table: the descent resumes below it), or nullptr / 0
 };
 
 // Host-side launchers (lookup.cu)
@@ -47,6 +49,7 @@ cudaError_t launch_scatter(const uint8_t* depth, long long n, int L, const uint3
                            long long nblk, cudaStream_t st);
 cudaError_t launch_bake_octree(const uint32_t* nodes, const uint8_t* leaf_depth, const float* leaf_far,
                                int level, uint8_t* grid, float* grid_far, int* err_flag, cudaStream_t st);
+cudaError_t launch_bake_top(const uint32_t* nodes, int top_level, uint32_t* top, cudaStream_t st);
 
 // T-MLP parameters as the kernels consume them (built by sand_load_weights).
 struct MlpDev {
