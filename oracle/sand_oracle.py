@@ -225,3 +225,45 @@ def populate_leaf_depths(params, samples, r):
     n, spl = s.shape[0], s.shape[1]
     d = required_depth(params, s.reshape(-1, 3), r, near=True).reshape(n, spl)
     return d.max(axis=1)
+
+
+# --------------------------------------------------------------------------------------------
+# Dynamic-exit inference without a depth map   (Sec. 5 ablation "Necessity of
+# the Octree Structure", "SAND w/o Octree", Tab. octree)
+# --------------------------------------------------------------------------------------------
+def query_dynamic(params, points, r):
+    """'SAND w/o Octree': no depth map; every point proceeds layer by layer and 'if the
+    absolute value of the predicted residual at the current layer falls below the error threshold r,
+    the computation is terminated; otherwise, it proceeds to the next layer until the maximum depth
+    is reached'.  The residual of layer i is t_i = y_i - y_{i-1} (Eq. 2); reading R23: the
+    test applies from i = 2 (t_1 = y_1 is the first prediction itself, not a residual), so
+      d(x) = min{ i >= 2 : |t_i(x)| < r }  (L if none; 1 if L = 1),   sdf = y_{d(x)}(x).
+    Layer i is evaluated only for the points still running.  Non-finite points -> (NaN, 255).
+    Returns (sdf float64 [n], exit depth u8 [n])."""
+    pts = np.asarray(points, np.float32)
+    n = pts.shape[0]
+    L = params.spec.L
+    fin = _finite_rows(pts)
+    sdf = np.zeros(n)
+    dep = np.full(n, L, np.int64)
+    act = np.nonzero(fin)[0]
+    h = np.asarray(pts[act], np.float64)
+    y = np.zeros(act.size)
+    for i in range(1, L + 1):
+        h = _layer(params, i, h)
+        t = _tail(params, i, h)
+        y = y + t
+        if i == L:
+            sdf[act] = y
+            break
+        if i >= 2:
+            stop = np.abs(t) < r
+            sdf[act[stop]] = y[stop]
+            dep[act[stop]] = i
+            keep = ~stop
+            act, h, y = act[keep], h[keep], y[keep]
+            if act.size == 0:
+                break
+    sdf[~fin] = np.nan
+    dep[~fin] = NONFINITE_DEPTH
+    return sdf, dep.astype(np.uint8)
