@@ -310,6 +310,78 @@ def run_sweep(args):
     return 0
 
 
+def run_dynamic(args):
+    """the paper's 'SAND w/o Octree' alternative -- dynamic exit on
+    |t_i| < r without a depth map -- on C2's 512^3 grid and 8x256 net, next to the octree path on the
+    same points.  Two thresholds: the paper's r = 1.5e-4 (with SIREN-init weights no residual is
+    that small, so every point runs to L) and the 30% quantile of |t_i| over a sample (exits spread over
+    the layers).  FP32 SIMT kernel (sand_query_dynamic), tile-level early exit.  Single GPU."""
+    import torch
+    import sandgen as g
+    from paper_2604_25936_b200 import SAND_BF16, SandContext
+    ws, rank, local = _dist()
+    if rank != 0:
+        return 0
+    steps = min(args.steps, 3)
+    c = g.make_config("C2")
+    p = c.params()
+    dev = torch.device("cuda", 0)
+    pts_np = g.grid_points(c.grid_R)
+    n = pts_np.shape[0]
+    pts = torch.from_numpy(pts_np).to(dev)
+    sdf = torch.empty(n, dtype=torch.float32, device=dev)
+    dep = torch.empty(n, dtype=torch.uint8, device=dev)
+    import oracle
+    samp = pts_np[np.random.default_rng(0).choice(n, 4096, replace=False)]
+    _, ts, _ = oracle.tmlp_trace(p, samp)
+    r30 = float(np.quantile(np.abs(ts[1:]), 0.3))
+    entries = []
+    with SandContext(c.spec.L, c.spec.H, c.spec.omega0, SAND_BF16, c.spec.tail, 0) as ctx:
+        ctx.sand_load_weights(g.pack_blob(p))
+        ctx.sand_load_depthmap(c.depthmap)
+        ctx.sand_reserve(n)
+        st = torch.cuda.current_stream(dev)
+        ctx.sand_set_stream(st.cuda_stream)
+
+        def timed(fn, k):
+            for _ in range(min(args.warmup, 3)):
+                fn()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize(dev)
+            e0.record(st)
+            for _ in range(k):
+                fn()
+            e1.record(st)
+            torch.cuda.synchronize(dev)
+            return e0.elapsed_time(e1) / k
+
+        ms_oct = timed(lambda: ctx.sand_query(pts.data_ptr(), n, sdf.data_ptr(), dep.data_ptr()), 5)
+        for name, r in (("paper r = 1.5e-4", 1.5e-4), (f"r = 30% quantile of |t_i| ({r30:.3e})", r30)):
+            ms = timed(lambda: ctx.sand_query_dynamic(pts.data_ptr(), n, r, sdf.data_ptr(), dep.data_ptr()), steps)
+            hist = np.bincount(dep.cpu().numpy(), minlength=c.spec.L + 1)[:c.spec.L + 1].tolist()
+            entries.append({"threshold": name, "r": r, "value": n / (ms / 1e3), "unit": UNIT, "ms_per_step": ms,
+                            "exit_depth_hist": hist,
+                            "mean_exit_depth": float(np.dot(np.arange(len(hist)), hist) / n)})
+            print(f"[dynamic] {name}: {n / (ms / 1e3) / 1e9:.3f} G points/s ({ms:.1f} ms)", file=sys.stderr, flush=True)
+    cpu = None
+    if not args.no_cpu:
+        k = 20000
+        t0 = time.perf_counter()
+        oracle.query_dynamic(p, pts_np[:k], r30)
+        dt = time.perf_counter() - t0
+        cpu = {"value": k / dt, "unit": UNIT, "cores": _cores(), "kind": "oracle",
+               "sample": f"first {k} grid points, r = {r30:.3e}"}
+    line = {"task": "dynamic", "metric": "dynamic-exit (no octree) SDF queries/sec vs the octree path",
+            "unit": UNIT, "n_gpus": 1, "steps": steps, "warmup": args.warmup, "higher_is_better": True,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"C2 512^3 grid ({n} points), 8x256 SIREN T-MLP (seeded init)"},
+            "octree_path": {"value": n / (ms_oct / 1e3), "unit": UNIT, "ms_per_step": ms_oct,
+                            "dtype": "bf16", "note": "sand_query with C2's level-7 octree, same points"},
+            "entries": entries, "cpu_baseline": cpu}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -324,7 +396,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-sample", type=int, default=1 << 15)
     ap.add_argument("--full-depth", action="store_true", help="all-L depth map (non-adaptive GPU baseline)")
-    ap.add_argument("--task", default="query", choices=["query", "populate", "sweep"],
+    ap.add_argument("--task", default="query", choices=["query", "populate", "sweep", "dynamic"],
                     help="query: the adaptive SDF query path (BASELINE metric); populate: depth-map "
                          "population (Eq. 5/6, SURVEY 8(f) NEXT #1) on the config's finest octree leaves")
     args = ap.parse_args()
@@ -336,6 +408,8 @@ def main():
         return run_populate(args)
     if args.task == "sweep":
         return run_sweep(args)
+    if args.task == "dynamic":
+        return run_dynamic(args)
 
     import torch
     import torch.distributed as dist

@@ -180,6 +180,19 @@ int sand_required_depth(sand_ctx* ctx, const float* d_points, int64_t n, float r
 int sand_populate_leaf_depths(sand_ctx* ctx, const float* d_samples, int64_t n_leaves, int samples_per_leaf,
                               float r, uint8_t* d_leaf_depth);
 
+/* ---------------------------------------------------------------------------------------------------
+ * Dynamic-exit query without a depth map: the paper's 'SAND w/o Octree' alternative (Sec. 5, P:736-738,
+ * Tab. octree).  Each point runs the T-MLP layer by layer and stops at the first
+ * layer i >= 2 whose residual |t_i| < r (reading R23: t_1 = y_1 is the first prediction, not
+ * a residual), else at L:
+ *   d_out_exit_depth[p] = that layer (255 for a non-finite point),  d_out_sdf[p] = y_d (NaN if 255).
+ * FP32 (accurate sine) like the population calls above; a 64-point tile stops as soon as all of its
+ * points have stopped (no re-compaction across tiles).  Only the weights must be loaded; the depth map
+ * and LOD cap are ignored.  Asynchronous on ctx's stream.  Errors: SAND_ERR_ARG (n < 0, r < 0 or NaN,
+ * NULL buffer), SAND_ERR_STATE, SAND_ERR_UNSUPPORTED (H as above), SAND_ERR_CUDA. */
+int sand_query_dynamic(sand_ctx* ctx, const float* d_points, int64_t n, float r, float* d_out_sdf,
+                       uint8_t* d_out_exit_depth);
+
 /* Message for the last error on ctx (or of the last failed sand_create if ctx is NULL).
  * Valid until the next call on ctx.  Never NULL. */
 const char* sand_last_error(const sand_ctx* ctx);

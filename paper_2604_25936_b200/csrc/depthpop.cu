@@ -43,10 +43,15 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <int H, int TAIL>
+// MODE 0: Eq. 5 required depth of every point (full-depth evaluation, decision after layer L).
+// MODE 1: dynamic exit without a depth map ('SAND w/o Octree'; R23): a point stops at
+//   the first layer i >= 2 with |t_i| < r (else L) and returns y_i; a tile stops computing as soon as all
+//   of its points have stopped (tile-level early exit; no re-compaction across tiles).
+template <int H, int TAIL, int MODE>
 __global__ void __launch_bounds__(kDpThreads, 1) k_required_depth(MlpDev m, const float* __restrict__ w_t,
                                                                   const float* __restrict__ pts, long long n,
-                                                                  float r, int near, uint8_t* __restrict__ out) {
+                                                                  float r, int near, uint8_t* __restrict__ out,
+                                                                  float* __restrict__ out_sdf) {
   using C = DpShape<H>;
   extern __shared__ __align__(16) float sm[];
   float* hA = sm;                               // [HP][kDpS]
@@ -54,6 +59,8 @@ __global__ void __launch_bounds__(kDpThreads, 1) k_required_depth(MlpDev m, cons
   float* ws = hB + C::HP * kDpS;                // [2][C::KC][HP] (columns >= H stay zero)
   __shared__ float ys[32][kDpP];                // y_i per point (L <= 32)
   __shared__ float px[3][kDpP];
+  __shared__ float tl[kDpP];                    // MODE 1: t_l of the current layer
+  __shared__ int xit[kDpP];                     // MODE 1: 0 running, l = stopped after layer l, 255 none
   const int L = m.L;
   const float w0 = m.omega0;
   const int tid = threadIdx.x, tj = tid & 31, tp = tid >> 5;   // warp = point group
@@ -82,6 +89,8 @@ __global__ void __launch_bounds__(kDpThreads, 1) k_required_depth(MlpDev m, cons
       px[c][p] = (p0 + p < n) ? pts[3 * (p0 + p) + c] : 0.f;
     }
     __syncthreads();
+    if (MODE == 1 && tid < kDpP)
+      xit[tid] = (p0 + tid < n && isfinite(px[0][tid]) && isfinite(px[1][tid]) && isfinite(px[2][tid])) ? 0 : 255;
     // ---- layer 1 (K = 3) + tail 1
     for (int i = tid; i < C::HP * kDpP; i += kDpThreads) {
       const int j = i / kDpP, p = i % kDpP;
@@ -112,6 +121,7 @@ __global__ void __launch_bounds__(kDpThreads, 1) k_required_depth(MlpDev m, cons
           float t = s0 + c_t[l - 1];
           if (TAIL == SAND_TAIL_MULT && l >= 2) t *= s1 + c1_t[l - 2];
           ys[l - 1][p] = (l == 1 ? 0.f : ys[l - 2][p]) + t;
+          if (MODE == 1) tl[p] = t;
         }
       }
     };
@@ -166,8 +176,27 @@ __global__ void __launch_bounds__(kDpThreads, 1) k_required_depth(MlpDev m, cons
       __syncthreads();
       tails(l, hout);
       float* t = hin; hin = hout; hout = t;
+      if (MODE == 1 && l < L) {
+        __syncthreads();
+        int run = 0;
+        if (tid < kDpP) {
+          if (xit[tid] == 0 && fabsf(tl[tid]) < r) xit[tid] = l;
+          run = xit[tid] == 0;
+        }
+        if (!__syncthreads_or(run)) break;   // every point of the tile has stopped
+      }
     }
     __syncthreads();
+    if (MODE == 1) {
+      if (tid < kDpP && p0 + tid < n) {
+        const int x = xit[tid];
+        const int d = x == 0 ? L : x;
+        out[p0 + tid] = (uint8_t)d;
+        out_sdf[p0 + tid] = d == 255 ? __int_as_float(0x7fc00000) : ys[d - 1][tid];
+      }
+      __syncthreads();
+      continue;
+    }
     // ---- Eq. 5 decision per point
     if (tid < kDpP && p0 + tid < n) {
       const float yL = ys[L - 1][tid];
@@ -192,16 +221,16 @@ __global__ void k_leaf_max(const uint8_t* __restrict__ d, long long n_leaves, in
   out[leaf] = (uint8_t)mx;
 }
 
-template <int H, int TAIL>
+template <int H, int TAIL, int MODE>
 static cudaError_t launch_rd_t(const MlpDev& m, const float* w_t, const float* pts, long long n, float r, int near,
-                               uint8_t* out, int num_sms, cudaStream_t st) {
+                               uint8_t* out, float* out_sdf, int num_sms, cudaStream_t st) {
   const size_t sm = DpShape<H>::SMEM;
-  cudaError_t e = cudaFuncSetAttribute(k_required_depth<H, TAIL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)sm);
+  cudaError_t e = cudaFuncSetAttribute(k_required_depth<H, TAIL, MODE>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
   const long long ntiles = (n + kDpP - 1) / kDpP;
   const int grid = (int)(ntiles < num_sms ? ntiles : num_sms);
-  k_required_depth<H, TAIL><<<grid, kDpThreads, sm, st>>>(m, w_t, pts, n, r, near, out);
+  k_required_depth<H, TAIL, MODE><<<grid, kDpThreads, sm, st>>>(m, w_t, pts, n, r, near, out, out_sdf);
   return cudaGetLastError();
 }
 
@@ -209,14 +238,17 @@ bool depthpop_supported(int H) {
   return H == 16 || H == 32 || H == 64 || H == 128 || H == 256 || H == 336;
 }
 
-cudaError_t launch_required_depth(const MlpDev& m, const float* w_t, const float* pts, long long n, float r,
-                                  int near, uint8_t* out, int num_sms, cudaStream_t st) {
+static cudaError_t launch_dp(const MlpDev& m, const float* w_t, const float* pts, long long n, float r, int near,
+                             uint8_t* out, float* out_sdf, int mode, int num_sms, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   const bool mult = m.tail == SAND_TAIL_MULT;
-#define SAND_DP_CASE(HH)                                                                          \
-  case HH:                                                                                        \
-    return mult ? launch_rd_t<HH, 1>(m, w_t, pts, n, r, near, out, num_sms, st)                   \
-                : launch_rd_t<HH, 0>(m, w_t, pts, n, r, near, out, num_sms, st);
+#define SAND_DP_CASE(HH)                                                                                   \
+  case HH:                                                                                                 \
+    if (mode == 1)                                                                                         \
+      return mult ? launch_rd_t<HH, 1, 1>(m, w_t, pts, n, r, near, out, out_sdf, num_sms, st)              \
+                  : launch_rd_t<HH, 0, 1>(m, w_t, pts, n, r, near, out, out_sdf, num_sms, st);             \
+    return mult ? launch_rd_t<HH, 1, 0>(m, w_t, pts, n, r, near, out, out_sdf, num_sms, st)                \
+                : launch_rd_t<HH, 0, 0>(m, w_t, pts, n, r, near, out, out_sdf, num_sms, st);
   switch (m.H) {
     SAND_DP_CASE(16)
     SAND_DP_CASE(32)
@@ -227,6 +259,16 @@ cudaError_t launch_required_depth(const MlpDev& m, const float* w_t, const float
     default: return cudaErrorInvalidValue;
   }
 #undef SAND_DP_CASE
+}
+
+cudaError_t launch_required_depth(const MlpDev& m, const float* w_t, const float* pts, long long n, float r,
+                                  int near, uint8_t* out, int num_sms, cudaStream_t st) {
+  return launch_dp(m, w_t, pts, n, r, near, out, nullptr, 0, num_sms, st);
+}
+
+cudaError_t launch_query_dynamic(const MlpDev& m, const float* w_t, const float* pts, long long n, float r,
+                                 float* out_sdf, uint8_t* out_depth, int num_sms, cudaStream_t st) {
+  return launch_dp(m, w_t, pts, n, r, 1, out_depth, out_sdf, 1, num_sms, st);
 }
 
 cudaError_t launch_leaf_max(const uint8_t* d, long long n_leaves, int spl, uint8_t* out, cudaStream_t st) {

@@ -712,6 +712,20 @@ extern "C" int sand_required_depth(sand_ctx* ctx, const float* d_points, int64_t
   return SAND_OK;
 }
 
+extern "C" int sand_query_dynamic(sand_ctx* ctx, const float* d_points, int64_t n, float r, float* d_out_sdf,
+                                  uint8_t* d_out_exit_depth) {
+  if (!ctx) return fail(ctx, SAND_ERR_ARG, "NULL ctx");
+  if (n < 0 || !(r >= 0.0f)) return fail(ctx, SAND_ERR_ARG, "sand_query_dynamic: n < 0 or r < 0");
+  if (!ctx->have_w) return fail(ctx, SAND_ERR_STATE, "load weights before sand_query_dynamic");
+  if (n == 0) return SAND_OK;
+  if (!d_points || !d_out_sdf || !d_out_exit_depth) return fail(ctx, SAND_ERR_ARG, "NULL buffer");
+  if (!depthpop_supported(ctx->cfg.H)) return fail(ctx, SAND_ERR_UNSUPPORTED, "H = %d", ctx->cfg.H);
+  CU(cudaSetDevice(ctx->cfg.device));
+  CU(launch_query_dynamic(ctx->mlp, ctx->d_wt_f32, d_points, n, r, d_out_sdf, d_out_exit_depth, ctx->num_sms,
+                          ctx->stream));
+  return SAND_OK;
+}
+
 extern "C" int sand_populate_leaf_depths(sand_ctx* ctx, const float* d_samples, int64_t n_leaves,
                                          int samples_per_leaf, float r, uint8_t* d_leaf_depth) {
   if (!ctx) return fail(ctx, SAND_ERR_ARG, "NULL ctx");

@@ -97,6 +97,8 @@ size_t simt_smem_bytes(int L, int H, int tail);
 cudaError_t prepare_tmlp_kernels(int L, int H, int tail, int prec);
 // depth-map population (depthpop.cu)
 bool depthpop_supported(int H);
+cudaError_t launch_query_dynamic(const MlpDev& m, const float* w_t, const float* pts, long long n, float r,
+                                 float* out_sdf, uint8_t* out_depth, int num_sms, cudaStream_t st);
 cudaError_t launch_required_depth(const MlpDev& m, const float* w_t, const float* pts, long long n, float r,
                                   int near, uint8_t* out, int num_sms, cudaStream_t st);
 cudaError_t launch_leaf_max(const uint8_t* d, long long n_leaves, int spl, uint8_t* out, cudaStream_t st);

@@ -51,7 +51,7 @@ class sand_stats(ctypes.Structure):
 EXPORTS = ("sand_create", "sand_destroy", "sand_load_weights", "sand_load_depthmap", "sand_set_stream",
            "sand_set_lod_cap", "sand_reserve", "sand_query", "sand_query_host", "sand_get_stats",
            "sand_debug_perm", "sand_last_error", "sand_abi_version", "sand_required_depth",
-           "sand_populate_leaf_depths")
+           "sand_populate_leaf_depths", "sand_query_dynamic")
 
 _lib = None
 
@@ -82,6 +82,7 @@ def load_library(path=None):
     lib.sand_abi_version.argtypes = []
     lib.sand_required_depth.argtypes = [vp, vp, i64, ctypes.c_float, ctypes.c_int, vp]
     lib.sand_populate_leaf_depths.argtypes = [vp, vp, i64, ctypes.c_int, ctypes.c_float, vp]
+    lib.sand_query_dynamic.argtypes = [vp, vp, i64, ctypes.c_float, vp, vp]
     for f in EXPORTS:
         if f not in ("sand_last_error",):
             getattr(lib, f).restype = ctypes.c_int
@@ -192,6 +193,11 @@ class SandContext:
     def sand_populate_leaf_depths(self, d_samples, n_leaves, samples_per_leaf, r, d_leaf_depth):
         self._chk(self.lib.sand_populate_leaf_depths(self.h, ctypes.c_void_p(d_samples), int(n_leaves),
                                                      int(samples_per_leaf), float(r), ctypes.c_void_p(d_leaf_depth)))
+
+    # -- dynamic exit without a depth map ('SAND w/o Octree') ----------------------------------
+    def sand_query_dynamic(self, d_points, n, r, d_out_sdf, d_out_exit_depth):
+        self._chk(self.lib.sand_query_dynamic(self.h, ctypes.c_void_p(d_points), int(n), float(r),
+                                              ctypes.c_void_p(d_out_sdf), ctypes.c_void_p(d_out_exit_depth)))
 
     # -- torch convenience (device tensors in, device tensors out) -----------------------------------
     def query_tensor(self, pts, sdf=None, depth=None):
