@@ -17,11 +17,11 @@ Parity unpinned: nothing in this module.
 from .sand_oracle import (
     cell_coords, lookup_voxel, lookup_octree, lookup_bruteforce, lookup,
     tmlp_forward, tmlp_trace, query, query_full, NONFINITE_DEPTH, required_depth, populate_leaf_depths,
-    query_dynamic,
+    query_dynamic, marching_cubes, mc_loops,
 )
 
 __all__ = [
     "cell_coords", "lookup_voxel", "lookup_octree", "lookup_bruteforce", "lookup",
     "tmlp_forward", "tmlp_trace", "query", "query_full", "NONFINITE_DEPTH", "required_depth",
-    "populate_leaf_depths", "query_dynamic",
+    "populate_leaf_depths", "query_dynamic", "marching_cubes", "mc_loops",
 ]

@@ -267,3 +267,91 @@ def query_dynamic(params, points, r):
     sdf[~fin] = np.nan
     dep[~fin] = NONFINITE_DEPTH
     return sdf, dep.astype(np.uint8)
+
+
+# --------------------------------------------------------------------------------------------
+# Marching cubes on the query grid   (meshes are extracted from the SDF on a
+# 512^3 grid with Marching Cubes [Lorensen and Cline])
+# --------------------------------------------------------------------------------------------
+# DESIGN.md reading R24.  The per-configuration triangulation is derived here from the cube itself
+# (no stored table): a corner is inside iff sdf < 0; on each of the 6 faces, walked counter-clockwise
+# as seen from outside the cube, every crossing edge entered from an outside corner starts a segment
+# that ends at the next crossing edge of the walk, so a face with two diagonal inside corners keeps
+# them separated (a rule that depends on the face's own corners only, hence watertight across
+# cubes).  Every crossing edge starts one segment and ends one, the segments chain into closed loops,
+# and each loop of k edge points becomes a fan of k - 2 triangles.
+def _mc_edges():
+    """Cube corners v = x + 2y + 4z; the 12 edges as (v0, v1), v1 = v0 + 2^axis, axis-major."""
+    return [(v, v | (1 << a)) for a in range(3) for v in range(8) if not (v >> a) & 1]
+
+
+def _mc_faces():
+    """6 faces as corner cycles, counter-clockwise seen from outside the cube."""
+    faces = []
+    for a in range(3):
+        u, w = (a + 1) % 3, (a + 2) % 3                  # e_u x e_w = e_a
+        for side in (0, 1):
+            cyc = [(0, 0), (1, 0), (1, 1), (0, 1)]       # CCW about +e_a
+            if side == 0:
+                cyc = cyc[::-1]                          # CCW about -e_a
+            faces.append([(side << a) | (cu << u) | (cw << w) for cu, cw in cyc])
+    return faces
+
+
+def mc_loops(case):
+    """Closed loops (lists of edge ids) of the iso-surface inside one cube; bit v of case = corner v
+    inside."""
+    edges = _mc_edges()
+    eid = {frozenset(e): i for i, e in enumerate(edges)}
+    inside = [(case >> v) & 1 for v in range(8)]
+    nxt = {}
+    for cyc in _mc_faces():
+        cross = []                                       # (edge, entering?) in walk order
+        for k in range(4):
+            p, q = cyc[k], cyc[(k + 1) % 4]
+            if inside[p] != inside[q]:
+                cross.append((eid[frozenset((p, q))], inside[q] == 1))
+        for k, (e, entering) in enumerate(cross):
+            if entering:
+                nxt[e] = cross[(k + 1) % len(cross)][0]
+    loops, seen = [], set()
+    for e0 in sorted(nxt):
+        if e0 in seen:
+            continue
+        loop, e = [], e0
+        while e not in seen:
+            seen.add(e)
+            loop.append(e)
+            e = nxt[e]
+        loops.append(loop)
+    return loops
+
+
+def marching_cubes(sdf, R):
+    """Triangles of the sdf = 0 surface of an R x R x R vertex grid (sdf[i + R (j + R k)], vertex
+    (i, j, k) at (x_i, x_j, x_k), x_i = fl32(2 i / (R - 1) - 1), reading R8).  A vertex on a crossing
+    edge (v0, v1) lies at P0 + t (P1 - P0), t = s0 / (s0 - s1), computed from the edge's lower corner
+    (so both cubes sharing the edge produce the same point).  Float64.  Returns [T, 3, 3]."""
+    s = np.asarray(sdf, np.float64).reshape(R, R, R)     # [k][j][i]
+    ax = (2.0 * np.arange(R) / (R - 1) - 1.0).astype(np.float32).astype(np.float64)
+    edges = _mc_edges()
+    tris = []
+    for k in range(R - 1):
+        for j in range(R - 1):
+            for i in range(R - 1):
+                vals = [s[k + (v >> 2), j + ((v >> 1) & 1), i + (v & 1)] for v in range(8)]
+                case = sum(1 << v for v in range(8) if vals[v] < 0)
+                if case == 0 or case == 255:
+                    continue
+                def point(e):
+                    v0, v1 = edges[e]
+                    s0, s1 = vals[v0], vals[v1]
+                    t = s0 / (s0 - s1)
+                    p0 = np.array([ax[i + (v0 & 1)], ax[j + ((v0 >> 1) & 1)], ax[k + (v0 >> 2)]])
+                    p1 = np.array([ax[i + (v1 & 1)], ax[j + ((v1 >> 1) & 1)], ax[k + (v1 >> 2)]])
+                    return p0 + t * (p1 - p0)
+                for loop in mc_loops(case):
+                    pts = [point(e) for e in loop]
+                    for m in range(1, len(pts) - 1):
+                        tris.append([pts[0], pts[m], pts[m + 1]])
+    return np.array(tris).reshape(-1, 3, 3)
