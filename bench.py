@@ -382,6 +382,68 @@ def run_dynamic(args):
     return 0
 
 
+def run_mesh(args):
+    """marching cubes on C2's 512^3 grid (the paper's mesh extraction, P:415, P:423;
+    triangulation rule DESIGN.md R24).  (a) fused: sand_mesh_grid -- the query path slab by slab (32
+    planes of cubes) with each slab meshed as soon as its sdf exists, the 512^3 sdf never materialised;
+    (b) unfused: sand_query over the whole grid, then sand_marching_cubes on the 537 MB sdf grid.  The MC
+    kernel alone is timed in (b) (HBM-bound: 4 B of sdf per cube + 36 B per triangle).  Single GPU."""
+    import torch
+    import sandgen as g
+    from paper_2604_25936_b200 import SAND_BF16, SandContext
+    ws, rank, local = _dist()
+    if rank != 0:
+        return 0
+    steps = min(args.steps, 5)
+    c = g.make_config("C2")
+    p = c.params()
+    R = c.grid_R
+    dev = torch.device("cuda", 0)
+    n = R ** 3
+    pk = _peaks()
+    with SandContext(c.spec.L, c.spec.H, c.spec.omega0, SAND_BF16, c.spec.tail, 0) as ctx:
+        ctx.sand_load_weights(g.pack_blob(p))
+        ctx.sand_load_depthmap(c.depthmap)
+        st = torch.cuda.current_stream(dev)
+        ctx.sand_set_stream(st.cuda_stream)
+        ntri = ctx.sand_mesh_grid(R, 32, 0, 0)
+        tris = torch.empty(9 * ntri, dtype=torch.float32, device=dev)
+
+        def timed(fn, k):
+            for _ in range(min(args.warmup, 3)):
+                fn()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize(dev)
+            e0.record(st)
+            for _ in range(k):
+                fn()
+            e1.record(st)
+            torch.cuda.synchronize(dev)
+            return e0.elapsed_time(e1) / k
+
+        ms_fused = timed(lambda: ctx.sand_mesh_grid(R, 32, tris.data_ptr(), ntri), steps)
+        pts = torch.from_numpy(g.grid_points(R)).to(dev)
+        sdf = torch.empty(n, dtype=torch.float32, device=dev)
+        dep = torch.empty(n, dtype=torch.uint8, device=dev)
+        ctx.sand_reserve(n)
+        ms_query = timed(lambda: ctx.sand_query(pts.data_ptr(), n, sdf.data_ptr(), dep.data_ptr()), steps)
+        ms_mc = timed(lambda: ctx.sand_marching_cubes(sdf.data_ptr(), R, tris.data_ptr(), ntri), steps)
+        n2 = ctx.sand_marching_cubes(sdf.data_ptr(), R, tris.data_ptr(), ntri)
+    mc_bytes = 4.0 * n + 36.0 * ntri
+    line = {"task": "mesh", "metric": "marching-cubes mesh extraction of the 512^3 SDF grid (fused with the query path)",
+            "value": n / (ms_fused / 1e3), "unit": UNIT, "n_gpus": 1, "steps": steps, "warmup": args.warmup,
+            "ms_per_step": ms_fused, "higher_is_better": True, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"C2 {R}^3 grid, 8x256 SIREN T-MLP, level-7 octree, slabs of 32 cube planes"},
+            "triangles": ntri, "triangles_unfused": n2,
+            "unfused": {"ms_query": ms_query, "ms_marching_cubes": ms_mc, "ms_total": ms_query + ms_mc,
+                        "sdf_grid_bytes": 4 * n},
+            "roofline": {"bound": "hbm", "kernel": "k_marching_cubes (unfused call)", "achieved": mc_bytes / (ms_mc / 1e3) / 1e9,
+                         "peak": pk["hbm"], "unit": "GB/s", "frac": mc_bytes / (ms_mc / 1e3) / 1e9 / pk["hbm"],
+                         "bytes_formula": "4 B sdf per grid vertex + 36 B per triangle", "traffic": None}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -396,7 +458,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-sample", type=int, default=1 << 15)
     ap.add_argument("--full-depth", action="store_true", help="all-L depth map (non-adaptive GPU baseline)")
-    ap.add_argument("--task", default="query", choices=["query", "populate", "sweep", "dynamic"],
+    ap.add_argument("--task", default="query", choices=["query", "populate", "sweep", "dynamic", "mesh"],
                     help="query: the adaptive SDF query path (BASELINE metric); populate: depth-map "
                          "population (Eq. 5/6, SURVEY 8(f) NEXT #1) on the config's finest octree leaves")
     args = ap.parse_args()
@@ -410,6 +472,8 @@ def main():
         return run_sweep(args)
     if args.task == "dynamic":
         return run_dynamic(args)
+    if args.task == "mesh":
+        return run_mesh(args)
 
     import torch
     import torch.distributed as dist

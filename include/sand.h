@@ -193,6 +193,26 @@ int sand_populate_leaf_depths(sand_ctx* ctx, const float* d_samples, int64_t n_l
 int sand_query_dynamic(sand_ctx* ctx, const float* d_points, int64_t n, float r, float* d_out_sdf,
                        uint8_t* d_out_exit_depth);
 
+/* ---------------------------------------------------------------------------------------------------
+ * Marching cubes on the R x R x R query grid (the paper's mesh extraction; SURVEY.md 8(f)
+ * NEXT #2; triangulation rule: DESIGN.md reading R24 -- a corner is inside iff sdf < 0, at most 5
+ * triangles per cube, normals toward sdf > 0, watertight).  Grid vertex (i, j, k) is at
+ * (x_i, x_j, x_k), x_i = fl32(2 i / (R - 1) - 1); its sdf is element i + R (j + R k).
+ * Output: triangle soup d_tris[9 t + 3 m + c] = coordinate c of vertex m of triangle t (float32,
+ * device, caller-owned, room for cap triangles).  *n_tris (host) receives the number of triangles of
+ * the surface; only the first min(n, cap) are written, so a call with cap = 0 sizes the buffer.  The
+ * order of triangles is not deterministic (the set is).  Synchronous (returns after the count is
+ * read back).  Errors: SAND_ERR_ARG, SAND_ERR_STATE, SAND_ERR_CUDA, SAND_ERR_OOM. */
+
+/* Marching cubes on a caller-provided sdf grid (R^3 float32, device). */
+int sand_marching_cubes(sand_ctx* ctx, const float* d_sdf, int R, float* d_tris, int64_t cap, int64_t* n_tris);
+
+/* Fused extraction: evaluates the adaptive query path (sand_query with the loaded weights, depth map and
+ * LOD cap) slab by slab -- slab planes of cubes at a time (0 = 32), slab + 1 grid planes of points
+ * generated on the device -- and meshes each slab as soon as its sdf exists, so the R^3 sdf grid is
+ * never materialised (R = 512: 35 MB of slab buffers instead of 537 MB). */
+int sand_mesh_grid(sand_ctx* ctx, int R, int slab, float* d_tris, int64_t cap, int64_t* n_tris);
+
 /* Message for the last error on ctx (or of the last failed sand_create if ctx is NULL).
  * Valid until the next call on ctx.  Never NULL. */
 const char* sand_last_error(const sand_ctx* ctx);

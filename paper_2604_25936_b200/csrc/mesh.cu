@@ -1,0 +1,227 @@
+// mesh.cu -- marching cubes on the query grid, standalone or fused slab by slab with the query path
+// (meshes are extracted from the SDF on a 512^3 grid with
+// Marching Cubes; reading R24 for the triangulation rule, which the paper does not give).
+//
+// Configuration tables are derived at load time from the cube geometry (mc_build_tables), not stored:
+// corner v = x + 2y + 4z is inside iff sdf < 0; each face is walked counter-clockwise as seen from
+// outside; a crossing edge reached from an outside corner starts a segment that ends at the next
+// crossing of the walk (diagonal inside corners of a face stay separated; face-local, so watertight);
+// segments chain into loops; each loop, started at its smallest edge id, becomes a triangle fan.
+//
+// k_marching_cubes: one thread per grid vertex column of a cube row (4 loads, the x + 1 corners from the
+// next lane), tables in shared memory, warp scan + one atomicAdd per warp that meets the surface
+// (output order is therefore not deterministic; the triangle set is).  Vertices are interpolated from the
+// edge's lower corner so both cubes sharing an edge produce the same bits.  Bound: HBM (4 B of sdf per
+// grid vertex + 36 B per triangle).
+#include <algorithm>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "sand_internal.h"
+
+namespace sand {
+
+__constant__ uint8_t c_mc_ntri[256];
+__constant__ uint8_t c_mc_tri[256][15];   // up to 5 triangles x 3 edge ids
+__constant__ uint8_t c_mc_edge[12][2];    // (lower corner, upper corner)
+
+static void mc_build_tables(uint8_t ntri[256], uint8_t tri[256][15], uint8_t edge[12][2]) {
+  int ne = 0;
+  for (int a = 0; a < 3; ++a)
+    for (int v = 0; v < 8; ++v)
+      if (!((v >> a) & 1)) {
+        edge[ne][0] = (uint8_t)v;
+        edge[ne][1] = (uint8_t)(v | (1 << a));
+        ++ne;
+      }
+  int edge_id[8][8];
+  for (int p = 0; p < 8; ++p)
+    for (int q = 0; q < 8; ++q) edge_id[p][q] = -1;
+  for (int e = 0; e < 12; ++e) edge_id[edge[e][0]][edge[e][1]] = edge_id[edge[e][1]][edge[e][0]] = e;
+  // faces: normal axis a, side s; in-face axes u = a+1, w = a+2 (mod 3) with e_u x e_w = e_a, so the
+  // cycle (0,0) (1,0) (1,1) (0,1) in (u, w) is counter-clockwise about +e_a; reversed for side 0
+  int face[6][4];
+  for (int a = 0, f = 0; a < 3; ++a) {
+    const int u = (a + 1) % 3, w = (a + 2) % 3;
+    const int cu[4] = {0, 1, 1, 0}, cw[4] = {0, 0, 1, 1};
+    for (int s = 0; s < 2; ++s, ++f)
+      for (int k = 0; k < 4; ++k) {
+        const int kk = s ? k : 3 - k;
+        face[f][k] = (s << a) | (cu[kk] << u) | (cw[kk] << w);
+      }
+  }
+  for (int c = 0; c < 256; ++c) {
+    int next[12];
+    for (int e = 0; e < 12; ++e) next[e] = -1;
+    for (int f = 0; f < 6; ++f) {
+      int ce[4], cin[4], m = 0;
+      for (int k = 0; k < 4; ++k) {
+        const int p = face[f][k], q = face[f][(k + 1) & 3];
+        const int ip = (c >> p) & 1, iq = (c >> q) & 1;
+        if (ip != iq) {
+          ce[m] = edge_id[p][q];
+          cin[m] = iq;   // walked from outside into inside
+          ++m;
+        }
+      }
+      for (int k = 0; k < m; ++k)
+        if (cin[k]) next[ce[k]] = ce[(k + 1) % m];
+    }
+    bool used[12] = {};
+    int nt = 0;
+    for (int e0 = 0; e0 < 12; ++e0) {
+      if (next[e0] < 0 || used[e0]) continue;
+      int loop[12], k = 0;
+      for (int e = e0; !used[e]; e = next[e]) {
+        used[e] = true;
+        loop[k++] = e;
+      }
+      for (int m = 1; m + 1 < k; ++m) {
+        tri[c][3 * nt] = (uint8_t)loop[0];
+        tri[c][3 * nt + 1] = (uint8_t)loop[m];
+        tri[c][3 * nt + 2] = (uint8_t)loop[m + 1];
+        ++nt;
+      }
+    }
+    ntri[c] = (uint8_t)nt;
+  }
+}
+
+cudaError_t mc_upload_tables() {
+  static bool done = false;
+  if (done) return cudaSuccess;
+  uint8_t ntri[256], tri[256][15] = {}, edge[12][2];
+  mc_build_tables(ntri, tri, edge);
+  cudaError_t e = cudaMemcpyToSymbol(c_mc_ntri, ntri, sizeof ntri);
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_mc_tri, tri, sizeof tri);
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_mc_edge, edge, sizeof edge);
+  done = e == cudaSuccess;
+  return e;
+}
+
+// Grid axis x_i = fl32(2 i / (R - 1) - 1), computed in double (reading R8).
+__global__ void k_grid_axis(int R, float* __restrict__ axis) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < R) axis[i] = (float)(2.0 * (double)i / (double)(R - 1) - 1.0);
+}
+
+// Points of grid planes [k0, k0 + np): index (i + R j) + R^2 (k - k0), x fastest.
+__global__ void k_grid_points(const float* __restrict__ axis, int R, int k0, int np, float* __restrict__ pts) {
+  const long long n = (long long)R * R * np;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n; q += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(q % R), j = (int)((q / R) % R), k = k0 + (int)(q / ((long long)R * R));
+    pts[3 * q] = axis[i];
+    pts[3 * q + 1] = axis[j];
+    pts[3 * q + 2] = axis[k];
+  }
+}
+
+// Cubes (i, j, k), 0 <= i, j < R - 1, kc0 <= k < kc1, over an sdf buffer holding planes from kp0 on.
+// Thread = grid vertex column i of a cube row (j, k): it loads the 4 values at x = i of the row's two
+// y rows and two z planes and takes the x = i + 1 values from the next lane (the last lane of a warp
+// loads them itself), so a cube costs ~4 loads instead of 8.  32-bit indices (the host splits launches
+// so R (R - 1) (kc1 - kc0) < 2^31).
+__global__ void __launch_bounds__(256) k_marching_cubes(const float* __restrict__ sdf, int R, int kc0, int kc1,
+                                                        int kp0, const float* __restrict__ axis,
+                                                        float* __restrict__ tris, long long cap,
+                                                        unsigned long long* __restrict__ counter) {
+  const unsigned R1 = (unsigned)R - 1u;
+  const unsigned n = (unsigned)R * R1 * (unsigned)(kc1 - kc0);
+  const int lane = threadIdx.x & 31;
+  const long long R2 = (long long)R * R;
+  __shared__ uint8_t s_tri[256][15];   // tables in shared memory: per-thread (divergent) indices
+  __shared__ uint8_t s_ntri[256];
+  __shared__ uint8_t s_edge[12][2];
+  for (int t = threadIdx.x; t < 256 * 15; t += blockDim.x) s_tri[t / 15][t % 15] = c_mc_tri[t / 15][t % 15];
+  for (int t = threadIdx.x; t < 256; t += blockDim.x) s_ntri[t] = c_mc_ntri[t];
+  if (threadIdx.x < 24) s_edge[threadIdx.x >> 1][threadIdx.x & 1] = c_mc_edge[threadIdx.x >> 1][threadIdx.x & 1];
+  __syncthreads();
+  // corner value v of the current cube without dynamic register indexing
+  auto corner = [](const float (&lo)[4], const float (&hi)[4], int v) {
+    const int u = ((v >> 1) & 1) | (((v >> 2) & 1) << 1);
+    const float a = u == 0 ? lo[0] : u == 1 ? lo[1] : u == 2 ? lo[2] : lo[3];
+    const float b = u == 0 ? hi[0] : u == 1 ? hi[1] : u == 2 ? hi[2] : hi[3];
+    return (v & 1) ? b : a;
+  };
+  for (unsigned base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
+    const unsigned q = base + threadIdx.x;
+    const bool inr = q < n;
+    const unsigned i = inr ? q % (unsigned)R : 0u, row = inr ? q / (unsigned)R : 0u;
+    const unsigned j = row % R1, k = (unsigned)kc0 + row / R1;
+    const float* s0 = sdf + (long long)(k - kp0) * R2 + (long long)j * R + i;
+    float lo[4];   // x = i: (y, z) = (0,0) (1,0) (0,1) (1,1)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) lo[u] = inr ? __ldg(s0 + (u >> 1) * R2 + (u & 1) * R) : 0.f;
+    float hi[4];   // x = i + 1
+#pragma unroll
+    for (int u = 0; u < 4; ++u) hi[u] = __shfl_down_sync(0xffffffffu, lo[u], 1);
+    const bool cube = inr && i + 1u < (unsigned)R;
+    if (cube && lane == 31) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) hi[u] = __ldg(s0 + 1 + (u >> 1) * R2 + (u & 1) * R);
+    }
+    int c = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int v = ((u & 1) << 1) | ((u >> 1) << 2);   // corner of (y, z) = (u & 1, u >> 1) at x = 0
+      c |= (lo[u] < 0.f) << v;
+      c |= (hi[u] < 0.f) << (v | 1);
+    }
+    const int nt = cube ? s_ntri[c] : 0;
+    if (!__any_sync(0xffffffffu, nt)) continue;   // most warps meet no surface
+    int off = nt;   // warp-inclusive scan of the triangle counts
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, off, d);
+      if (lane >= d) off += y;
+    }
+    unsigned long long wbase = 0;
+    if (lane == 31) wbase = atomicAdd(counter, (unsigned long long)off);
+    wbase = __shfl_sync(0xffffffffu, wbase, 31);
+    const long long first = (long long)wbase + off - nt;
+    for (int t = 0; t < nt; ++t) {
+      if (first + t >= cap) break;
+      float* out = tris + 9 * (first + t);
+#pragma unroll
+      for (int m = 0; m < 3; ++m) {
+        const int e = s_tri[c][3 * t + m];
+        const int v0 = s_edge[e][0], v1 = s_edge[e][1];
+        const float a0 = corner(lo, hi, v0), a1 = corner(lo, hi, v1);
+        const float tt = a0 / (a0 - a1);
+        const float p0x = axis[i + (v0 & 1)], p0y = axis[j + ((v0 >> 1) & 1)], p0z = axis[k + (v0 >> 2)];
+        const float p1x = axis[i + (v1 & 1)], p1y = axis[j + ((v1 >> 1) & 1)], p1z = axis[k + (v1 >> 2)];
+        out[3 * m] = p0x + tt * (p1x - p0x);
+        out[3 * m + 1] = p0y + tt * (p1y - p0y);
+        out[3 * m + 2] = p0z + tt * (p1z - p0z);
+      }
+    }
+  }
+}
+
+cudaError_t launch_grid_axis(int R, float* axis, cudaStream_t st) {
+  k_grid_axis<<<(R + 255) / 256, 256, 0, st>>>(R, axis);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_grid_points(const float* axis, int R, int k0, int np, float* pts, int num_sms, cudaStream_t st) {
+  k_grid_points<<<num_sms * 8, 256, 0, st>>>(axis, R, k0, np, pts);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_marching_cubes(const float* sdf, int R, int kc0, int kc1, int kp0, const float* axis, float* tris,
+                                  long long cap, unsigned long long* counter, int num_sms, cudaStream_t st) {
+  const long long per_plane = (long long)R * (R - 1);
+  const int kstep = (int)std::max(1ll, ((1ll << 31) - 1) / std::max(per_plane, 1ll));
+  for (int k0 = kc0; k0 < kc1; k0 += kstep) {
+    const int k1 = std::min(kc1, k0 + kstep);
+    const long long n = per_plane * (k1 - k0);
+    long long blocks = (n + 255) / 256;
+    if (blocks > (long long)num_sms * 16) blocks = (long long)num_sms * 16;
+    k_marching_cubes<<<(unsigned)blocks, 256, 0, st>>>(sdf, R, k0, k1, kp0, axis, tris, cap, counter);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace sand

@@ -40,6 +40,14 @@ struct sand_ctx {
   float* d_wt_f32 = nullptr;      // FP32 hidden weights transposed [L-1][k][j] (depth-map population)
   uint8_t* d_dp_tmp = nullptr;    // per-sample depths of sand_populate_leaf_depths
   long long cap_dp = 0;
+  // marching cubes (mesh.cu): grid axis, slab buffers of the fused extraction, triangle counter
+  float* d_axis = nullptr;
+  int axis_R = 0;
+  float* d_mpts = nullptr;
+  float* d_msdf = nullptr;
+  uint8_t* d_mdep = nullptr;
+  long long cap_m = 0;
+  unsigned long long* d_tricount = nullptr;
   MlpDev mlp{};
   // depth map
   bool have_dm = false;
@@ -189,6 +197,7 @@ extern "C" int sand_destroy(sand_ctx* ctx) {
   free_weights(ctx);
   free_hostpipe(ctx);
   dfree(ctx->d_dp_tmp);
+  dfree(ctx->d_axis); dfree(ctx->d_mpts); dfree(ctx->d_msdf); dfree(ctx->d_mdep); dfree(ctx->d_tricount);
   for (auto& q : ctx->evq)
     for (auto& v : q)
       if (v) cudaEventDestroy(v);
@@ -695,6 +704,74 @@ extern "C" int sand_debug_perm(sand_ctx* ctx, uint32_t* host_perm, int64_t cap, 
   *n_binned = nb;
   if (host_perm && cap > 0) CU(cudaMemcpy(host_perm, ctx->d_perm, sizeof(uint32_t) * (size_t)std::min<long long>(cap, nb), cudaMemcpyDeviceToHost));
   return SAND_OK;
+}
+
+// ------------------------------------------------------------------------------- marching cubes
+static int mesh_prepare(sand_ctx* ctx, int R) {
+  CU(mc_upload_tables());
+  if (ctx->axis_R != R) {
+    CU(cudaStreamSynchronize(ctx->stream));
+    dfree(ctx->d_axis);
+    CU(cudaMalloc(&ctx->d_axis, sizeof(float) * R));
+    ctx->axis_R = R;
+    CU(launch_grid_axis(R, ctx->d_axis, ctx->stream));
+  }
+  if (!ctx->d_tricount) CU(cudaMalloc(&ctx->d_tricount, sizeof(unsigned long long)));
+  CU(cudaMemsetAsync(ctx->d_tricount, 0, sizeof(unsigned long long), ctx->stream));
+  return SAND_OK;
+}
+
+static int mesh_finish(sand_ctx* ctx, int64_t* n_tris) {
+  unsigned long long h = 0;
+  CU(cudaMemcpyAsync(&h, ctx->d_tricount, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  *n_tris = (int64_t)h;
+  return SAND_OK;
+}
+
+extern "C" int sand_marching_cubes(sand_ctx* ctx, const float* d_sdf, int R, float* d_tris, int64_t cap,
+                                   int64_t* n_tris) {
+  if (!ctx) return fail(ctx, SAND_ERR_ARG, "NULL ctx");
+  if (R < 2 || cap < 0 || !n_tris || !d_sdf || (cap > 0 && !d_tris))
+    return fail(ctx, SAND_ERR_ARG, "sand_marching_cubes: R < 2, cap < 0 or NULL argument");
+  CU(cudaSetDevice(ctx->cfg.device));
+  int rc = mesh_prepare(ctx, R);
+  if (rc) return rc;
+  CU(launch_marching_cubes(d_sdf, R, 0, R - 1, 0, ctx->d_axis, d_tris, cap, ctx->d_tricount, ctx->num_sms,
+                           ctx->stream));
+  return mesh_finish(ctx, n_tris);
+}
+
+extern "C" int sand_mesh_grid(sand_ctx* ctx, int R, int slab, float* d_tris, int64_t cap, int64_t* n_tris) {
+  if (!ctx) return fail(ctx, SAND_ERR_ARG, "NULL ctx");
+  if (R < 2 || slab < 0 || cap < 0 || !n_tris || (cap > 0 && !d_tris))
+    return fail(ctx, SAND_ERR_ARG, "sand_mesh_grid: R < 2, slab < 0, cap < 0 or NULL argument");
+  if (!ctx->have_w || !ctx->have_dm) return fail(ctx, SAND_ERR_STATE, "load weights and depth map first");
+  CU(cudaSetDevice(ctx->cfg.device));
+  if (slab == 0) slab = 32;
+  if (slab > R - 1) slab = R - 1;
+  int rc = mesh_prepare(ctx, R);
+  if (rc) return rc;
+  const long long np = (long long)R * R * (slab + 1);   // points of the slab's slab + 1 planes
+  if (np > ctx->cap_m) {
+    CU(cudaStreamSynchronize(ctx->stream));
+    dfree(ctx->d_mpts); dfree(ctx->d_msdf); dfree(ctx->d_mdep);
+    CU(cudaMalloc(&ctx->d_mpts, sizeof(float) * 3 * np));
+    CU(cudaMalloc(&ctx->d_msdf, sizeof(float) * np));
+    CU(cudaMalloc(&ctx->d_mdep, (size_t)np));
+    ctx->cap_m = np;
+  }
+  for (int kc0 = 0; kc0 < R - 1; kc0 += slab) {
+    const int kc1 = std::min(kc0 + slab, R - 1);   // cubes kc0 .. kc1 - 1 need planes kc0 .. kc1
+    const int npl = kc1 - kc0 + 1;
+    const long long n = (long long)R * R * npl;
+    CU(launch_grid_points(ctx->d_axis, R, kc0, npl, ctx->d_mpts, ctx->num_sms, ctx->stream));
+    rc = sand_query(ctx, ctx->d_mpts, n, ctx->d_msdf, ctx->d_mdep);
+    if (rc) return rc;
+    CU(launch_marching_cubes(ctx->d_msdf, R, kc0, kc1, kc0, ctx->d_axis, d_tris, cap, ctx->d_tricount,
+                             ctx->num_sms, ctx->stream));
+  }
+  return mesh_finish(ctx, n_tris);
 }
 
 // ------------------------------------------------------------------------------- depth-map population

@@ -97,6 +97,12 @@ size_t simt_smem_bytes(int L, int H, int tail);
 cudaError_t prepare_tmlp_kernels(int L, int H, int tail, int prec);
 // depth-map population (depthpop.cu)
 bool depthpop_supported(int H);
+// Marching cubes (mesh.cu)
+cudaError_t mc_upload_tables();
+cudaError_t launch_grid_axis(int R, float* axis, cudaStream_t st);
+cudaError_t launch_grid_points(const float* axis, int R, int k0, int np, float* pts, int num_sms, cudaStream_t st);
+cudaError_t launch_marching_cubes(const float* sdf, int R, int kc0, int kc1, int kp0, const float* axis, float* tris,
+                                  long long cap, unsigned long long* counter, int num_sms, cudaStream_t st);
 cudaError_t launch_query_dynamic(const MlpDev& m, const float* w_t, const float* pts, long long n, float r,
                                  float* out_sdf, uint8_t* out_depth, int num_sms, cudaStream_t st);
 cudaError_t launch_required_depth(const MlpDev& m, const float* w_t, const float* pts, long long n, float r,

@@ -51,7 +51,7 @@ class sand_stats(ctypes.Structure):
 EXPORTS = ("sand_create", "sand_destroy", "sand_load_weights", "sand_load_depthmap", "sand_set_stream",
            "sand_set_lod_cap", "sand_reserve", "sand_query", "sand_query_host", "sand_get_stats",
            "sand_debug_perm", "sand_last_error", "sand_abi_version", "sand_required_depth",
-           "sand_populate_leaf_depths", "sand_query_dynamic")
+           "sand_populate_leaf_depths", "sand_query_dynamic", "sand_marching_cubes", "sand_mesh_grid")
 
 _lib = None
 
@@ -83,6 +83,8 @@ def load_library(path=None):
     lib.sand_required_depth.argtypes = [vp, vp, i64, ctypes.c_float, ctypes.c_int, vp]
     lib.sand_populate_leaf_depths.argtypes = [vp, vp, i64, ctypes.c_int, ctypes.c_float, vp]
     lib.sand_query_dynamic.argtypes = [vp, vp, i64, ctypes.c_float, vp, vp]
+    lib.sand_marching_cubes.argtypes = [vp, vp, ctypes.c_int, vp, i64, ctypes.POINTER(i64)]
+    lib.sand_mesh_grid.argtypes = [vp, ctypes.c_int, ctypes.c_int, vp, i64, ctypes.POINTER(i64)]
     for f in EXPORTS:
         if f not in ("sand_last_error",):
             getattr(lib, f).restype = ctypes.c_int
@@ -198,6 +200,19 @@ class SandContext:
     def sand_query_dynamic(self, d_points, n, r, d_out_sdf, d_out_exit_depth):
         self._chk(self.lib.sand_query_dynamic(self.h, ctypes.c_void_p(d_points), int(n), float(r),
                                               ctypes.c_void_p(d_out_sdf), ctypes.c_void_p(d_out_exit_depth)))
+
+    # -- marching cubes on the query grid ----------------------------------------------
+    def sand_marching_cubes(self, d_sdf, R, d_tris, cap):
+        n = ctypes.c_int64(0)
+        self._chk(self.lib.sand_marching_cubes(self.h, ctypes.c_void_p(d_sdf), int(R), ctypes.c_void_p(d_tris),
+                                               int(cap), ctypes.byref(n)))
+        return n.value
+
+    def sand_mesh_grid(self, R, slab, d_tris, cap):
+        n = ctypes.c_int64(0)
+        self._chk(self.lib.sand_mesh_grid(self.h, int(R), int(slab), ctypes.c_void_p(d_tris), int(cap),
+                                          ctypes.byref(n)))
+        return n.value
 
     # -- torch convenience (device tensors in, device tensors out) -----------------------------------
     def query_tensor(self, pts, sdf=None, depth=None):

@@ -6,7 +6,7 @@ mkdir -p abl
 C=paper_2604_25936_b200/csrc
 F="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr -I include"
 objs=""
-for src in sand_api lookup tmlp_simt tmlp_tc tmlp_tc3 depthpop; do
+for src in sand_api lookup tmlp_simt tmlp_tc tmlp_tc3 depthpop mesh; do
   nvcc $F -c $C/$src.cu -o abl/$src.o & objs="$objs abl/$src.o"
 done
 nvcc $F $2 -c $C/tmlp_tc2.cu -o abl/tc2_$1.o &

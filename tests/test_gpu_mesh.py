@@ -1,0 +1,122 @@
+"""GPU parity for marching cubes (reading R24) through the C ABI:
+sand_marching_cubes on analytic sdf grids against oracle.marching_cubes (same rule, independent code),
+and the fused slab-by-slab extraction sand_mesh_grid against the unfused pipeline (sand_query on the
+whole grid, then sand_marching_cubes) on the same weights and depth map.
+
+The triangulation is unique under R24, so the triangle sets are compared exactly (vertex coordinates
+within FP32 interpolation error); the output order is not (atomic placement), so triangles are sorted
+canonically before comparing."""
+import numpy as np
+import pytest
+
+import oracle
+import sandgen as g
+from _engine import make_ctx
+
+pytestmark = pytest.mark.gpu
+
+
+def _grid(R):
+    ax = (2.0 * np.arange(R) / (R - 1) - 1.0).astype(np.float32).astype(np.float64)
+    Z, Y, X = np.meshgrid(ax, ax, ax, indexing="ij")
+    return X, Y, Z
+
+
+def _canon(T, q=1e-4):
+    """Sort triangles by their quantised vertex tuples (vertex order within a triangle kept: it is
+    fixed by R24 up to the fan's start, which R24 also fixes)."""
+    T = np.asarray(T, np.float64).reshape(-1, 9)
+    key = np.round(T / q).astype(np.int64)
+    return T[np.lexsort(key.T[::-1])]
+
+
+def _gpu_mc(ctx, sdf_np, R):
+    import torch
+    s = torch.from_numpy(np.ascontiguousarray(sdf_np, np.float32)).cuda()
+    n = ctx.sand_marching_cubes(s.data_ptr(), R, 0, 0)
+    tris = torch.empty(max(n, 1) * 9, dtype=torch.float32, device="cuda")
+    n2 = ctx.sand_marching_cubes(s.data_ptr(), R, tris.data_ptr(), n)
+    assert n2 == n
+    return tris[: 9 * n].cpu().numpy().reshape(-1, 3, 3)
+
+
+def _watertight(T):
+    keys = {}
+    idx = [[keys.setdefault(tuple(v), len(keys)) for v in map(tuple, tri)] for tri in np.asarray(T, np.float32)]
+    directed = {}
+    for a, b, c in idx:
+        for u, v in ((a, b), (b, c), (c, a)):
+            directed[(u, v)] = directed.get((u, v), 0) + 1
+    return all(n == 1 and directed.get((v, u), 0) == 1 for (u, v), n in directed.items()), len(keys), len(directed) // 2, len(idx)
+
+
+@pytest.mark.parametrize("shape,R", [("sphere", 33), ("torus", 40), ("two", 29)])
+def test_marching_cubes_matches_oracle(shape, R):
+    X, Y, Z = _grid(R)
+    if shape == "sphere":
+        sdf = np.sqrt(X ** 2 + Y ** 2 + Z ** 2) - 0.61
+    elif shape == "torus":
+        sdf = np.sqrt((np.sqrt(X ** 2 + Y ** 2) - 0.55) ** 2 + Z ** 2) - 0.22
+    else:
+        sdf = np.minimum(np.sqrt((X - 0.45) ** 2 + Y ** 2 + Z ** 2), np.sqrt((X + 0.45) ** 2 + Y ** 2 + Z ** 2)) - 0.3
+    sdf = sdf.astype(np.float32)
+    spec = g.TMlpSpec(L=2, H=64, omega0=30.0, seed=1)
+    with make_ctx(spec, 2) as ctx:
+        T = _gpu_mc(ctx, sdf.ravel(), R)
+    To = oracle.marching_cubes(sdf.ravel().astype(np.float64), R)
+    assert T.shape == To.shape
+    np.testing.assert_allclose(_canon(T), _canon(To), rtol=0, atol=2e-6)
+    ok, V, E, F = _watertight(T)                      # bit-identical shared vertices on the GPU too
+    assert ok and V - E + F == {"sphere": 2, "torus": 0, "two": 4}[shape]
+
+
+def test_capacity_and_empty():
+    R = 21
+    X, Y, Z = _grid(R)
+    sdf = (np.sqrt(X ** 2 + Y ** 2 + Z ** 2) - 0.5).astype(np.float32).ravel()
+    import torch
+    spec = g.TMlpSpec(L=2, H=64, omega0=30.0, seed=1)
+    with make_ctx(spec, 2) as ctx:
+        s = torch.from_numpy(sdf).cuda()
+        n = ctx.sand_marching_cubes(s.data_ptr(), R, 0, 0)
+        guard = torch.full((9 * (n // 2) + 9,), 7.0, device="cuda")
+        assert ctx.sand_marching_cubes(s.data_ptr(), R, guard.data_ptr(), n // 2) == n   # count, partial write
+        assert torch.all(guard[9 * (n // 2):] == 7.0)                                  # nothing past cap
+        pos = torch.ones(R ** 3, device="cuda")
+        assert ctx.sand_marching_cubes(pos.data_ptr(), R, guard.data_ptr(), 1) == 0    # no surface
+
+
+@pytest.mark.parametrize("slab", [0, 7, 64])
+def test_fused_mesh_equals_unfused(slab):
+    """sand_mesh_grid (slab-wise, device-generated grid points) == sand_query over the whole grid then
+    sand_marching_cubes, exactly (same sdf values, same triangles)."""
+    import torch
+    c = g.make_config("C0")
+    p = c.params()
+    R = 65
+    with make_ctx(c.spec, 0) as ctx:
+        ctx.sand_load_weights(g.pack_blob(p))
+        ctx.sand_load_depthmap(c.depthmap)
+        pts = torch.from_numpy(g.grid_points(R)).cuda()
+        sdf, _ = ctx.query_tensor(pts)
+        torch.cuda.synchronize()
+        n = ctx.sand_marching_cubes(sdf.data_ptr(), R, 0, 0)
+        a = torch.empty(9 * n, device="cuda")
+        ctx.sand_marching_cubes(sdf.data_ptr(), R, a.data_ptr(), n)
+        m = ctx.sand_mesh_grid(R, slab, 0, 0)
+        b = torch.empty(9 * max(m, 1), device="cuda")
+        assert ctx.sand_mesh_grid(R, slab, b.data_ptr(), m) == m == n
+        A, B = _canon(a.cpu().numpy()), _canon(b[: 9 * m].cpu().numpy())
+        np.testing.assert_array_equal(A, B)
+        assert n > 1000
+        # the SIREN surface leaves the [-1, 1]^3 domain: every directed edge occurs once, and an edge
+        # without its reverse must lie on the domain boundary
+        Tv = B.reshape(-1, 3, 3).astype(np.float32)
+        directed = {}
+        for tri in Tv:
+            vs = [tuple(v) for v in tri]
+            for u, v in ((vs[0], vs[1]), (vs[1], vs[2]), (vs[2], vs[0])):
+                directed[(u, v)] = directed.get((u, v), 0) + 1
+        assert max(directed.values()) == 1
+        on_face = lambda v: np.any(np.abs(np.abs(np.array(v)) - 1.0) < 1e-6)
+        assert all(on_face(u) and on_face(v) for (u, v) in directed if (v, u) not in directed)
