@@ -395,8 +395,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc3Shape<H>::THREADS
     const uint32_t tm_q = tmem_base + ((uint32_t)(32 * q) << 16);
     const uint32_t a_st = sA + (uint32_t)(4 * q + (lane >> 3)) * 1024 + (uint32_t)(lane & 7) * 128;
     const float2 SM2 = make_float2(p.m.omega0, p.m.omega0);
-    const float* tb = tab + p.m.pt_off_bias;   // [L][HP], row 0 = 0
-    const float* ta = tab + p.m.pt_off_a;      // [L][HP]
+    const float* tba = tab + p.m.pt_off_bias;  // [L][HP/2][bias pair, a pair], row 0 bias = 0
     const uint32_t afull_dst0 = rank == 0 ? b_afull : mapa_shared(b_afull, 0);
     auto quad_sum = [](float v) {
       v += __shfl_xor_sync(0xffffffffu, v, 1);
@@ -418,8 +417,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc3Shape<H>::THREADS
     auto half_cols = [&](auto nch_c, int c0, int l, bool store, bool wait_b) {
       constexpr int NCH = decltype(nch_c)::value;
       constexpr int HOLD = 4;
-      const float* bias = tb + (l - 1) * HP + c0 + 2 * tq;
-      const float* a = ta + (l - 1) * HP + c0 + 2 * tq;
+      const float* ba = tba + (l - 1) * 2 * HP + (c0 + 2 * tq) * 2;
       float2 yv[4] = {};
       uint32_t held[HOLD][4];
       auto put = [&](int ci, const uint32_t (&pk)[4]) {
@@ -458,8 +456,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc3Shape<H>::THREADS
           if (i0 + i < NCH) {
             const int ci = i0 + i;
             const int jc = 8 * ci;
-            const float2 b2 = *reinterpret_cast<const float2*>(bias + jc);
-            const float2 a2 = *reinterpret_cast<const float2*>(a + jc);
+            const float4 ba4 = *reinterpret_cast<const float4*>(ba + 2 * jc);
+            const float2 b2 = make_float2(ba4.x, ba4.y), a2 = make_float2(ba4.z, ba4.w);
             uint32_t pk[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
@@ -564,7 +562,7 @@ int tc3_padded_width(int H) { return (H + 31) / 32 * 32; }
 bool tc3_usable(int L, int H, int tail) {
   if (!tc3_available(H, tail)) return false;
   MlpDev m{};
-  tc2_table_layout(L, tc3_padded_width(H), tail, &m, false);
+  tc2_table_layout(L, tc3_padded_width(H), tail, &m, true);
   return smem_for3<336>(m.pt_floats, L, 2) <= kSmemMax3;
 }
 
@@ -573,13 +571,13 @@ void tc3_build_host(int L, int H, float w0, const float* const* W, const float* 
                     std::vector<uint8_t>* img) {
   using C = Tc3Shape<336>;
   const int HP = C::HP;
-  tc2_table_layout(L, HP, SAND_TAIL_LINEAR, m, false);
+  tc2_table_layout(L, HP, SAND_TAIL_LINEAR, m, true);
   m->pt_npoly = 0;
   tables->assign((size_t)m->pt_floats, 0.f);
   for (int i = 1; i < L; ++i)
-    for (int j = 0; j < H; ++j) (*tables)[m->pt_off_bias + (size_t)i * HP + j] = w0 * b[i][j];
+    for (int j = 0; j < H; ++j) (*tables)[m->pt_off_bias + (size_t)i * 2 * HP + (size_t)(j / 2) * 4 + (j & 1)] = w0 * b[i][j];
   for (int i = 0; i < L; ++i) {
-    for (int j = 0; j < H; ++j) (*tables)[m->pt_off_a + (size_t)i * HP + j] = a[i][j];
+    for (int j = 0; j < H; ++j) (*tables)[m->pt_off_bias + (size_t)i * 2 * HP + (size_t)(j / 2) * 4 + 2 + (j & 1)] = a[i][j];
     (*tables)[m->pt_off_c + i] = c[i];
   }
   double cs = 0.0;

@@ -9,6 +9,8 @@ timeout 300 python bench.py --config C1 --no-cpu > gpurun_out/${tag}_bench_c1.lo
 timeout 300 python bench.py --full-depth --no-cpu --no-e2e > gpurun_out/${tag}_bench_c2_full.log 2>&1; echo "bench full rc=$?"
 timeout 300 python bench.py --task populate > gpurun_out/${tag}_bench_pop.log 2>&1; echo "bench pop rc=$?"
 timeout 600 python bench.py --task sweep --steps 5 > gpurun_out/${tag}_bench_sweep.log 2>&1; echo "bench sweep rc=$?"
+timeout 600 python bench.py --task dynamic > gpurun_out/${tag}_bench_dynamic.log 2>&1; echo "bench dynamic rc=$?"
+timeout 600 python bench.py --task mesh > gpurun_out/${tag}_bench_mesh.log 2>&1; echo "bench mesh rc=$?"
 timeout 300 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/${tag}_bench_ref.log 2>&1; echo "bench ref rc=$?"
 python bench.py --no-cpu --no-e2e --steps 1 --warmup 3 > gpurun_out/${tag}_plain.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${tag}_launches.csv python bench.py --no-cpu --no-e2e --steps 1 --warmup 3 > gpurun_out/${tag}_ncu1.log 2>&1
