@@ -416,10 +416,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc3Shape<H>::THREADS
     // registers until b_bhead (by then job B is normally past K-chunk 2).
     auto half_cols = [&](auto nch_c, int c0, int l, bool store, bool wait_b) {
       constexpr int NCH = decltype(nch_c)::value;
-      constexpr int HOLD = 4;
+      constexpr int HOLD = 2;
       const float* ba = tba + (l - 1) * 2 * HP + (c0 + 2 * tq) * 2;
       float2 yv[4] = {};
-      uint32_t held[HOLD][4];
+      uint32_t held[HOLD > 0 ? HOLD : 1][4];
       auto put = [&](int ci, const uint32_t (&pk)[4]) {
         const uint32_t u = (uint32_t)((c0 + 8 * ci) >> 3);
         stmatrix_x4(a_st + (u >> 3) * C::A_CHUNK + (((u & 7u) ^ (uint32_t)(lane & 7)) << 4), pk);
