@@ -8,8 +8,9 @@
 // crossing of the walk (diagonal inside corners of a face stay separated; face-local, so watertight);
 // segments chain into loops; each loop, started at its smallest edge id, becomes a triangle fan.
 //
-// k_marching_cubes: one thread per grid vertex column of a cube row (4 loads, the x + 1 corners from the
-// next lane), tables in shared memory, warp scan + one atomicAdd per warp that meets the surface
+// k_marching_cubes: blocks walk cube rows; one thread per grid vertex column of a row (4 loads, the x + 1
+// corners from the next lane), tables in shared memory, warp scan + one atomicAdd per warp that meets
+// the surface
 // (output order is therefore not deterministic; the triangle set is).  Vertices are interpolated from the
 // edge's lower corner so both cubes sharing an edge produce the same bits.  Bound: HBM (4 B of sdf per
 // grid vertex + 36 B per triangle).
@@ -117,18 +118,17 @@ __global__ void k_grid_points(const float* __restrict__ axis, int R, int k0, int
 }
 
 // Cubes (i, j, k), 0 <= i, j < R - 1, kc0 <= k < kc1, over an sdf buffer holding planes from kp0 on.
-// Thread = grid vertex column i of a cube row (j, k): it loads the 4 values at x = i of the row's two
-// y rows and two z planes and takes the x = i + 1 values from the next lane (the last lane of a warp
-// loads them itself), so a cube costs ~4 loads instead of 8.  32-bit indices (the host splits launches
-// so R (R - 1) (kc1 - kc0) < 2^31).
+// A block walks cube rows (j, k) (grid-stride, no per-element index division); a thread is grid vertex
+// column i of the row: it loads the 4 values at x = i of the row's two y rows and two z planes and takes
+// the x = i + 1 values from the next lane (the last lane of a warp loads them itself), ~4 loads a cube.
 __global__ void __launch_bounds__(256) k_marching_cubes(const float* __restrict__ sdf, int R, int kc0, int kc1,
                                                         int kp0, const float* __restrict__ axis,
                                                         float* __restrict__ tris, long long cap,
                                                         unsigned long long* __restrict__ counter) {
-  const unsigned R1 = (unsigned)R - 1u;
-  const unsigned n = (unsigned)R * R1 * (unsigned)(kc1 - kc0);
   const int lane = threadIdx.x & 31;
+  const int R1 = R - 1;
   const long long R2 = (long long)R * R;
+  const long long nrows = (long long)R1 * (kc1 - kc0);
   __shared__ uint8_t s_tri[256][15];   // tables in shared memory: per-thread (divergent) indices
   __shared__ uint8_t s_ntri[256];
   __shared__ uint8_t s_edge[12][2];
@@ -143,56 +143,57 @@ __global__ void __launch_bounds__(256) k_marching_cubes(const float* __restrict_
     const float b = u == 0 ? hi[0] : u == 1 ? hi[1] : u == 2 ? hi[2] : hi[3];
     return (v & 1) ? b : a;
   };
-  for (unsigned base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
-    const unsigned q = base + threadIdx.x;
-    const bool inr = q < n;
-    const unsigned i = inr ? q % (unsigned)R : 0u, row = inr ? q / (unsigned)R : 0u;
-    const unsigned j = row % R1, k = (unsigned)kc0 + row / R1;
-    const float* s0 = sdf + (long long)(k - kp0) * R2 + (long long)j * R + i;
-    float lo[4];   // x = i: (y, z) = (0,0) (1,0) (0,1) (1,1)
+  for (long long row = blockIdx.x; row < nrows; row += gridDim.x) {
+    const int j = (int)(row % R1), k = kc0 + (int)(row / R1);
+    const float* rowp = sdf + (long long)(k - kp0) * R2 + (long long)j * R;
+    for (int i0 = 0; i0 < R; i0 += blockDim.x) {
+      const int i = i0 + threadIdx.x;
+      const bool inr = i < R;
+      float lo[4];   // x = i: (y, z) = (0,0) (1,0) (0,1) (1,1)
 #pragma unroll
-    for (int u = 0; u < 4; ++u) lo[u] = inr ? __ldg(s0 + (u >> 1) * R2 + (u & 1) * R) : 0.f;
-    float hi[4];   // x = i + 1
+      for (int u = 0; u < 4; ++u) lo[u] = inr ? __ldg(rowp + i + (u >> 1) * R2 + (u & 1) * R) : 0.f;
+      float hi[4];   // x = i + 1
 #pragma unroll
-    for (int u = 0; u < 4; ++u) hi[u] = __shfl_down_sync(0xffffffffu, lo[u], 1);
-    const bool cube = inr && i + 1u < (unsigned)R;
-    if (cube && lane == 31) {
+      for (int u = 0; u < 4; ++u) hi[u] = __shfl_down_sync(0xffffffffu, lo[u], 1);
+      const bool cube = inr && i + 1 < R;
+      if (cube && lane == 31) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) hi[u] = __ldg(s0 + 1 + (u >> 1) * R2 + (u & 1) * R);
-    }
-    int c = 0;
+        for (int u = 0; u < 4; ++u) hi[u] = __ldg(rowp + i + 1 + (u >> 1) * R2 + (u & 1) * R);
+      }
+      int c = 0;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int v = ((u & 1) << 1) | ((u >> 1) << 2);   // corner of (y, z) = (u & 1, u >> 1) at x = 0
-      c |= (lo[u] < 0.f) << v;
-      c |= (hi[u] < 0.f) << (v | 1);
-    }
-    const int nt = cube ? s_ntri[c] : 0;
-    if (!__any_sync(0xffffffffu, nt)) continue;   // most warps meet no surface
-    int off = nt;   // warp-inclusive scan of the triangle counts
+      for (int u = 0; u < 4; ++u) {
+        const int v = ((u & 1) << 1) | ((u >> 1) << 2);   // corner of (y, z) = (u & 1, u >> 1) at x = 0
+        c |= (lo[u] < 0.f) << v;
+        c |= (hi[u] < 0.f) << (v | 1);
+      }
+      const int nt = cube ? s_ntri[c] : 0;
+      if (!__any_sync(0xffffffffu, nt)) continue;   // most warps meet no surface
+      int off = nt;   // warp-inclusive scan of the triangle counts
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, off, d);
-      if (lane >= d) off += y;
-    }
-    unsigned long long wbase = 0;
-    if (lane == 31) wbase = atomicAdd(counter, (unsigned long long)off);
-    wbase = __shfl_sync(0xffffffffu, wbase, 31);
-    const long long first = (long long)wbase + off - nt;
-    for (int t = 0; t < nt; ++t) {
-      if (first + t >= cap) break;
-      float* out = tris + 9 * (first + t);
+      for (int d = 1; d < 32; d <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, off, d);
+        if (lane >= d) off += y;
+      }
+      unsigned long long wbase = 0;
+      if (lane == 31) wbase = atomicAdd(counter, (unsigned long long)off);
+      wbase = __shfl_sync(0xffffffffu, wbase, 31);
+      const long long first = (long long)wbase + off - nt;
+      for (int t = 0; t < nt; ++t) {
+        if (first + t >= cap) break;
+        float* out = tris + 9 * (first + t);
 #pragma unroll
-      for (int m = 0; m < 3; ++m) {
-        const int e = s_tri[c][3 * t + m];
-        const int v0 = s_edge[e][0], v1 = s_edge[e][1];
-        const float a0 = corner(lo, hi, v0), a1 = corner(lo, hi, v1);
-        const float tt = a0 / (a0 - a1);
-        const float p0x = axis[i + (v0 & 1)], p0y = axis[j + ((v0 >> 1) & 1)], p0z = axis[k + (v0 >> 2)];
-        const float p1x = axis[i + (v1 & 1)], p1y = axis[j + ((v1 >> 1) & 1)], p1z = axis[k + (v1 >> 2)];
-        out[3 * m] = p0x + tt * (p1x - p0x);
-        out[3 * m + 1] = p0y + tt * (p1y - p0y);
-        out[3 * m + 2] = p0z + tt * (p1z - p0z);
+        for (int m = 0; m < 3; ++m) {
+          const int e = s_tri[c][3 * t + m];
+          const int v0 = s_edge[e][0], v1 = s_edge[e][1];
+          const float a0 = corner(lo, hi, v0), a1 = corner(lo, hi, v1);
+          const float tt = a0 / (a0 - a1);
+          const float p0x = axis[i + (v0 & 1)], p0y = axis[j + ((v0 >> 1) & 1)], p0z = axis[k + (v0 >> 2)];
+          const float p1x = axis[i + (v1 & 1)], p1y = axis[j + ((v1 >> 1) & 1)], p1z = axis[k + (v1 >> 2)];
+          out[3 * m] = p0x + tt * (p1x - p0x);
+          out[3 * m + 1] = p0y + tt * (p1y - p0y);
+          out[3 * m + 2] = p0z + tt * (p1z - p0z);
+        }
       }
     }
   }
@@ -210,18 +211,11 @@ cudaError_t launch_grid_points(const float* axis, int R, int k0, int np, float* 
 
 cudaError_t launch_marching_cubes(const float* sdf, int R, int kc0, int kc1, int kp0, const float* axis, float* tris,
                                   long long cap, unsigned long long* counter, int num_sms, cudaStream_t st) {
-  const long long per_plane = (long long)R * (R - 1);
-  const int kstep = (int)std::max(1ll, ((1ll << 31) - 1) / std::max(per_plane, 1ll));
-  for (int k0 = kc0; k0 < kc1; k0 += kstep) {
-    const int k1 = std::min(kc1, k0 + kstep);
-    const long long n = per_plane * (k1 - k0);
-    long long blocks = (n + 255) / 256;
-    if (blocks > (long long)num_sms * 16) blocks = (long long)num_sms * 16;
-    k_marching_cubes<<<(unsigned)blocks, 256, 0, st>>>(sdf, R, k0, k1, kp0, axis, tris, cap, counter);
-    const cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-  }
-  return cudaSuccess;
+  const long long nrows = (long long)(R - 1) * (kc1 - kc0);
+  if (nrows <= 0) return cudaSuccess;
+  const long long blocks = std::min<long long>(nrows, (long long)num_sms * 8);
+  k_marching_cubes<<<(unsigned)blocks, 256, 0, st>>>(sdf, R, kc0, kc1, kp0, axis, tris, cap, counter);
+  return cudaGetLastError();
 }
 
 }  // namespace sand
