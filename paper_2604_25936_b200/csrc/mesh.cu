@@ -16,6 +16,7 @@
 // grid vertex + 36 B per triangle).
 #include <algorithm>
 #include <cstdint>
+#include <mutex>
 #include <cuda_runtime.h>
 
 #include "sand_internal.h"
@@ -89,14 +90,20 @@ static void mc_build_tables(uint8_t ntri[256], uint8_t tri[256][15], uint8_t edg
 }
 
 cudaError_t mc_upload_tables() {
-  static bool done = false;
-  if (done) return cudaSuccess;
+  // constant memory is per device: upload once for each device this process uses
+  static std::mutex mu;
+  static uint64_t done = 0;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  if (dev < 64 && ((done >> dev) & 1)) return cudaSuccess;
   uint8_t ntri[256], tri[256][15] = {}, edge[12][2];
   mc_build_tables(ntri, tri, edge);
-  cudaError_t e = cudaMemcpyToSymbol(c_mc_ntri, ntri, sizeof ntri);
+  e = cudaMemcpyToSymbol(c_mc_ntri, ntri, sizeof ntri);
   if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_mc_tri, tri, sizeof tri);
   if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_mc_edge, edge, sizeof edge);
-  done = e == cudaSuccess;
+  if (e == cudaSuccess && dev < 64) done |= 1ull << dev;
   return e;
 }
 

@@ -691,14 +691,14 @@ bool tc2_usable(int L, int H, int tail) {
 }
 
 int tc2_npoly() {
-  static int np = -1;
-  if (np < 0) {
-    np = kPairPolyDefault;
+  static const int np = [] {   // thread-safe one-time initialisation
+    int v = kPairPolyDefault;
     if (const char* ev = getenv("SAND_NPOLY")) {
-      const int v = atoi(ev);
-      if (v == 0 || v == 8 || v == 16) np = v;
+      const int x = atoi(ev);
+      if (x == 0 || x == 8 || x == 16) v = x;
     }
-  }
+    return v;
+  }();
   return np;
 }
 
