@@ -356,13 +356,17 @@ def run_dynamic(args):
             return e0.elapsed_time(e1) / k
 
         ms_oct = timed(lambda: ctx.sand_query(pts.data_ptr(), n, sdf.data_ptr(), dep.data_ptr()), 5)
-        for name, r in (("paper r = 1.5e-4", 1.5e-4), (f"r = 30% quantile of |t_i| ({r30:.3e})", r30)):
-            ms = timed(lambda: ctx.sand_query_dynamic(pts.data_ptr(), n, r, sdf.data_ptr(), dep.data_ptr()), steps)
-            hist = np.bincount(dep.cpu().numpy(), minlength=c.spec.L + 1)[:c.spec.L + 1].tolist()
-            entries.append({"threshold": name, "r": r, "value": n / (ms / 1e3), "unit": UNIT, "ms_per_step": ms,
-                            "exit_depth_hist": hist,
-                            "mean_exit_depth": float(np.dot(np.arange(len(hist)), hist) / n)})
-            print(f"[dynamic] {name}: {n / (ms / 1e3) / 1e9:.3f} G points/s ({ms:.1f} ms)", file=sys.stderr, flush=True)
+        for mode in ("tile", "pool"):   # tile-level early exit / pools re-compacted after every layer
+            os.environ["SAND_DYN_POOL"] = "1" if mode == "pool" else "0"
+            for name, r in (("paper r = 1.5e-4", 1.5e-4), (f"r = 30% quantile of |t_i| ({r30:.3e})", r30)):
+                ms = timed(lambda: ctx.sand_query_dynamic(pts.data_ptr(), n, r, sdf.data_ptr(), dep.data_ptr()), steps)
+                hist = np.bincount(dep.cpu().numpy(), minlength=c.spec.L + 1)[:c.spec.L + 1].tolist()
+                entries.append({"mode": mode, "threshold": name, "r": r, "value": n / (ms / 1e3), "unit": UNIT,
+                                "ms_per_step": ms, "exit_depth_hist": hist,
+                                "mean_exit_depth": float(np.dot(np.arange(len(hist)), hist) / n)})
+                print(f"[dynamic] {mode} {name}: {n / (ms / 1e3) / 1e9:.3f} G points/s ({ms:.1f} ms)", file=sys.stderr,
+                      flush=True)
+        os.environ.pop("SAND_DYN_POOL", None)
     cpu = None
     if not args.no_cpu:
         k = 20000

@@ -186,8 +186,9 @@ int sand_populate_leaf_depths(sand_ctx* ctx, const float* d_samples, int64_t n_l
  * layer i >= 2 whose residual |t_i| < r (reading R23: t_1 = y_1 is the first prediction, not
  * a residual), else at L:
  *   d_out_exit_depth[p] = that layer (255 for a non-finite point),  d_out_sdf[p] = y_d (NaN if 255).
- * FP32 (accurate sine) like the population calls above; a 64-point tile stops as soon as all of its
- * points have stopped (no re-compaction across tiles).  Only the weights must be loaded; the depth map
+ * FP32 (accurate sine) like the population calls above.  Default schedule: a 64-point tile stops as
+ * soon as all of its points have stopped; with the environment variable SAND_DYN_POOL=1 (read per call)
+ * pools of 512 points are re-compacted after every layer instead.  Only the weights must be loaded; the depth map
  * and LOD cap are ignored.  Asynchronous on ctx's stream.  Errors: SAND_ERR_ARG (n < 0, r < 0 or NaN,
  * NULL buffer), SAND_ERR_STATE, SAND_ERR_UNSUPPORTED (H as above), SAND_ERR_CUDA. */
 int sand_query_dynamic(sand_ctx* ctx, const float* d_points, int64_t n, float r, float* d_out_sdf,

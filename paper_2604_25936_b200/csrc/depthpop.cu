@@ -43,6 +43,227 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// ---- building blocks shared by the kernels below (one 64-point tile, activations [unit][point])
+// W^T rows [k0, k0 + KC) of a layer -> stage buffer b (H % 16 == 0: rows are whole float4s)
+template <int H>
+__device__ __forceinline__ void dp_stage(float* ws, const float* W, int k0, int b, int tid) {
+  using C = DpShape<H>;
+  constexpr int RV = H / 4;
+  for (int i = tid; i < C::KC * RV; i += kDpThreads) {
+    const int kk = i / RV, j4 = i % RV;
+    cp_async16(ws + (b * C::KC + kk) * C::HP + 4 * j4, W + (size_t)(k0 + kk) * H + 4 * j4);
+  }
+  cp_async_commit();
+}
+
+// hout[j][p] = sin(w0 (W h_in)[j][p] + w0 b[j]) for a hidden layer (W^T given, [k][j]); register-blocked
+// FP32 GEMM, W^T streamed through two cp.async stages.  Ends with the block synchronised.
+template <int H>
+__device__ __forceinline__ void dp_hidden(const float* W, const float* bias, float w0, const float* hin, float* hout,
+                                          float* ws, int tid) {
+  using C = DpShape<H>;
+  const int tj = tid & 31, tp = tid >> 5;
+  float acc[kDpPPW][C::U];
+#pragma unroll
+  for (int a = 0; a < kDpPPW; ++a)
+#pragma unroll
+    for (int u = 0; u < C::U; ++u) acc[a][u] = 0.f;
+  __syncthreads();   // previous users of both stage buffers are done
+  dp_stage<H>(ws, W, 0, 0, tid);
+  for (int k0 = 0, b = 0; k0 < H; k0 += C::KC, b ^= 1) {
+    if (k0 + C::KC < H) {
+      dp_stage<H>(ws, W, k0 + C::KC, b ^ 1, tid);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const float* wsb = ws + b * C::KC * C::HP;
+#pragma unroll 4
+    for (int kk = 0; kk < C::KC; ++kk) {
+      float hv[kDpPPW];
+#pragma unroll
+      for (int q4 = 0; q4 < kDpPPW / 4; ++q4) {
+        const float4 hq = *reinterpret_cast<const float4*>(hin + (k0 + kk) * kDpS + tp * kDpPPW + 4 * q4);
+        hv[4 * q4] = hq.x; hv[4 * q4 + 1] = hq.y; hv[4 * q4 + 2] = hq.z; hv[4 * q4 + 3] = hq.w;
+      }
+#pragma unroll
+      for (int u = 0; u < C::U; ++u) {
+        const float w = wsb[kk * C::HP + tj + 32 * u];
+#pragma unroll
+        for (int a = 0; a < kDpPPW; ++a) acc[a][u] = fmaf(w, hv[a], acc[a][u]);
+      }
+    }
+    __syncthreads();   // stage b is overwritten by the copy issued next iteration
+  }
+#pragma unroll
+  for (int u = 0; u < C::U; ++u) {
+    const int j = tj + 32 * u;
+    const float bb = j < H ? bias[j] : 0.f;
+#pragma unroll
+    for (int a = 0; a < kDpPPW; ++a) hout[j * kDpS + tp * kDpPPW + a] = j < H ? sinf(fmaf(acc[a][u], w0, bb)) : 0.f;
+  }
+  __syncthreads();
+}
+
+// t_l of every tile point (LINEAR: a . h + c;  MULT, l >= 2: (a . h + c)(a1 . h + c1)) -> tl[p]
+template <int H, int TAIL>
+__device__ __forceinline__ void dp_tails(const MlpDev& m, int l, const float* hcur, float* tl, int tid) {
+  const int tj = tid & 31, tp = tid >> 5;
+  const float* a_t = m.tables + m.off_a;
+  const float* a1_t = m.tables + m.off_a1;
+  const float* c_t = m.tables + m.off_c;
+  const float* c1_t = m.tables + m.off_c1;
+  for (int pp = 0; pp < kDpPPW; ++pp) {
+    const int p = tp * kDpPPW + pp;
+    float s0 = 0.f, s1 = 0.f;
+    for (int j = tj; j < H; j += 32) {
+      const float h = hcur[j * kDpS + p];
+      s0 = fmaf(a_t[(l - 1) * H + j], h, s0);
+      if (TAIL == SAND_TAIL_MULT && l >= 2) s1 = fmaf(a1_t[(l - 2) * H + j], h, s1);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    }
+    if (tj == 0) {
+      float t = s0 + c_t[l - 1];
+      if (TAIL == SAND_TAIL_MULT && l >= 2) t *= s1 + c1_t[l - 2];
+      tl[p] = t;
+    }
+  }
+}
+
+// Dynamic exit with re-compaction (SURVEY 8(f) NEXT #3 as the north star states it): a block owns pools
+// of kDynPool points and runs them layer-synchronously -- every layer over the pool's still-running
+// points only, packed into full 64-point tiles (the survivors' slots are compacted after each layer),
+// with their activations parked in a per-block global scratch hbuf[slot][HP] between layers (L2-
+// resident).  The work is the sum of the exit layers, not a tile's slowest point.
+constexpr int kDynPool = 512;
+#ifndef SAND_DYN_ABL
+#define SAND_DYN_ABL 0   // timing ablation (wrong results): 1 = no activation gather / park
+#endif
+
+template <int H, int TAIL>
+__global__ void __launch_bounds__(kDpThreads, 1) k_dynamic_pool(MlpDev m, const float* __restrict__ w_t,
+                                                                const float* __restrict__ pts, long long n, float r,
+                                                                float* __restrict__ out_sdf,
+                                                                uint8_t* __restrict__ out_dep,
+                                                                float* __restrict__ hbuf_all) {
+  using C = DpShape<H>;
+  extern __shared__ __align__(16) float sm[];
+  float* hA = sm;                               // [HP][kDpS]: this tile's h_{l-1}
+  float* hB = hA + C::HP * kDpS;                // [HP][kDpS]: this tile's h_l
+  float* ws = hB + C::HP * kDpS;                // [2][KC][HP]
+  __shared__ float px[3][kDpP];
+  __shared__ float tl[kDpP];
+  __shared__ int act[kDynPool];                 // running slots, packed
+  __shared__ float ybuf[kDynPool];              // y_l per slot
+  __shared__ int keep[kDynPool];                // scan scratch for the compaction
+  __shared__ int s_nact;
+  const int L = m.L;
+  const float w0 = m.omega0;
+  const int tid = threadIdx.x;
+  const float4* w1 = reinterpret_cast<const float4*>(m.tables + m.off_w1);
+  const float* bias_t = m.tables + m.off_bias;
+  float* hbuf = hbuf_all + (size_t)blockIdx.x * kDynPool * C::HP;
+  for (int i = tid; i < 2 * C::KC * C::HP; i += kDpThreads) ws[i] = 0.f;
+  const long long npool = (n + kDynPool - 1) / kDynPool;
+  for (long long pool = blockIdx.x; pool < npool; pool += gridDim.x) {
+    const long long base = pool * kDynPool;
+    const int cnt = (int)min((long long)kDynPool, n - base);
+    __syncthreads();
+    // non-finite points leave at once; the others start running
+    if (tid == 0) s_nact = 0;
+    __syncthreads();
+    for (int q = tid; q < kDynPool; q += kDpThreads) {
+      int run = 0;
+      if (q < cnt) {
+        const float x = pts[3 * (base + q)], y = pts[3 * (base + q) + 1], z = pts[3 * (base + q) + 2];
+        run = isfinite(x) && isfinite(y) && isfinite(z);
+        if (!run) { out_dep[base + q] = 255; out_sdf[base + q] = __int_as_float(0x7fc00000); }
+      }
+      keep[q] = run;
+      ybuf[q] = 0.f;
+    }
+    __syncthreads();
+    if (tid == 0) {   // serial stable compaction (kDynPool entries; negligible against a layer's GEMM)
+      int k = 0;
+      for (int q = 0; q < cnt; ++q) if (keep[q]) act[k++] = q;
+      s_nact = k;
+    }
+    __syncthreads();
+    for (int l = 1; l <= L && s_nact > 0; ++l) {
+      const int nact = s_nact;
+      for (int t0 = 0; t0 < nact; t0 += kDpP) {
+        const int np = min(kDpP, nact - t0);
+        if (l == 1) {
+          for (int i = tid; i < 3 * kDpP; i += kDpThreads) {
+            const int p = i / 3, c = i % 3;
+            px[c][p] = p < np ? pts[3 * (base + act[t0 + p]) + c] : 0.f;
+          }
+          __syncthreads();
+          for (int i = tid; i < C::HP * kDpP; i += kDpThreads) {
+            const int j = i / kDpP, p = i % kDpP;
+            float h = 0.f;
+            if (j < H) {
+              const float4 w = w1[j];
+              h = sinf(fmaf(w.z, px[2][p], fmaf(w.y, px[1][p], fmaf(w.x, px[0][p], w.w))));
+            }
+            hB[j * kDpS + p] = h;
+          }
+          __syncthreads();
+        } else {
+          // gather h_{l-1} of the tile's slots: float4 loads, all of a thread's loads in flight at once
+          constexpr int NV = kDpP * C::HP / 4 / kDpThreads;   // float4 per thread
+          float4 v[NV];
+#pragma unroll
+          for (int u = 0; u < NV; ++u) {
+            const int i = tid + u * kDpThreads, p = i / (C::HP / 4), j4 = i % (C::HP / 4);
+            v[u] = (p < np && SAND_DYN_ABL != 1)
+                       ? *reinterpret_cast<const float4*>(hbuf + (size_t)act[t0 + p] * C::HP + 4 * j4)
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+#pragma unroll
+          for (int u = 0; u < NV; ++u) {
+            const int i = tid + u * kDpThreads, p = i / (C::HP / 4), j = 4 * (i % (C::HP / 4));
+            hA[j * kDpS + p] = v[u].x;
+            hA[(j + 1) * kDpS + p] = v[u].y;
+            hA[(j + 2) * kDpS + p] = v[u].z;
+            hA[(j + 3) * kDpS + p] = v[u].w;
+          }
+          dp_hidden<H>(w_t + (size_t)(l - 2) * H * H, bias_t + (size_t)(l - 2) * H, w0, hA, hB, ws, tid);
+        }
+        dp_tails<H, TAIL>(m, l, hB, tl, tid);
+        __syncthreads();
+        if (tid < np) {
+          const int q = act[t0 + tid];
+          const float y = ybuf[q] + tl[tid];
+          ybuf[q] = y;
+          const bool stop = l == L || (l >= 2 && fabsf(tl[tid]) < r);
+          if (stop) { out_sdf[base + q] = y; out_dep[base + q] = (uint8_t)l; }
+          keep[t0 + tid] = !stop;
+        }
+        if (l < L && SAND_DYN_ABL != 1)   // park h_l of the tile's slots for the next layer (float4 stores)
+          for (int i = tid; i < kDpP * C::HP / 4; i += kDpThreads) {
+            const int p = i / (C::HP / 4), j = 4 * (i % (C::HP / 4));
+            if (p < np)
+              *reinterpret_cast<float4*>(hbuf + (size_t)act[t0 + p] * C::HP + j) =
+                  make_float4(hB[j * kDpS + p], hB[(j + 1) * kDpS + p], hB[(j + 2) * kDpS + p], hB[(j + 3) * kDpS + p]);
+          }
+        __syncthreads();
+      }
+      if (tid == 0) {
+        int k = 0;
+        for (int q = 0; q < nact; ++q) if (keep[q]) act[k++] = act[q];
+        s_nact = k;
+      }
+      __syncthreads();
+    }
+  }
+}
+
 // MODE 0: Eq. 5 required depth of every point (full-depth evaluation, decision after layer L).
 // MODE 1: dynamic exit without a depth map ('SAND w/o Octree'; R23): a point stops at
 //   the first layer i >= 2 with |t_i| < r (else L) and returns y_i; a tile stops computing as soon as all
@@ -266,9 +487,42 @@ cudaError_t launch_required_depth(const MlpDev& m, const float* w_t, const float
   return launch_dp(m, w_t, pts, n, r, near, out, nullptr, 0, num_sms, st);
 }
 
+template <int H, int TAIL>
+static cudaError_t launch_pool_t(const MlpDev& m, const float* w_t, const float* pts, long long n, float r,
+                                 float* out_sdf, uint8_t* out_depth, float* hbuf, int grid, cudaStream_t st) {
+  const size_t sm = DpShape<H>::SMEM;
+  cudaError_t e = cudaFuncSetAttribute(k_dynamic_pool<H, TAIL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  k_dynamic_pool<H, TAIL><<<grid, kDpThreads, sm, st>>>(m, w_t, pts, n, r, out_sdf, out_depth, hbuf);
+  return cudaGetLastError();
+}
+
+size_t dynamic_scratch_floats(int H, int num_sms) {
+  return (size_t)num_sms * kDynPool * (size_t)((H + 31) / 32 * 32);
+}
+
 cudaError_t launch_query_dynamic(const MlpDev& m, const float* w_t, const float* pts, long long n, float r,
-                                 float* out_sdf, uint8_t* out_depth, int num_sms, cudaStream_t st) {
-  return launch_dp(m, w_t, pts, n, r, 1, out_depth, out_sdf, 1, num_sms, st);
+                                 float* out_sdf, uint8_t* out_depth, float* hbuf, int num_sms, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  if (!hbuf)   // tile-level early exit (no scratch): MODE 1 of the population kernel
+    return launch_dp(m, w_t, pts, n, r, 1, out_depth, out_sdf, 1, num_sms, st);
+  const long long npool = (n + kDynPool - 1) / kDynPool;
+  const int grid = (int)(npool < num_sms ? npool : num_sms);
+  const bool mult = m.tail == SAND_TAIL_MULT;
+#define SAND_DYN_CASE(HH)                                                                              \
+  case HH:                                                                                             \
+    return mult ? launch_pool_t<HH, 1>(m, w_t, pts, n, r, out_sdf, out_depth, hbuf, grid, st)          \
+                : launch_pool_t<HH, 0>(m, w_t, pts, n, r, out_sdf, out_depth, hbuf, grid, st);
+  switch (m.H) {
+    SAND_DYN_CASE(16)
+    SAND_DYN_CASE(32)
+    SAND_DYN_CASE(64)
+    SAND_DYN_CASE(128)
+    SAND_DYN_CASE(256)
+    SAND_DYN_CASE(336)
+    default: return cudaErrorInvalidValue;
+  }
+#undef SAND_DYN_CASE
 }
 
 cudaError_t launch_leaf_max(const uint8_t* d, long long n_leaves, int spl, uint8_t* out, cudaStream_t st) {

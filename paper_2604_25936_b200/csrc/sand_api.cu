@@ -48,6 +48,7 @@ struct sand_ctx {
   uint8_t* d_mdep = nullptr;
   long long cap_m = 0;
   unsigned long long* d_tricount = nullptr;
+  float* d_dyn_h = nullptr;       // dynamic-exit activation scratch (per block, kDynPool x HP floats)
   MlpDev mlp{};
   // depth map
   bool have_dm = false;
@@ -197,6 +198,7 @@ extern "C" int sand_destroy(sand_ctx* ctx) {
   free_weights(ctx);
   free_hostpipe(ctx);
   dfree(ctx->d_dp_tmp);
+  dfree(ctx->d_dyn_h);
   dfree(ctx->d_axis); dfree(ctx->d_mpts); dfree(ctx->d_msdf); dfree(ctx->d_mdep); dfree(ctx->d_tricount);
   for (auto& q : ctx->evq)
     for (auto& v : q)
@@ -798,7 +800,18 @@ extern "C" int sand_query_dynamic(sand_ctx* ctx, const float* d_points, int64_t 
   if (!d_points || !d_out_sdf || !d_out_exit_depth) return fail(ctx, SAND_ERR_ARG, "NULL buffer");
   if (!depthpop_supported(ctx->cfg.H)) return fail(ctx, SAND_ERR_UNSUPPORTED, "H = %d", ctx->cfg.H);
   CU(cudaSetDevice(ctx->cfg.device));
-  CU(launch_query_dynamic(ctx->mlp, ctx->d_wt_f32, d_points, n, r, d_out_sdf, d_out_exit_depth, ctx->num_sms,
+  // default: tile-level early exit (measured faster on the synthetic workloads);
+  // SAND_DYN_POOL=1: pools re-compacted after every layer (read per call)
+  const char* ev = getenv("SAND_DYN_POOL");
+  const bool pool = ev && atoi(ev) != 0;
+  float* hbuf = nullptr;
+  if (pool) {
+    if (!ctx->d_dyn_h) {
+      CU(cudaMalloc(&ctx->d_dyn_h, sizeof(float) * dynamic_scratch_floats(ctx->cfg.H, ctx->num_sms)));
+    }
+    hbuf = ctx->d_dyn_h;
+  }
+  CU(launch_query_dynamic(ctx->mlp, ctx->d_wt_f32, d_points, n, r, d_out_sdf, d_out_exit_depth, hbuf, ctx->num_sms,
                           ctx->stream));
   return SAND_OK;
 }

@@ -103,8 +103,11 @@ cudaError_t launch_grid_axis(int R, float* axis, cudaStream_t st);
 cudaError_t launch_grid_points(const float* axis, int R, int k0, int np, float* pts, int num_sms, cudaStream_t st);
 cudaError_t launch_marching_cubes(const float* sdf, int R, int kc0, int kc1, int kp0, const float* axis, float* tris,
                                   long long cap, unsigned long long* counter, int num_sms, cudaStream_t st);
+// hbuf: per-block activation scratch (dynamic_scratch_floats) -> pool kernel with re-compaction;
+// nullptr -> tile-level early exit
 cudaError_t launch_query_dynamic(const MlpDev& m, const float* w_t, const float* pts, long long n, float r,
-                                 float* out_sdf, uint8_t* out_depth, int num_sms, cudaStream_t st);
+                                 float* out_sdf, uint8_t* out_depth, float* hbuf, int num_sms, cudaStream_t st);
+size_t dynamic_scratch_floats(int H, int num_sms);
 cudaError_t launch_required_depth(const MlpDev& m, const float* w_t, const float* pts, long long n, float r,
                                   int near, uint8_t* out, int num_sms, cudaStream_t st);
 cudaError_t launch_leaf_max(const uint8_t* d, long long n_leaves, int spl, uint8_t* out, cudaStream_t st);

@@ -51,8 +51,10 @@ def _check(p, pts, r, sdf, dep):
     return same.mean(), np.bincount(d, minlength=L + 1)
 
 
+@pytest.mark.parametrize("pool", [0, 1])
 @pytest.mark.parametrize("H,L,tail", [(64, 6, 0), (256, 8, 0), (128, 5, 1), (336, 8, 0), (32, 1, 0)])
-def test_dynamic_exit_matches_oracle(H, L, tail):
+def test_dynamic_exit_matches_oracle(H, L, tail, pool, monkeypatch):
+    monkeypatch.setenv("SAND_DYN_POOL", str(pool))   # tile-level exit / per-layer re-compaction
     spec = g.TMlpSpec(L=L, H=H, omega0=30.0, tail=tail, seed=21 + H)
     p = g.make_weights(spec)
     pts = np.random.default_rng(H).uniform(-1, 1, (5003, 3)).astype(np.float32)
@@ -71,9 +73,11 @@ def test_dynamic_exit_matches_oracle(H, L, tail):
         assert hist[2] > 0 and hist[L] > 0, hist   # some points stop early, some run to L
 
 
-def test_dynamic_special_cases_and_sizes():
+@pytest.mark.parametrize("pool", [0, 1])
+def test_dynamic_special_cases_and_sizes(pool, monkeypatch):
     """r = 0 -> full depth (= query_full); huge r -> everyone stops at layer 2; n in {0, 1, 65} and a
     ragged last tile."""
+    monkeypatch.setenv("SAND_DYN_POOL", str(pool))
     spec = g.TMlpSpec(L=5, H=64, omega0=30.0, seed=31)
     p = g.make_weights(spec)
     pts = np.random.default_rng(3).uniform(-1, 1, (1000, 3)).astype(np.float32)
