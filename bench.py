@@ -410,7 +410,7 @@ def run_mesh(args):
         ctx.sand_load_depthmap(c.depthmap)
         st = torch.cuda.current_stream(dev)
         ctx.sand_set_stream(st.cuda_stream)
-        ntri = ctx.sand_mesh_grid(R, 32, 0, 0)
+        ntri = ctx.sand_mesh_grid(R, 0, 0, 0)
         tris = torch.empty(9 * ntri, dtype=torch.float32, device=dev)
 
         def timed(fn, k):
@@ -425,7 +425,7 @@ def run_mesh(args):
             torch.cuda.synchronize(dev)
             return e0.elapsed_time(e1) / k
 
-        ms_fused = timed(lambda: ctx.sand_mesh_grid(R, 32, tris.data_ptr(), ntri), steps)
+        ms_fused = timed(lambda: ctx.sand_mesh_grid(R, 0, tris.data_ptr(), ntri), steps)
         pts = torch.from_numpy(g.grid_points(R)).to(dev)
         sdf = torch.empty(n, dtype=torch.float32, device=dev)
         dep = torch.empty(n, dtype=torch.uint8, device=dev)
@@ -437,7 +437,7 @@ def run_mesh(args):
     line = {"task": "mesh", "metric": "marching-cubes mesh extraction of the 512^3 SDF grid (fused with the query path)",
             "value": n / (ms_fused / 1e3), "unit": UNIT, "n_gpus": 1, "steps": steps, "warmup": args.warmup,
             "ms_per_step": ms_fused, "higher_is_better": True, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": f"C2 {R}^3 grid, 8x256 SIREN T-MLP, level-7 octree, slabs of 32 cube planes"},
+            "config": {"workload": f"C2 {R}^3 grid, 8x256 SIREN T-MLP, level-7 octree, slabs of 64 cube planes"},
             "triangles": ntri, "triangles_unfused": n2,
             "unfused": {"ms_query": ms_query, "ms_marching_cubes": ms_mc, "ms_total": ms_query + ms_mc,
                         "sdf_grid_bytes": 4 * n},

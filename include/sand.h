@@ -209,9 +209,10 @@ int sand_query_dynamic(sand_ctx* ctx, const float* d_points, int64_t n, float r,
 int sand_marching_cubes(sand_ctx* ctx, const float* d_sdf, int R, float* d_tris, int64_t cap, int64_t* n_tris);
 
 /* Fused extraction: evaluates the adaptive query path (sand_query with the loaded weights, depth map and
- * LOD cap) slab by slab -- slab planes of cubes at a time (0 = 32), slab + 1 grid planes of points
- * generated on the device -- and meshes each slab as soon as its sdf exists, so the R^3 sdf grid is
- * never materialised (R = 512: 35 MB of slab buffers instead of 537 MB). */
+ * LOD cap) slab by slab -- slab planes of cubes at a time (0 = 64), the slab's grid planes of points
+ * generated on the device (the shared boundary plane's sdf carried over, not re-queried) -- and meshes
+ * each slab as soon as its sdf exists, so the R^3 sdf grid is never materialised (R = 512, slab 64:
+ * 290 MB of slab buffers instead of the 1.6 GB of points and 537 MB of sdf of the whole grid). */
 int sand_mesh_grid(sand_ctx* ctx, int R, int slab, float* d_tris, int64_t cap, int64_t* n_tris);
 
 /* Message for the last error on ctx (or of the last failed sand_create if ctx is NULL).

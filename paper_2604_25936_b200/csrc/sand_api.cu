@@ -750,7 +750,7 @@ extern "C" int sand_mesh_grid(sand_ctx* ctx, int R, int slab, float* d_tris, int
     return fail(ctx, SAND_ERR_ARG, "sand_mesh_grid: R < 2, slab < 0, cap < 0 or NULL argument");
   if (!ctx->have_w || !ctx->have_dm) return fail(ctx, SAND_ERR_STATE, "load weights and depth map first");
   CU(cudaSetDevice(ctx->cfg.device));
-  if (slab == 0) slab = 32;
+  if (slab == 0) slab = 64;
   if (slab > R - 1) slab = R - 1;
   int rc = mesh_prepare(ctx, R);
   if (rc) return rc;
@@ -763,12 +763,17 @@ extern "C" int sand_mesh_grid(sand_ctx* ctx, int R, int slab, float* d_tris, int
     CU(cudaMalloc(&ctx->d_mdep, (size_t)np));
     ctx->cap_m = np;
   }
+  const long long R2 = (long long)R * R;
   for (int kc0 = 0; kc0 < R - 1; kc0 += slab) {
     const int kc1 = std::min(kc0 + slab, R - 1);   // cubes kc0 .. kc1 - 1 need planes kc0 .. kc1
-    const int npl = kc1 - kc0 + 1;
-    const long long n = (long long)R * R * npl;
-    CU(launch_grid_points(ctx->d_axis, R, kc0, npl, ctx->d_mpts, ctx->num_sms, ctx->stream));
-    rc = sand_query(ctx, ctx->d_mpts, n, ctx->d_msdf, ctx->d_mdep);
+    // plane kc0 was the previous slab's last plane: move its sdf down instead of querying it again
+    const int q0 = kc0 == 0 ? 0 : 1;
+    if (q0) CU(cudaMemcpyAsync(ctx->d_msdf, ctx->d_msdf + (long long)slab * R2, sizeof(float) * R2,
+                               cudaMemcpyDeviceToDevice, ctx->stream));
+    const int npl = kc1 - kc0 + 1 - q0;
+    const long long n = R2 * npl;
+    CU(launch_grid_points(ctx->d_axis, R, kc0 + q0, npl, ctx->d_mpts, ctx->num_sms, ctx->stream));
+    rc = sand_query(ctx, ctx->d_mpts, n, ctx->d_msdf + q0 * R2, ctx->d_mdep);
     if (rc) return rc;
     CU(launch_marching_cubes(ctx->d_msdf, R, kc0, kc1, kc0, ctx->d_axis, d_tris, cap, ctx->d_tricount,
                              ctx->num_sms, ctx->stream));
