@@ -462,6 +462,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-sample", type=int, default=1 << 15)
     ap.add_argument("--full-depth", action="store_true", help="all-L depth map (non-adaptive GPU baseline)")
+    ap.add_argument("--prec", default="bf16", choices=["bf16", "fp32"],
+                    help="fp32: the accurate FP32 path (register-blocked SIMT GEMM), reported against the FP32 ALU peak")
     ap.add_argument("--task", default="query", choices=["query", "populate", "sweep", "dynamic", "mesh"],
                     help="query: the adaptive SDF query path (BASELINE metric); populate: depth-map "
                          "population (Eq. 5/6, SURVEY 8(f) NEXT #1) on the config's finest octree leaves")
@@ -519,7 +521,9 @@ def main():
     sdf = torch.empty(n, dtype=torch.float32, device=dev)
     dep = torch.empty(n, dtype=torch.uint8, device=dev)
 
-    ctx = SandContext(c.spec.L, c.spec.H, c.spec.omega0, SAND_BF16, c.spec.tail, dev_index)
+    from paper_2604_25936_b200 import SAND_FP32
+    fp32 = args.prec == "fp32"
+    ctx = SandContext(c.spec.L, c.spec.H, c.spec.omega0, SAND_FP32 if fp32 else SAND_BF16, c.spec.tail, dev_index)
     ctx.sand_load_weights(g.pack_blob(p))
     ctx.sand_load_depthmap(dm)
     ctx.sand_reserve(n)
@@ -601,20 +605,28 @@ def main():
         f_ns = sum(per_depth[d] * d * 2.0 * H * H for d in range(1, c.spec.L + 1))
         f_exec_rank0 = st["flops_exec"]
         ach = f_exec_rank0 / (ms_mlp / 1e3) / 1e12
+        if fp32:   # the FP32 path: roofline against the FP32 FMA pipe (148 SM x 128 lanes x 2 FLOP x clock)
+            sm_mhz = (clocks or {}).get("sm_mhz") or 1965.0
+            pk = dict(pk, bf16=148 * 128 * 2 * sm_mhz * 1e6 / 1e12, bf16_sus=148 * 128 * 2 * sm_mhz * 1e6 / 1e12,
+                      src="derived FP32 ALU (148 SM x 128 lanes x 2 FLOP x median clock);")
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "vs_baseline": None, "dtype": "f32" if fp32 else "bf16", "data": "synthetic",
             "config": {"workload": wl_desc if ws == 1 else f"{args.config} weak-scaled: 512x512x{Rz} grid, "
                        "work-balanced z-slabs", "model": f"{c.spec.L}x{c.spec.H} SIREN T-MLP (seeded SIREN init), linear tails",
                        "depth_map": "level-7 sphere-union octree (baked 128^3)" if args.config == "C2" else args.config,
                        "global_points": summ["n_total"], "parallelism": f"dp{ws} (z-slab shards)",
                        "l2": f"inputs {12 * n / 1e9:.2f} GB per rank > 126 MB L2; no flush needed",
                        "full_depth_baseline": bool(args.full_depth)},
-            "roofline": {"bound": "tensor", "kernel": ("k_tmlp_wide (K3 fused T-MLP, CTA pair, N-halves)" if c.spec.H == 336 else "k_tmlp_tc2 (K3 fused T-MLP, CTA pair)"), "achieved": ach,
+            "roofline": {"bound": "alu" if fp32 else "tensor",
+                         "kernel": ("k_query_fp32 (FP32 register-blocked GEMM)" if fp32 else
+                                    "k_tmlp_wide (K3 fused T-MLP, CTA pair, N-halves)" if c.spec.H == 336 else
+                                    "k_tmlp_tc2 (K3 fused T-MLP, CTA pair)"), "achieved": ach,
                          "peak": pk["bf16"], "unit": "TFLOP/s", "frac": ach / pk["bf16"],
-                         "peak_source": pk["src"] + " bf16_tflops (burst)",
-                         "frac_vs_sustained": ach / pk["bf16_sus"], "traffic": _traffic() if args.config == "C2" else None,
+                         "peak_source": pk["src"] + ("" if fp32 else " bf16_tflops (burst)"),
+                         "frac_vs_sustained": ach / pk["bf16_sus"],
+                         "traffic": _traffic() if (args.config == "C2" and not fp32) else None,
                          "algorithmic_flops_per_launch": f_exec_rank0,
                          "flops_formula": "executed H x H FLOPs sum_p (d_p - 1) * 2 H^2 (Eq. 2 reading R3)",
                          "ms_per_launch": ms_mlp,

@@ -44,7 +44,8 @@ typedef enum {
 } sand_status;
 
 /* Arithmetic of the H x H layers.
- *   SAND_FP32  : FP32 SIMT kernels (FFMA, accurate sinf); supported H in {16, 32, 64}.
+ *   SAND_FP32  : FP32 SIMT kernels (FFMA, accurate sinf); supported H in {16, 32, 64} (one thread per
+ *                point) and {128, 256, 336} (register-blocked GEMM over 64-point sub-tiles, L <= 32).
  *                Tolerance vs the oracle: 1e-4 max-abs (BASELINE.json north_star).
  *   SAND_BF16  : tcgen05 tensor cores, BF16 operands, FP32 accumulate in TMEM; layer 1 (K = 3) as a
  *                split-BF16 MMA (x = x_hi + x_lo, relative error ~2^-16) or FP32 SIMT, all tails and

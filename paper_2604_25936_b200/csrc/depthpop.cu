@@ -264,6 +264,86 @@ __global__ void __launch_bounds__(kDpThreads, 1) k_dynamic_pool(MlpDev m, const 
   }
 }
 
+// FP32 adaptive query for wide nets (SAND_FP32 contexts with H >= 128; the one-thread-per-point SIMT
+// kernel keeps H <= 64): the binned 128-row tiles of uniform depth d (K2), each as two 64-point
+// sub-tiles evaluated to layer d with the register-blocked FP32 GEMM above; y_d -> out[perm[row]].
+template <int H, int TAIL>
+__global__ void __launch_bounds__(kDpThreads, 1) k_query_fp32(MlpDev m, const float* __restrict__ w_t,
+                                                              const float* __restrict__ pts,
+                                                              const uint32_t* __restrict__ perm,
+                                                              const QueryMeta* __restrict__ meta,
+                                                              float* __restrict__ out) {
+  using C = DpShape<H>;
+  extern __shared__ __align__(16) float sm[];
+  float* hA = sm;
+  float* hB = hA + C::HP * kDpS;
+  float* ws = hB + C::HP * kDpS;
+  __shared__ float px[3][kDpP];
+  __shared__ float tl[kDpP];
+  __shared__ float yv[kDpP];
+  __shared__ uint32_t idx[kDpP];
+  __shared__ long long s_tile_end[kMaxBins], s_tile_begin[kMaxBins], s_start[kMaxBins], s_count[kMaxBins];
+  const int L = m.L, tid = threadIdx.x;
+  const float w0 = m.omega0;
+  const float4* w1 = reinterpret_cast<const float4*>(m.tables + m.off_w1);
+  const float* bias_t = m.tables + m.off_bias;
+  for (int i = tid; i < 2 * C::KC * C::HP; i += kDpThreads) ws[i] = 0.f;
+  if (tid < kMaxBins) {
+    s_tile_end[tid] = meta->tile_end[tid];
+    s_tile_begin[tid] = meta->tile_begin[tid];
+    s_start[tid] = meta->start[tid];
+    s_count[tid] = meta->count[tid];
+  }
+  __syncthreads();
+  const long long T = meta->total_tiles;
+  for (long long t = blockIdx.x; t < T; t += gridDim.x) {
+    int d = 0;
+    for (int dd = L; dd >= 1; --dd)
+      if (t < s_tile_end[dd]) { d = dd; break; }
+    const long long rend = s_start[d] + s_count[d];
+    for (int sub = 0; sub < kTileM / kDpP; ++sub) {
+      const long long r0 = s_start[d] + (t - s_tile_begin[d]) * kTileM + (long long)sub * kDpP;
+      const int np = (int)min((long long)kDpP, rend - r0);
+      if (np <= 0) break;
+      __syncthreads();
+      if (tid < kDpP) {
+        idx[tid] = tid < np ? perm[r0 + tid] : 0u;
+        yv[tid] = 0.f;
+      }
+      __syncthreads();
+      for (int i = tid; i < 3 * kDpP; i += kDpThreads) {
+        const int p = i / 3, c = i % 3;
+        px[c][p] = p < np ? pts[3ll * idx[p] + c] : 0.f;
+      }
+      __syncthreads();
+      for (int i = tid; i < C::HP * kDpP; i += kDpThreads) {   // layer 1 (K = 3)
+        const int j = i / kDpP, p = i % kDpP;
+        float h = 0.f;
+        if (j < H) {
+          const float4 w = w1[j];
+          h = sinf(fmaf(w.z, px[2][p], fmaf(w.y, px[1][p], fmaf(w.x, px[0][p], w.w))));
+        }
+        hA[j * kDpS + p] = h;
+      }
+      __syncthreads();
+      dp_tails<H, TAIL>(m, 1, hA, tl, tid);
+      __syncthreads();
+      if (tid < kDpP) yv[tid] += tl[tid];
+      float* hin = hA;
+      float* hout = hB;
+      for (int l = 2; l <= d; ++l) {
+        dp_hidden<H>(w_t + (size_t)(l - 2) * H * H, bias_t + (size_t)(l - 2) * H, w0, hin, hout, ws, tid);
+        dp_tails<H, TAIL>(m, l, hout, tl, tid);
+        __syncthreads();
+        if (tid < kDpP) yv[tid] += tl[tid];
+        float* x = hin; hin = hout; hout = x;
+      }
+      __syncthreads();
+      if (tid < np) out[idx[tid]] = yv[tid];
+    }
+  }
+}
+
 // MODE 0: Eq. 5 required depth of every point (full-depth evaluation, decision after layer L).
 // MODE 1: dynamic exit without a depth map ('SAND w/o Octree'; R23): a point stops at
 //   the first layer i >= 2 with |t_i| < r (else L) and returns y_i; a tile stops computing as soon as all
@@ -495,6 +575,32 @@ static cudaError_t launch_pool_t(const MlpDev& m, const float* w_t, const float*
   if (e != cudaSuccess) return e;
   k_dynamic_pool<H, TAIL><<<grid, kDpThreads, sm, st>>>(m, w_t, pts, n, r, out_sdf, out_depth, hbuf);
   return cudaGetLastError();
+}
+
+template <int H, int TAIL>
+static cudaError_t launch_qf_t(const MlpDev& m, const float* w_t, const float* pts, const uint32_t* perm,
+                               const QueryMeta* meta, float* out, int num_sms, cudaStream_t st) {
+  const size_t sm = DpShape<H>::SMEM;
+  cudaError_t e = cudaFuncSetAttribute(k_query_fp32<H, TAIL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  k_query_fp32<H, TAIL><<<num_sms, kDpThreads, sm, st>>>(m, w_t, pts, perm, meta, out);
+  return cudaGetLastError();
+}
+
+bool query_fp32_supported(int H) { return H == 128 || H == 256 || H == 336; }
+
+cudaError_t launch_query_fp32(const MlpDev& m, const float* w_t, const float* pts, const uint32_t* perm,
+                              const QueryMeta* meta, float* out, int num_sms, cudaStream_t st) {
+  const bool mult = m.tail == SAND_TAIL_MULT;
+  switch (m.H) {
+    case 128: return mult ? launch_qf_t<128, 1>(m, w_t, pts, perm, meta, out, num_sms, st)
+                          : launch_qf_t<128, 0>(m, w_t, pts, perm, meta, out, num_sms, st);
+    case 256: return mult ? launch_qf_t<256, 1>(m, w_t, pts, perm, meta, out, num_sms, st)
+                          : launch_qf_t<256, 0>(m, w_t, pts, perm, meta, out, num_sms, st);
+    case 336: return mult ? launch_qf_t<336, 1>(m, w_t, pts, perm, meta, out, num_sms, st)
+                          : launch_qf_t<336, 0>(m, w_t, pts, perm, meta, out, num_sms, st);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 size_t dynamic_scratch_floats(int H, int num_sms) {

@@ -109,7 +109,9 @@ static void dfree(T*& p) {
 }
 
 static bool supported(const sand_config& c) {
-  if (c.prec == SAND_FP32) return simt_supported_H(c.H) && simt_smem_bytes(c.L, c.H, c.tail) <= 232448;
+  if (c.prec == SAND_FP32)
+    return (simt_supported_H(c.H) && simt_smem_bytes(c.L, c.H, c.tail) <= 232448) ||
+           (query_fp32_supported(c.H) && c.L <= 32);
   if (c.prec == SAND_BF16)
     return tc_supported_H(c.H) && (tc2_usable(c.L, c.H, c.tail) || tc3_usable(c.L, c.H, c.tail) ||
                                    tc_smem_bytes(c.L, c.H, c.tail) > 0);
@@ -575,7 +577,9 @@ extern "C" int sand_query(sand_ctx* ctx, const float* d_points, int64_t n, float
                  ctx->d_meta, ctx->d_scan, st));
   CU(launch_scatter(d_depth, n, ctx->cfg.L, ctx->d_offs, ctx->d_perm, nblk, st));
   CU(cudaEventRecord(ev[2], st));
-  if (ctx->cfg.prec == SAND_FP32)
+  if (ctx->cfg.prec == SAND_FP32 && !simt_supported_H(ctx->cfg.H))
+    CU(launch_query_fp32(ctx->mlp, ctx->d_wt_f32, d_points, ctx->d_perm, ctx->d_meta, d_sdf, ctx->num_sms, st));
+  else if (ctx->cfg.prec == SAND_FP32)
     CU(launch_tmlp_simt(ctx->mlp, d_points, ctx->d_perm, ctx->d_meta, d_sdf, ctx->num_sms, st));
   else
     CU(launch_tmlp_tc(ctx->mlp, d_points, ctx->d_perm, ctx->d_meta, d_sdf, ctx->num_sms, st, ctx->use_pair));

@@ -108,6 +108,10 @@ cudaError_t launch_marching_cubes(const float* sdf, int R, int kc0, int kc1, int
 cudaError_t launch_query_dynamic(const MlpDev& m, const float* w_t, const float* pts, long long n, float r,
                                  float* out_sdf, uint8_t* out_depth, float* hbuf, int num_sms, cudaStream_t st);
 size_t dynamic_scratch_floats(int H, int num_sms);
+// FP32 adaptive query for H in {128, 256, 336} (binned 128-row tiles; depthpop.cu)
+bool query_fp32_supported(int H);
+cudaError_t launch_query_fp32(const MlpDev& m, const float* w_t, const float* pts, const uint32_t* perm,
+                              const QueryMeta* meta, float* out, int num_sms, cudaStream_t st);
 cudaError_t launch_required_depth(const MlpDev& m, const float* w_t, const float* pts, long long n, float r,
                                   int near, uint8_t* out, int num_sms, cudaStream_t st);
 cudaError_t launch_leaf_max(const uint8_t* d, long long n_leaves, int spl, uint8_t* out, cudaStream_t st);

@@ -344,7 +344,7 @@ cudaError_t launch_tmlp_tc(const MlpDev& m, const float* pts, const uint32_t* pe
 cudaError_t prepare_simt(int L, int H, int tail);
 
 cudaError_t prepare_tmlp_kernels(int L, int H, int tail, int prec) {
-  if (prec == SAND_FP32) return prepare_simt(L, H, tail);
+  if (prec == SAND_FP32) return simt_supported_H(H) ? prepare_simt(L, H, tail) : cudaSuccess;   // wide: launch-time
   const bool mult = tail == SAND_TAIL_MULT;
   if (tc2_available(H)) {
     const cudaError_t e = prepare_tc2(H, tail);

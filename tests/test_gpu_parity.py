@@ -57,7 +57,7 @@ def test_bf16_wide_pair_kernel(L):
     assert_parity(sdf, dep, sdf_or, dep_or, TOL_BF16)
 
 
-@pytest.mark.parametrize("H", [16, 32, 64])
+@pytest.mark.parametrize("H", [16, 32, 64, 128, 256, 336])
 @pytest.mark.parametrize("tail", [0, 1])
 def test_fp32_random_depths_small(H, tail):
     L = 4
@@ -65,6 +65,19 @@ def test_fp32_random_depths_small(H, tail):
     p = g.make_weights(spec)
     dm = _random_voxel_map(4, L, 3)
     pts = _pts(5003, 4)
+    with make_ctx(spec, FP32) as ctx:
+        sdf, dep = run_engine(ctx, p, dm, pts)
+    sdf_or, dep_or = oracle.query(p, dm, pts)
+    assert_parity(sdf, dep, sdf_or, dep_or, TOL_FP32)
+
+
+def test_fp32_wide_deep_net():
+    """SAND_FP32 with an 8x256 net (the register-blocked FP32 query kernel for wide nets): all depths
+    1..8 over many binned 128-row tiles (two 64-point sub-tiles each) with ragged ends, 1e-4 parity."""
+    spec = g.TMlpSpec(L=8, H=256, omega0=30.0, tail=0, seed=17)
+    p = g.make_weights(spec)
+    dm = _random_voxel_map(4, 8, 5)
+    pts = _pts(40011, 6)
     with make_ctx(spec, FP32) as ctx:
         sdf, dep = run_engine(ctx, p, dm, pts)
     sdf_or, dep_or = oracle.query(p, dm, pts)
