@@ -10,23 +10,24 @@
 //   output    : sdf[perm[row]] = y_d = sum_{l <= d} t_l (Eq. 2).
 //
 // Warp roles (per CTA of the pair; "leader" = even CTA):
-//   warp 0       weight producer: this CTA's half (H/2 rows) of every 64-wide K-chunk of W_l (l >= 2),
-//                bulk async copy (TMA engine) into an NST-stage ring (w_full / w_empty mbarriers)
-//   warp 1       leader: tcgen05.mma.cta_group::2 issuer; odd CTA: relays "my half landed" (w_peer)
-//   warp 2       TMEM allocator (2 accumulator slots x H columns)
-//   warp 3       IO: all global traffic of the tile rows -- gathers perm -> points, writes the split-BF16
+//   warp 0       weight producer (lane 0): this CTA's half (H/2 rows) of W_l (l >= 2), 2 K-chunks per bulk
+//                async copy (TMA engine) into an NST-stage ring (w_full / w_empty mbarriers)
+//   warp 1       TMEM allocator (2 accumulator slots x H columns); leader: the tcgen05.mma.cta_group::2
+//                issuer (converged warp, one elected lane issues 4 K-steps per asm block); odd CTA: relays
+//                "my half landed" (w_peer)
+//   warp 2       IO: all global traffic of the tile rows -- gathers perm -> points, writes the split-BF16
 //                layer-1 A operand (a1_full), drains finished tiles (partials + csum -> sdf[perm[row]])
-//   warps 4..19  16 epilogue warps = 4 TMEM lane quadrants x 4 column quarters.  All of them work on one
+//   warps 3..18  16 epilogue warps = 4 TMEM lane quadrants x 4 column quarters.  All of them work on one
 //                tile slot at a time, alternating slot 0 / slot 1 step by step, so the MMA of one slot
 //                overlaps the epilogue of the other (ping-pong).  A step = one layer of one slot.  They
 //                issue no global memory operations (their proxy fence never waits on DRAM).
 // Every role walks the same deterministic step sequence (rounds: slot 0 then slot 1; a slot's steps are
 // its tiles' layers 1..d).  The MMA order equals the epilogue order, so the ping-pong cannot deadlock.
 //
-// Sine split: of every 16 accumulator columns the first NP go through an odd
-// degree-7 polynomial on the FMA pipe (range reduction to [-pi/2, pi/2] by a magic-number round), the
-// rest through MUFU.SIN, so MUFU and FMA pipes share the transcendental load.  Bias tables are
-// pre-scaled on the host for the path their column takes (w0 or w0/(2 pi)).
+// Sine: MUFU.SIN (__sinf) by default.  A compile-time share NP of every 32 output columns can instead use
+// an odd degree-9 polynomial on the FMA pipe after a magic-number range reduction (SAND_NPOLY = 8 / 16,
+// H = 256 LINEAR builds; measured slower).  Bias tables are pre-scaled on the host for the
+// path their column takes (w0 or w0/(2 pi)).
 //
 // Tails: LINEAR tails sum linearly over layers, so every thread keeps a running partial over its columns;
 // the IO warp adds the four column quarters of a row and the tail-bias prefix sum csum[d] once per tile.
