@@ -248,6 +248,31 @@ def test_determinism_and_host_e2e():
             np.testing.assert_array_equal(hd.numpy(), d1)
 
 
+def test_shard_invariance_of_the_multi_gpu_partition():
+    """SURVEY 8(e) pin: the z-slab shards of partition.shard_planes (world = 1, 2, 4, 8), each queried on
+    its own as a rank would, reproduce the single-query SDF and exit depths bit for bit (per-point math
+    does not depend on tile mates)."""
+    import torch
+    from paper_2604_25936_b200 import partition
+    c = g.make_config("C1")
+    p = c.params()
+    R = c.grid_R
+    pts = g.grid_points(R)
+    with make_ctx(c.spec, BF16) as ctx:
+        s_all, d_all = run_engine(ctx, p, c.depthmap, pts)
+        for world in (2, 4, 8):
+            s_sh = np.empty_like(s_all)
+            d_sh = np.empty_like(d_all)
+            for rank in range(world):
+                k0, k1, _ = partition.shard_planes(c.depthmap, R, world, rank, weak=False)
+                sl = slice(k0 * R * R, k1 * R * R)
+                sdf, dep = ctx.query_tensor(torch.from_numpy(np.ascontiguousarray(pts[sl])).cuda())
+                torch.cuda.synchronize()
+                s_sh[sl], d_sh[sl] = sdf.cpu().numpy(), dep.cpu().numpy()
+            np.testing.assert_array_equal(d_sh, d_all)
+            np.testing.assert_array_equal(s_sh, s_all)
+
+
 def test_all_max_depth_equals_full_depth():
     """BJ oracle check 2 on the GPU: an all-L map == uniform full-depth evaluation (query_full)."""
     L = 8
