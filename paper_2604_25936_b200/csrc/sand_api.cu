@@ -483,15 +483,17 @@ extern "C" int sand_load_depthmap(sand_ctx* ctx, const sand_depthmap* dm) {
       const size_t nc = (size_t)1 << (3 * dm->level);
       CU(cudaMalloc(&ctx->d_grid, nc));
       if (dm->far_sdf) CU(cudaMalloc(&ctx->d_grid_far, nc * 4));
-      int* d_err = nullptr;
-      CU(cudaMalloc(&d_err, 4));
-      CU(cudaMemset(d_err, 0, 4));
+      struct DevFlag {   // freed on every return path
+        int* p = nullptr;
+        ~DevFlag() { if (p) cudaFree(p); }
+      } err;
+      CU(cudaMalloc(&err.p, 4));
+      CU(cudaMemset(err.p, 0, 4));
       CU(launch_bake_octree(ctx->d_nodes, ctx->d_leaf_depth, ctx->d_leaf_far, dm->level, ctx->d_grid,
-                            ctx->d_grid_far, d_err, ctx->stream));
+                            ctx->d_grid_far, err.p, ctx->stream));
       int herr = 0;
-      CU(cudaMemcpyAsync(&herr, d_err, 4, cudaMemcpyDeviceToHost, ctx->stream));
+      CU(cudaMemcpyAsync(&herr, err.p, 4, cudaMemcpyDeviceToHost, ctx->stream));
       CU(cudaStreamSynchronize(ctx->stream));
-      cudaFree(d_err);
       if (herr) return fail(ctx, SAND_ERR_DEPTHMAP, "octree bake failed (descent exceeded level)");
       lp.dense = 1;
     } else {
