@@ -63,11 +63,13 @@ __device__ __forceinline__ void dp_hidden(const float* W, const float* bias, flo
                                           float* ws, int tid) {
   using C = DpShape<H>;
   const int tj = tid & 31, tp = tid >> 5;
-  float acc[kDpPPW][C::U];
+  // accumulators for point pairs: one FFMA2 does two points' FMA of the same weight (half the issue slots
+  // of scalar FFMA for the same FMA-pipe work)
+  float2 acc[kDpPPW / 2][C::U];
 #pragma unroll
-  for (int a = 0; a < kDpPPW; ++a)
+  for (int a = 0; a < kDpPPW / 2; ++a)
 #pragma unroll
-    for (int u = 0; u < C::U; ++u) acc[a][u] = 0.f;
+    for (int u = 0; u < C::U; ++u) acc[a][u] = make_float2(0.f, 0.f);
   __syncthreads();   // previous users of both stage buffers are done
   dp_stage<H>(ws, W, 0, 0, tid);
   for (int k0 = 0, b = 0; k0 < H; k0 += C::KC, b ^= 1) {
@@ -81,17 +83,19 @@ __device__ __forceinline__ void dp_hidden(const float* W, const float* bias, flo
     const float* wsb = ws + b * C::KC * C::HP;
 #pragma unroll 4
     for (int kk = 0; kk < C::KC; ++kk) {
-      float hv[kDpPPW];
+      float2 hv[kDpPPW / 2];
 #pragma unroll
       for (int q4 = 0; q4 < kDpPPW / 4; ++q4) {
         const float4 hq = *reinterpret_cast<const float4*>(hin + (k0 + kk) * kDpS + tp * kDpPPW + 4 * q4);
-        hv[4 * q4] = hq.x; hv[4 * q4 + 1] = hq.y; hv[4 * q4 + 2] = hq.z; hv[4 * q4 + 3] = hq.w;
+        hv[2 * q4] = make_float2(hq.x, hq.y);
+        hv[2 * q4 + 1] = make_float2(hq.z, hq.w);
       }
 #pragma unroll
       for (int u = 0; u < C::U; ++u) {
         const float w = wsb[kk * C::HP + tj + 32 * u];
+        const float2 w2 = make_float2(w, w);
 #pragma unroll
-        for (int a = 0; a < kDpPPW; ++a) acc[a][u] = fmaf(w, hv[a], acc[a][u]);
+        for (int a = 0; a < kDpPPW / 2; ++a) acc[a][u] = __ffma2_rn(w2, hv[a], acc[a][u]);
       }
     }
     __syncthreads();   // stage b is overwritten by the copy issued next iteration
@@ -101,7 +105,10 @@ __device__ __forceinline__ void dp_hidden(const float* W, const float* bias, flo
     const int j = tj + 32 * u;
     const float bb = j < H ? bias[j] : 0.f;
 #pragma unroll
-    for (int a = 0; a < kDpPPW; ++a) hout[j * kDpS + tp * kDpPPW + a] = j < H ? sinf(fmaf(acc[a][u], w0, bb)) : 0.f;
+    for (int a = 0; a < kDpPPW / 2; ++a) {
+      hout[j * kDpS + tp * kDpPPW + 2 * a] = j < H ? sinf(fmaf(acc[a][u].x, w0, bb)) : 0.f;
+      hout[j * kDpS + tp * kDpPPW + 2 * a + 1] = j < H ? sinf(fmaf(acc[a][u].y, w0, bb)) : 0.f;
+    }
   }
   __syncthreads();
 }
@@ -374,15 +381,6 @@ __global__ void __launch_bounds__(kDpThreads, 1) k_required_depth(MlpDev m, cons
   const long long ntiles = (n + kDpP - 1) / kDpP;
   for (int i = tid; i < 2 * C::KC * C::HP; i += kDpThreads) ws[i] = 0.f;
   __syncthreads();
-  // W^T rows [k0, k0 + C::KC) of layer matrix W -> stage buffer b (H % 16 == 0: rows are whole float4s)
-  auto stage = [&](const float* W, int k0, int b) {
-    constexpr int RV = H / 4;   // float4 per row
-    for (int i = tid; i < C::KC * RV; i += kDpThreads) {
-      const int kk = i / RV, j4 = i % RV;
-      cp_async16(ws + (b * C::KC + kk) * C::HP + 4 * j4, W + (size_t)(k0 + kk) * H + 4 * j4);
-    }
-    cp_async_commit();
-  };
   for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const long long p0 = tile * kDpP;
     for (int i = tid; i < 3 * kDpP; i += kDpThreads) {
@@ -431,50 +429,7 @@ __global__ void __launch_bounds__(kDpThreads, 1) k_required_depth(MlpDev m, cons
     float* hin = hA;
     float* hout = hB;
     for (int l = 2; l <= L; ++l) {
-      const float* W = w_t + (size_t)(l - 2) * H * H;   // W^T [k][j]
-      float acc[kDpPPW][C::U];
-#pragma unroll
-      for (int a = 0; a < kDpPPW; ++a)
-#pragma unroll
-        for (int u = 0; u < C::U; ++u) acc[a][u] = 0.f;
-      // W^T streamed through two shared-memory stages: the copy of rows k0 + 16 .. overlaps the FMAs on
-      // rows k0 .. (cp.async, no register staging)
-      __syncthreads();   // previous users of both stage buffers are done
-      stage(W, 0, 0);
-      for (int k0 = 0, b = 0; k0 < H; k0 += C::KC, b ^= 1) {
-        if (k0 + C::KC < H) {
-          stage(W, k0 + C::KC, b ^ 1);
-          cp_async_wait<1>();
-        } else {
-          cp_async_wait<0>();
-        }
-        __syncthreads();
-        const float* wsb = ws + b * C::KC * C::HP;
-#pragma unroll 4
-        for (int kk = 0; kk < C::KC; ++kk) {
-          float hv[kDpPPW];
-#pragma unroll
-          for (int q4 = 0; q4 < kDpPPW / 4; ++q4) {
-            const float4 hq = *reinterpret_cast<const float4*>(hin + (k0 + kk) * kDpS + tp * kDpPPW + 4 * q4);
-            hv[4 * q4] = hq.x; hv[4 * q4 + 1] = hq.y; hv[4 * q4 + 2] = hq.z; hv[4 * q4 + 3] = hq.w;
-          }
-#pragma unroll
-          for (int u = 0; u < C::U; ++u) {
-            const float w = wsb[kk * C::HP + tj + 32 * u];
-#pragma unroll
-            for (int a = 0; a < kDpPPW; ++a) acc[a][u] = fmaf(w, hv[a], acc[a][u]);
-          }
-        }
-        __syncthreads();   // stage b is overwritten by the copy issued next iteration
-      }
-#pragma unroll
-      for (int u = 0; u < C::U; ++u) {
-        const int j = tj + 32 * u;
-        const float b = j < H ? bias_t[(l - 2) * H + j] : 0.f;
-#pragma unroll
-        for (int a = 0; a < kDpPPW; ++a) hout[j * kDpS + tp * kDpPPW + a] = j < H ? sinf(fmaf(acc[a][u], w0, b)) : 0.f;
-      }
-      __syncthreads();
+      dp_hidden<H>(w_t + (size_t)(l - 2) * H * H, bias_t + (size_t)(l - 2) * H, w0, hin, hout, ws, tid);
       tails(l, hout);
       float* t = hin; hin = hout; hout = t;
       if (MODE == 1 && l < L) {
