@@ -44,7 +44,8 @@ typedef enum {
 } sand_status;
 
 /* Arithmetic of the H x H layers.
- *   SAND_FP32  : FP32 SIMT kernels (FFMA, accurate sinf); supported H in {16, 32, 64} (one thread per
+ *   SAND_FP32  : FP32 SIMT kernels (FFMA; sine to ~5e-7: libm sinf for H <= 64, Cody-Waite reduction +
+ *                MUFU.SIN for wider nets); supported H in {16, 32, 64} (one thread per
  *                point) and {128, 256, 336} (register-blocked GEMM over 64-point sub-tiles, L <= 32).
  *                Tolerance vs the oracle: 1e-4 max-abs (BASELINE.json north_star).
  *   SAND_BF16  : tcgen05 tensor cores, BF16 operands, FP32 accumulate in TMEM; layer 1 (K = 3) as a
@@ -162,7 +163,8 @@ int sand_debug_perm(sand_ctx* ctx, uint32_t* host_perm, int64_t cap, int64_t* n_
 
 /* ---------------------------------------------------------------------------------------------------
  * Volumetric network-depth map population (the step before the query path; Sec. 3.2).
- * Both calls evaluate the full L-layer T-MLP in FP32 (accurate sine) whatever ctx's precision, because
+ * Both calls evaluate the full L-layer T-MLP in FP32 (sine to ~5e-7: Cody-Waite reduction to [-pi, pi],
+ * then MUFU.SIN) whatever ctx's precision, because
  * Eq. 5 compares cumulative outputs against r (1.5e-4 in the paper).  Only the weights must be
  * loaded.  Asynchronous on ctx's stream.  Errors: SAND_ERR_ARG, SAND_ERR_STATE, SAND_ERR_UNSUPPORTED
  * (H not in {16, 32, 64, 128, 256, 336}), SAND_ERR_CUDA, SAND_ERR_OOM.                              */
@@ -187,7 +189,7 @@ int sand_populate_leaf_depths(sand_ctx* ctx, const float* d_samples, int64_t n_l
  * layer i >= 2 whose residual |t_i| < r (reading R23: t_1 = y_1 is the first prediction, not
  * a residual), else at L:
  *   d_out_exit_depth[p] = that layer (255 for a non-finite point),  d_out_sdf[p] = y_d (NaN if 255).
- * FP32 (accurate sine) like the population calls above.  Default schedule: a 64-point tile stops as
+ * FP32 (sine to ~5e-7) like the population calls above.  Default schedule: a 64-point tile stops as
  * soon as all of its points have stopped; with the environment variable SAND_DYN_POOL=1 (read per call)
  * pools of 512 points are re-compacted after every layer instead.  Only the weights must be loaded; the depth map
  * and LOD cap are ignored.  Asynchronous on ctx's stream.  Errors: SAND_ERR_ARG (n < 0, r < 0 or NaN,

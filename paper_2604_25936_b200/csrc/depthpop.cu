@@ -6,7 +6,7 @@
 // and the leaf depth (Eq. 6) d(N) = max over the leaf's sample points of d(x).
 //
 // Eq. 5 compares cumulative outputs against r (1.5e-4 in the paper), far below the BF16 path's
-// error, so the full-depth evaluation here is FP32 (accurate sinf), whatever the context's precision.
+// error, so the full-depth evaluation here is FP32 (sine to ~5e-7, dp_sin), whatever the context's precision.
 // k_required_depth: persistent blocks of 256 threads over tiles of 64 points; every layer is a register-
 // blocked FP32 GEMM (thread = 8 points x ceil(H/32) units, W^T double-buffered in shared memory by cp.async, 16 rows at a
 // time, activations transposed [unit][point] in shared memory) with the sine, tail and running y_i
@@ -42,6 +42,16 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// sin(x) to ~4e-7 absolute: two-constant Cody-Waite reduction to [-pi, pi] (k = rint(x / 2pi),
+// 2pi = hi + lo with hi = fl32(2pi)), then MUFU.SIN, whose error on [-pi, pi] is ~2^-21.4 -- FP32-grade
+// for the |x| <~ 100 of a SIREN layer, at a quarter of the instructions of the libm sinf path.
+__device__ __forceinline__ float dp_sin(float x) {
+  const float k = rintf(x * 0.159154943091895f);
+  float r = fmaf(-k, 6.28318548202514648f, x);
+  r = fmaf(-k, -1.7484555314695172e-7f, r);
+  return __sinf(r);
+}
 
 // ---- building blocks shared by the kernels below (one 64-point tile, activations [unit][point])
 // W^T rows [k0, k0 + KC) of a layer -> stage buffer b (H % 16 == 0: rows are whole float4s)
@@ -106,8 +116,8 @@ __device__ __forceinline__ void dp_hidden(const float* W, const float* bias, flo
     const float bb = j < H ? bias[j] : 0.f;
 #pragma unroll
     for (int a = 0; a < kDpPPW / 2; ++a) {
-      hout[j * kDpS + tp * kDpPPW + 2 * a] = j < H ? sinf(fmaf(acc[a][u].x, w0, bb)) : 0.f;
-      hout[j * kDpS + tp * kDpPPW + 2 * a + 1] = j < H ? sinf(fmaf(acc[a][u].y, w0, bb)) : 0.f;
+      hout[j * kDpS + tp * kDpPPW + 2 * a] = j < H ? dp_sin(fmaf(acc[a][u].x, w0, bb)) : 0.f;
+      hout[j * kDpS + tp * kDpPPW + 2 * a + 1] = j < H ? dp_sin(fmaf(acc[a][u].y, w0, bb)) : 0.f;
     }
   }
   __syncthreads();
@@ -216,7 +226,7 @@ __global__ void __launch_bounds__(kDpThreads, 1) k_dynamic_pool(MlpDev m, const 
             float h = 0.f;
             if (j < H) {
               const float4 w = w1[j];
-              h = sinf(fmaf(w.z, px[2][p], fmaf(w.y, px[1][p], fmaf(w.x, px[0][p], w.w))));
+              h = dp_sin(fmaf(w.z, px[2][p], fmaf(w.y, px[1][p], fmaf(w.x, px[0][p], w.w))));
             }
             hB[j * kDpS + p] = h;
           }
@@ -328,7 +338,7 @@ __global__ void __launch_bounds__(kDpThreads, 1) k_query_fp32(MlpDev m, const fl
         float h = 0.f;
         if (j < H) {
           const float4 w = w1[j];
-          h = sinf(fmaf(w.z, px[2][p], fmaf(w.y, px[1][p], fmaf(w.x, px[0][p], w.w))));
+          h = dp_sin(fmaf(w.z, px[2][p], fmaf(w.y, px[1][p], fmaf(w.x, px[0][p], w.w))));
         }
         hA[j * kDpS + p] = h;
       }
@@ -396,7 +406,7 @@ __global__ void __launch_bounds__(kDpThreads, 1) k_required_depth(MlpDev m, cons
       float h = 0.f;
       if (j < H) {
         const float4 w = w1[j];
-        h = sinf(fmaf(w.z, px[2][p], fmaf(w.y, px[1][p], fmaf(w.x, px[0][p], w.w))));
+        h = dp_sin(fmaf(w.z, px[2][p], fmaf(w.y, px[1][p], fmaf(w.x, px[0][p], w.w))));
       }
       hA[j * kDpS + p] = h;
     }
