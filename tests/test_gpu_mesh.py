@@ -120,3 +120,26 @@ def test_fused_mesh_equals_unfused(slab):
         assert max(directed.values()) == 1
         on_face = lambda v: np.any(np.abs(np.abs(np.array(v)) - 1.0) < 1e-6)
         assert all(on_face(u) and on_face(v) for (u, v) in directed if (v, u) not in directed)
+
+
+def test_edge_grids_match_oracle():
+    """R = 2 (one cube) for every one of the 256 corner configurations, and a plane through grid vertices
+    (sdf exactly 0 at vertices: strict 'inside iff sdf < 0')."""
+    import torch
+    spec = g.TMlpSpec(L=2, H=64, omega0=30.0, seed=1)
+    with make_ctx(spec, 2) as ctx:
+        vals = np.array([-0.75, 0.5], np.float32)
+        for case in range(256):
+            sdf = np.array([vals[(case >> v) & 1 ^ 1] for v in range(8)], np.float32)   # bit v set -> inside
+            T = _gpu_mc(ctx, sdf, 2)
+            To = oracle.marching_cubes(sdf.astype(np.float64), 2)
+            assert T.shape == To.shape, case
+            if len(T):
+                np.testing.assert_allclose(_canon(T), _canon(To), rtol=0, atol=1e-6)
+        R = 9
+        X, Y, Z = _grid(R)
+        sdf = (X - X[0, 0, 4]).astype(np.float32).ravel()     # zero exactly on the plane of vertex column 4
+        T = _gpu_mc(ctx, sdf, R)
+        To = oracle.marching_cubes(sdf.astype(np.float64), R)
+        assert T.shape == To.shape
+        np.testing.assert_allclose(_canon(T), _canon(To), rtol=0, atol=1e-6)
