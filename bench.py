@@ -143,6 +143,18 @@ def _traffic():
         return None
 
 
+def _sine_roofline(per_depth, H, ms_mlp, clocks):
+    """K3's second bound: sum_p d_p * H sines per launch against MUFU.SIN at 16 / clk / SM (4 per SMSP;
+    scripts/micro/epi2.cu measures 15.3 elements / clk / SM for the sine + tail + BF16-pack chain)."""
+    sm_mhz = (clocks or {}).get("sm_mhz") or 1965.0
+    sines = float(sum(c * d * H for d, c in enumerate(per_depth)))
+    ach = sines / (ms_mlp / 1e3) / 1e9
+    peak = 148 * 16 * sm_mhz * 1e6 / 1e9
+    return {"bound": "alu", "kernel": "K3 epilogue (MUFU.SIN)", "achieved": ach, "peak": peak, "unit": "Gsin/s",
+            "frac": ach / peak, "sines_per_launch": sines,
+            "peak_source": "derived: 148 SM x 16 MUFU.SIN / clk x median SM clock (DESIGN.md, K3 per-SM budget)"}
+
+
 def _cores():
     try:
         from threadpoolctl import threadpool_info
@@ -631,6 +643,8 @@ def main():
                          "flops_formula": "executed H x H FLOPs sum_p (d_p - 1) * 2 H^2 (Eq. 2 reading R3)",
                          "ms_per_launch": ms_mlp,
                          "traffic_source": "profiles/r01_k3_traffic.json (ncu --set full, dram read+write per launch)"},
+            # the other pipe the step needs: one sine per hidden unit per evaluated layer (Eq. 2), MUFU.SIN
+            "sine_roofline": None if fp32 else _sine_roofline(st["per_depth"], H, ms_mlp, clocks),
             "tensor_frac_step": f_exec / (ms_step / 1e3) / 1e12 / pk["bf16"],
             "tensor_frac_ns_formula": f_ns / (ms_step / 1e3) / 1e12 / pk["bf16"],
             "flops_exec_per_step": f_exec, "flops_ns_per_step": f_ns,
