@@ -155,6 +155,16 @@ def _sine_roofline(per_depth, H, ms_mlp, clocks):
             "peak_source": "derived: 148 SM x 16 MUFU.SIN / clk x median SM clock (DESIGN.md, K3 per-SM budget)"}
 
 
+def _padding_waste(per_depth, H, fp32):
+    """Fraction of the H x H tensor FLOPs K3 executes that pad: ragged last tile per depth bucket (256-row
+    pair tiles, 128-row otherwise) and, for H = 336, the width padded to 352 (zero weights)."""
+    T = 128 if fp32 else 256
+    HP = (H + 31) // 32 * 32 if H > 256 and not fp32 else H
+    alg = sum(c * (d - 1) * 2.0 * H * H for d, c in enumerate(per_depth) if d >= 1)
+    ex = sum(-(-c // T) * T * (d - 1) * 2.0 * HP * HP for d, c in enumerate(per_depth) if d >= 1)
+    return {"tile_rows": T, "padded_width": HP, "executed_flops": ex, "waste_frac": 1.0 - alg / ex if ex else 0.0}
+
+
 def _cores():
     try:
         from threadpoolctl import threadpool_info
@@ -648,6 +658,7 @@ def main():
             "tensor_frac_step": f_exec / (ms_step / 1e3) / 1e12 / pk["bf16"],
             "tensor_frac_ns_formula": f_ns / (ms_step / 1e3) / 1e12 / pk["bf16"],
             "flops_exec_per_step": f_exec, "flops_ns_per_step": f_ns,
+            "padding_waste": _padding_waste(st["per_depth"], H, fp32),
             "stage_ms": {"lookup": ms_lookup, "bin": ms_bin, "mlp": ms_mlp},
             "per_depth": per_depth,
             "e2e": e2e, "cpu_baseline": cpu,
