@@ -1,0 +1,38 @@
+"""bench.py's host-side accounting (no GPU): the padding-waste and sine-roofline figures it prints are
+checked against hand counts, so a wrong tile size, padded width or layer count in them fails here."""
+import os
+import sys
+
+import pytest
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+
+
+def test_padding_waste_hand_counts():
+    # 512 depth-2 points and 256 depth-3 points fill whole 256-row tiles: nothing padded at H = 256
+    w = bench._padding_waste([7, 0, 512, 256], 256, False)
+    assert w["tile_rows"] == 256 and w["padded_width"] == 256
+    assert w["waste_frac"] == 0.0
+    # depth-1 points carry no H x H layer, so they never count; 1 depth-2 point pads a 256-row tile
+    w = bench._padding_waste([0, 1000, 1], 256, False)
+    assert w["executed_flops"] == 256 * 2.0 * 256 * 256
+    assert w["waste_frac"] == pytest.approx(255 / 256)
+    # H = 336 runs at the padded width 352 (zero weights): waste 1 - (336/352)^2 on full tiles
+    w = bench._padding_waste([0, 0, 256], 336, False)
+    assert w["padded_width"] == 352
+    assert w["waste_frac"] == pytest.approx(1 - (336 / 352) ** 2)
+    # the FP32 path: 128-row tiles, no width padding
+    w = bench._padding_waste([0, 0, 129], 336, True)
+    assert (w["tile_rows"], w["padded_width"]) == (128, 336)
+    assert w["waste_frac"] == pytest.approx(1 - 129 / 256)
+
+
+def test_sine_roofline_counts_every_evaluated_layer():
+    # Eq. 2: a depth-d point evaluates sin on H units in each of its d layers (layer 1 included);
+    # depth-0 points (cached far-field SDF) evaluate none
+    r = bench._sine_roofline([5, 10, 20, 0, 1], 64, 2.0, {"sm_mhz": 1000.0})
+    assert r["sines_per_launch"] == (10 * 1 + 20 * 2 + 1 * 4) * 64
+    assert r["achieved"] == pytest.approx(r["sines_per_launch"] / 2e-3 / 1e9)
+    assert r["peak"] == pytest.approx(148 * 16 * 1e9 / 1e9)
+    assert r["frac"] == pytest.approx(r["achieved"] / r["peak"])
