@@ -21,6 +21,8 @@
 //                tile slot at a time, alternating slot 0 / slot 1 step by step, so the MMA of one slot
 //                overlaps the epilogue of the other (ping-pong).  A step = one layer of one slot.  They
 //                issue no global memory operations (their proxy fence never waits on DRAM).
+//                (Compile-time SAND_EPI5=1 at H = 256: 20 warps in 5 column groups of 7/7/6/6/6 8-column
+//                chunks at 80 registers -- measured 3% slower.)
 // Every role walks the same deterministic step sequence (rounds: slot 0 then slot 1; a slot's steps are
 // its tiles' layers 1..d).  The MMA order equals the epilogue order, so the ping-pong cannot deadlock.
 //
@@ -39,6 +41,9 @@
 
 #include "ptx.cuh"
 
+#ifndef SAND_EPI5
+#define SAND_EPI5 0
+#endif
 #ifndef SAND_DIAG
 #define SAND_DIAG 0   // 1: diagnostic modes SAND_KPROF=2/3 (timing studies; build with SAND_BUILD_DEFS=-DSAND_DIAG=1)
 #endif
@@ -66,7 +71,10 @@ struct Tc2Shape {
   static constexpr int HQ = H / 4;                 // columns per epilogue thread (column quarter)
   static constexpr int NG = HQ / 16;               // 16-column TMEM load groups per thread
   static constexpr int TMEM_COLS = 2 * H <= 128 ? 128 : (2 * H <= 256 ? 256 : 512);
-  static constexpr int THREADS = 96 + 512;      // 3 control warps + 16 epilogue warps
+  // epilogue column groups: 4 (16 warps) or, with SAND_EPI5 at H = 256, 5 (20 warps, 7/7/6/6/6 chunks of
+  // 8 columns, 88 registers per thread)
+  static constexpr int NGRP = (H == 256 && SAND_EPI5) ? 5 : 4;
+  static constexpr int THREADS = 96 + 128 * NGRP;   // 3 control warps + 4 NGRP epilogue warps
   static constexpr int TILE = 256;
   static_assert(H % 64 == 0 && H <= 256 && HQ % 16 == 0, "CTA-pair kernel: H in {64, 128, 192, 256}");
 };
@@ -172,10 +180,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
   const uint32_t sA1 = sW1 + C::W1_HALF;                          // [slot] layer-1 A operand
   float* tab = reinterpret_cast<float*>(gbase + ((sA1 + NSLOT * C::A1_BYTES) - base));
   const long long ntab = p.m.pt_floats;
-  constexpr int NPL = TAIL == SAND_TAIL_MULT ? 5 : 4;   // partial planes: 4 column quarters (+ Eq. 3 products)
+  constexpr int NGRP = C::NGRP;
+  constexpr int NPL = TAIL == SAND_TAIL_MULT ? NGRP + 1 : NGRP;   // partial planes: column groups (+ Eq. 3 products)
   float* part = tab + ((ntab + 3) & ~3ll);                        // [slot][plane][128] tile-end partials
   float2* red2 = reinterpret_cast<float2*>(part + NSLOT * NPL * 128);   // MULT: [slot][kpar][cq][128]
-  const int red2_floats = (TAIL == SAND_TAIL_MULT) ? NSLOT * 2 * 4 * 128 * 2 : 0;
+  const int red2_floats = (TAIL == SAND_TAIL_MULT) ? NSLOT * 2 * NGRP * 128 * 2 : 0;
   const int nb = L + 2;
   long long* meta_s = reinterpret_cast<long long*>(part + NSLOT * NPL * 128 + red2_floats);
   long long* s_tile_end = meta_s;
@@ -216,7 +225,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
     }
     fence_proxy_async_smem();   // W1 (generic stores) -> tensor core (async proxy)
   }
-  constexpr uint32_t kEpiWarps = 16;
+  constexpr uint32_t kEpiWarps = 4 * NGRP;
   if (tid == 0) {
     for (int i = 0; i < nst; ++i) {
       mbar_init(b_wfull + 8 * i, 1);
@@ -432,8 +441,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const int r = lane + 32 * k;
-          y[k] = cs + pl[r] + pl[128 + r] + pl[256 + r] + pl[384 + r];
-          if (NPL == 5) y[k] += pl[512 + r];
+          float v = cs;
+#pragma unroll
+          for (int g = 0; g < NPL; ++g) v += pl[128 * g + r];
+          y[k] = v;
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(b_partfree + 8 * s);
@@ -456,15 +467,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
     // =========================== epilogue (16 warps, both slots, step by step)
     const int ew = warp - 3;
     const int q = warp & 3;                  // TMEM lane quadrant = warp % 4
-    const int cq = ew >> 2;                  // column quarter
+    const int cq = ew >> 2;                  // column group (quarter when NGRP = 4)
     // TMEM access in the 16x256b shape: thread (quad = lane / 4, tq = lane % 4) owns rows
     // R_k = 32q + quad + 8k (k = 0..3) and, in every 8-column chunk, columns 2 tq and 2 tq + 1.  Each
     // per-column table value it loads serves 4 rows (4x fewer shared-memory table reads than one row per
     // thread), at the price of 4-byte A-operand stores.
     const int quad = lane >> 2, tq = lane & 3;
-    const int c0 = cq * C::HQ;
+    constexpr int NCHB = H / 8 / NGRP, NCHX = H / 8 % NGRP;   // chunks per group: NCHB (+1 for the first NCHX)
+    const int c0 = 8 * (cq * NCHB + (cq < NCHX ? cq : NCHX));
     constexpr int BW = 16;                        // columns per TMEM load batch (2 x 8 registers)
     constexpr int CB = BW / 8;                    // 8-column chunks per batch
+    static_assert(NCHB % CB == 0, "whole TMEM load batches per group");
     const uint32_t tm_q = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)c0;
     const uint32_t a_st = sA + (uint32_t)(4 * q + (lane >> 3)) * 1024 + (uint32_t)(lane & 7) * 128;
     const float2 SM2 = make_float2(p.m.omega0, p.m.omega0);
@@ -509,76 +522,86 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
       const float* a1 = ta1 + (l - 2) * H + c0 + 2 * tq;
       const bool prod = TAIL == SAND_TAIL_MULT && l >= 2;
       const uint32_t tm = tm_q + (uint32_t)(s * H);
-      if (!(SAND_DIAG && p.prof >= 2))   // diagnostic 2/3 (SAND_DIAG builds): no epilogue math
+      // one 8-column chunk at column offset jc of this group: ra = rows R0, R1; rb = rows R2, R3 (4 regs each)
+      auto chunk = [&](const uint32_t* ra, const uint32_t* rb, const int jc) {
+#if SAND_ABL == 2   // ablation build (timing only): no table loads
+        const float4 ba4 = make_float4(0.1f * jc, 0.2f, 0.3f, 0.4f * jc);
+#else
+        const float4 ba4 = *reinterpret_cast<const float4*>(ba + 2 * jc);
+#endif
+        const float2 b2 = make_float2(ba4.x, ba4.y), a2 = make_float2(ba4.z, ba4.w);
+        float2 c2 = make_float2(0.f, 0.f);
+        if (TAIL == SAND_TAIL_MULT && prod) c2 = *reinterpret_cast<const float2*>(a1 + jc);
+        const uint32_t u = (uint32_t)((c0 + jc) >> 3);
+        uint32_t pk[4];
 #pragma unroll
-      for (int bb = 0; bb < C::HQ / BW; ++bb) {
-        uint32_t r0[4 * CB], r1[4 * CB];   // lane block 0 (rows R0, R1) and block 1 (rows R2, R3)
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t* r = k < 2 ? ra : rb;
+          const int o = 2 * (k & 1);
+          const float2 acc = make_float2(__uint_as_float(r[o]), __uint_as_float(r[o + 1]));
+          float2 h;
+          if (((c0 + jc) & 31) < NP) {   // polynomial sine on the first NP of every 32 columns (host tables match)
+            h = sin_poly2(__ffma2_rn(acc, SP2, b2));
+          } else {
+            const float2 z = __ffma2_rn(acc, SM2, b2);
+#if SAND_ABL == 4   // ablation build (timing only): no sine
+            h = z;
+#else
+            h = make_float2(__sinf(z.x), __sinf(z.y));
+#endif
+          }
+          yv[k] = __ffma2_rn(a2, h, yv[k]);
+          if (TAIL == SAND_TAIL_MULT) yv1[k] = __ffma2_rn(c2, h, yv1[k]);
+          pk[k] = pack_bf16x2(h.x, h.y);
+        }
+        // the 4 rows x 8 columns of this chunk are four 8x8 b16 matrices in the m8n8 fragment layout:
+        // one stmatrix.x4 (lane provides the address of row lane % 8 of matrix lane / 8)
+#if SAND_ABL == 1   // ablation build (timing only): no A-operand stores
+        if (store && pk[0] == 0x12345678u && pk[1] == 0x9u) stmatrix_x4(aSt, pk);
+#else
+        if (store) stmatrix_x4(aSt + (u >> 3) * C::A_CHUNK + (((u & 7u) ^ (uint32_t)(lane & 7)) << 4), pk);
+#endif
+      };
+      if (!(SAND_DIAG && p.prof >= 2)) {   // diagnostic 2/3 (SAND_DIAG builds): no epilogue math
+#pragma unroll
+        for (int bb = 0; bb < NCHB / CB; ++bb) {
+          uint32_t r0[4 * CB], r1[4 * CB];   // lane block 0 (rows R0, R1) and block 1 (rows R2, R3)
 #if SAND_ABL == 3   // ablation build (timing only): no TMEM loads
 #pragma unroll
-        for (int q_ = 0; q_ < 4 * CB; ++q_) { r0[q_] = __float_as_uint(0.01f * (lane + q_ + bb)); r1[q_] = r0[q_] ^ 1u; }
+          for (int q_ = 0; q_ < 4 * CB; ++q_) { r0[q_] = __float_as_uint(0.01f * (lane + q_ + bb)); r1[q_] = r0[q_] ^ 1u; }
 #else
-        tmem_ld_16x256b<CB>(tm + bb * BW, r0);
-        tmem_ld_16x256b<CB>(tm + (16u << 16) + bb * BW, r1);
-        tmem_wait_ld_dep(r0);
-        tmem_wait_ld_dep(r1);
+          tmem_ld_16x256b<CB>(tm + bb * BW, r0);
+          tmem_ld_16x256b<CB>(tm + (16u << 16) + bb * BW, r1);
+          tmem_wait_ld_dep(r0);
+          tmem_wait_ld_dep(r1);
 #endif
 #pragma unroll
-        for (int i = 0; i < CB; ++i) {
-          const int jc = bb * BW + 8 * i;     // chunk column offset within this column quarter
-#if SAND_ABL == 2   // ablation build (timing only): no table loads
-          const float4 ba4 = make_float4(0.1f * jc, 0.2f, 0.3f, 0.4f * jc);
-#else
-          const float4 ba4 = *reinterpret_cast<const float4*>(ba + 2 * jc);
-#endif
-          const float2 b2 = make_float2(ba4.x, ba4.y), a2 = make_float2(ba4.z, ba4.w);
-          float2 c2 = make_float2(0.f, 0.f);
-          if (TAIL == SAND_TAIL_MULT && prod) c2 = *reinterpret_cast<const float2*>(a1 + jc);
-          const uint32_t u = (uint32_t)((c0 + jc) >> 3);
-          uint32_t pk[4];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const uint32_t (&r)[4 * CB] = k < 2 ? r0 : r1;
-            const int o = 4 * i + 2 * (k & 1);
-            const float2 acc = make_float2(__uint_as_float(r[o]), __uint_as_float(r[o + 1]));
-            float2 h;
-            if (((bb * BW + 8 * i) & 31) < NP) {   // polynomial sine on the first NP of every 32 columns
-              h = sin_poly2(__ffma2_rn(acc, SP2, b2));
-            } else {
-              const float2 z = __ffma2_rn(acc, SM2, b2);
-#if SAND_ABL == 4   // ablation build (timing only): no sine
-              h = z;
-#else
-              h = make_float2(__sinf(z.x), __sinf(z.y));
-#endif
-            }
-            yv[k] = __ffma2_rn(a2, h, yv[k]);
-            if (TAIL == SAND_TAIL_MULT) yv1[k] = __ffma2_rn(c2, h, yv1[k]);
-            pk[k] = pack_bf16x2(h.x, h.y);
-          }
-          // the 4 rows x 8 columns of this chunk are four 8x8 b16 matrices in the m8n8 fragment layout:
-          // one stmatrix.x4 (lane provides the address of row lane % 8 of matrix lane / 8)
-#if SAND_ABL == 1   // ablation build (timing only): no A-operand stores
-          if (store && pk[0] == 0x12345678u && pk[1] == 0x9u) stmatrix_x4(aSt, pk);
-#else
-          if (store) stmatrix_x4(aSt + (u >> 3) * C::A_CHUNK + (((u & 7u) ^ (uint32_t)(lane & 7)) << 4), pk);
-#endif
+          for (int i = 0; i < CB; ++i) chunk(r0 + 4 * i, r1 + 4 * i, bb * BW + 8 * i);
+        }
+        if (NCHX > 0 && cq < NCHX) {   // uneven groups: one more chunk
+          uint32_t r0[4], r1[4];
+          tmem_ld_16x256b<1>(tm + NCHB * 8, r0);
+          tmem_ld_16x256b<1>(tm + (16u << 16) + NCHB * 8, r1);
+          tmem_wait_ld_dep(r0);
+          tmem_wait_ld_dep(r1);
+          chunk(r0, r1, NCHB * 8);
         }
       }
       if (prod) {
         // Eq. 3: t_l = (a_l0 . h + c_l0)(a_l1 . h + c_l1) needs both full dot products of the row:
         // sum over the quad (4 column pairs), then over the 4 column quarters through shared memory
-        float2* rb2 = red2 + ((s * 2 + e.kpar) * 4) * 128;
+        float2* rb2 = red2 + ((s * 2 + e.kpar) * NGRP) * 128;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const float s0 = quad_sum(yv[k].x + yv[k].y), s1 = quad_sum(yv1[k].x + yv1[k].y);
           if (tq == 0) rb2[cq * 128 + 32 * q + quad + 8 * k] = make_float2(s0, s1);
         }
-        named_bar_sync(bar_q, 128);
+        named_bar_sync(bar_q, 32 * NGRP);
         if (cq == 0) {
           const int rowl = 32 * q + lane;
           float s0 = tc0[l - 1], s1 = tc1[l - 1];
 #pragma unroll
-          for (int k = 0; k < 4; ++k) { const float2 v = rb2[k * 128 + rowl]; s0 += v.x; s1 += v.y; }
+          for (int k = 0; k < NGRP; ++k) { const float2 v = rb2[k * 128 + rowl]; s0 += v.x; s1 += v.y; }
           e.yprod += s0 * s1;
         }
         e.kpar ^= 1u;
@@ -602,7 +625,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
           if (tq == 0) pq[cq * 128 + 32 * q + quad + 8 * k] = v;
           e.ylin[k] = 0.f;
         }
-        if (NPL == 5 && cq == 0) pq[4 * 128 + 32 * q + lane] = e.yprod;
+        if (TAIL == SAND_TAIL_MULT && cq == 0) pq[NGRP * 128 + 32 * q + lane] = e.yprod;
         e.yprod = 0.f;
         __syncwarp();
         if (lane == 0) mbar_arrive(b_iodone + 8 * s);
@@ -646,8 +669,8 @@ template <int H>
 static size_t smem_for2(long long pt_floats, int L, int tail, int nst) {
   using C = Tc2Shape<H>;
   const size_t tab_bytes = (size_t)((pt_floats + 3) & ~3ll) * 4;
-  const size_t io_bytes = (size_t)C::NSLOT * (tail == SAND_TAIL_MULT ? 5 : 4) * 128 * 4;
-  const size_t red_bytes = tail == SAND_TAIL_MULT ? (size_t)C::NSLOT * 2 * 4 * 128 * 8 : 0;
+  const size_t io_bytes = (size_t)C::NSLOT * (tail == SAND_TAIL_MULT ? C::NGRP + 1 : C::NGRP) * 128 * 4;
+  const size_t red_bytes = tail == SAND_TAIL_MULT ? (size_t)C::NSLOT * 2 * C::NGRP * 128 * 8 : 0;
   return (size_t)C::NSLOT * C::A_BYTES + (size_t)nst * C::STAGE + C::W1_HALF + (size_t)C::NSLOT * C::A1_BYTES +
          tab_bytes + io_bytes + red_bytes + 4 * (size_t)(L + 2) * sizeof(long long) + (3 * nst + 7 * C::NSLOT) * 8 +
          16;
