@@ -10,9 +10,9 @@
 //
 // k_marching_cubes: blocks walk cube rows; one thread per grid vertex column of a row (4 loads, the x + 1
 // corners from the next lane), tables in shared memory, warp scan + one atomicAdd per warp that meets
-// the surface
-// (output order is therefore not deterministic; the triangle set is).  Vertices are interpolated from the
-// edge's lower corner so both cubes sharing an edge produce the same bits.  Bound: HBM (4 B of sdf per
+// the surface, then the warp's triangles emitted one per lane from the staged cubes (output order is
+// therefore not deterministic; the triangle set is).  Vertices are interpolated from the edge's lower
+// corner so both cubes sharing an edge produce the same bits.  Bound: HBM (4 B of sdf per
 // grid vertex + 36 B per triangle).
 #include <algorithm>
 #include <cstdint>
@@ -132,8 +132,10 @@ __global__ void __launch_bounds__(256) k_marching_cubes(const float* __restrict_
                                                         int kp0, const float* __restrict__ axis,
                                                         float* __restrict__ tris, long long cap,
                                                         unsigned long long* __restrict__ counter) {
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int R1 = R - 1;
+  __shared__ float s_lo[8][4][32], s_hi[8][4][32];   // per warp: the lanes' cube corners, case, count scan
+  __shared__ int s_c[8][32], s_off[8][32];
   const long long R2 = (long long)R * R;
   const long long nrows = (long long)R1 * (kc1 - kc0);
   __shared__ uint8_t s_tri[256][15];   // tables in shared memory: per-thread (divergent) indices
@@ -150,22 +152,40 @@ __global__ void __launch_bounds__(256) k_marching_cubes(const float* __restrict_
     const float b = u == 0 ? hi[0] : u == 1 ? hi[1] : u == 2 ? hi[2] : hi[3];
     return (v & 1) ? b : a;
   };
-  for (long long row = blockIdx.x; row < nrows; row += gridDim.x) {
-    const int j = (int)(row % R1), k = kc0 + (int)(row / R1);
+  // segments of 256 cube columns of a row, block-strided; the next segment's loads are issued before the
+  // current one is processed (its compute, counter atomic and emission hide their latency)
+  const unsigned nseg = (unsigned)((R + 255) / 256);
+  const unsigned nsg = (unsigned)nrows * nseg;
+  auto load = [&](unsigned sg, float (&v)[4], float (&x)[4], int& j, int& k, int& i) {
+    const unsigned row = sg / nseg;
+    j = (int)(row % (unsigned)R1);
+    k = kc0 + (int)(row / (unsigned)R1);
+    i = (int)(sg - row * nseg) * 256 + (int)threadIdx.x;
     const float* rowp = sdf + (long long)(k - kp0) * R2 + (long long)j * R;
-    for (int i0 = 0; i0 < R; i0 += blockDim.x) {
-      const int i = i0 + threadIdx.x;
-      const bool inr = i < R;
-      float lo[4];   // x = i: (y, z) = (0,0) (1,0) (0,1) (1,1)
+    const bool inr = i < R, ext = inr && i + 1 < R && lane == 31;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) lo[u] = inr ? __ldg(rowp + i + (u >> 1) * R2 + (u & 1) * R) : 0.f;
+    for (int u = 0; u < 4; ++u) v[u] = inr ? __ldg(rowp + i + (u >> 1) * R2 + (u & 1) * R) : 0.f;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) x[u] = ext ? __ldg(rowp + i + 1 + (u >> 1) * R2 + (u & 1) * R) : 0.f;
+  };
+  float nv[4], nx[4];
+  int nj = 0, nk = 0, ni = 0;
+  if (blockIdx.x < nsg) load(blockIdx.x, nv, nx, nj, nk, ni);
+  for (unsigned sg = blockIdx.x; sg < nsg; sg += gridDim.x) {
+    {
+      float lo[4], xx[4];   // x = i: (y, z) = (0,0) (1,0) (0,1) (1,1); lane 31 also x = i + 1
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { lo[u] = nv[u]; xx[u] = nx[u]; }
+      const int j = nj, k = nk, i = ni;
+      if (sg + gridDim.x < nsg) load(sg + gridDim.x, nv, nx, nj, nk, ni);
+      const bool inr = i < R;
       float hi[4];   // x = i + 1
 #pragma unroll
       for (int u = 0; u < 4; ++u) hi[u] = __shfl_down_sync(0xffffffffu, lo[u], 1);
       const bool cube = inr && i + 1 < R;
-      if (cube && lane == 31) {
+      if (lane == 31) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) hi[u] = __ldg(rowp + i + 1 + (u >> 1) * R2 + (u & 1) * R);
+        for (int u = 0; u < 4; ++u) hi[u] = xx[u];
       }
       int c = 0;
 #pragma unroll
@@ -182,26 +202,44 @@ __global__ void __launch_bounds__(256) k_marching_cubes(const float* __restrict_
         const int y = __shfl_up_sync(0xffffffffu, off, d);
         if (lane >= d) off += y;
       }
+      const int T = __shfl_sync(0xffffffffu, off, 31);   // the warp's triangles
       unsigned long long wbase = 0;
-      if (lane == 31) wbase = atomicAdd(counter, (unsigned long long)off);
+      if (lane == 31) wbase = atomicAdd(counter, (unsigned long long)T);
       wbase = __shfl_sync(0xffffffffu, wbase, 31);
-      const long long first = (long long)wbase + off - nt;
-      for (int t = 0; t < nt; ++t) {
-        if (first + t >= cap) break;
-        float* out = tris + 9 * (first + t);
+      // emit the warp's T triangles lane-parallel (triangle idx by lane idx % 32), not cube by cube: surface
+      // cubes are sparse along a row, so per-cube emission would run ~1 active lane per warp instruction
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { s_lo[warp][u][lane] = lo[u]; s_hi[warp][u][lane] = hi[u]; }
+      s_c[warp][lane] = c;
+      s_off[warp][lane] = off;
+      __syncwarp();
+      for (int idx = lane; idx < T; idx += 32) {
+        if ((long long)wbase + idx >= cap) break;
+        int L = 0;   // owner lane: the first L with inclusive count off[L] > idx
+#pragma unroll
+        for (int st = 16; st; st >>= 1)
+          if (s_off[warp][L + st - 1] <= idx) L += st;
+        const int cL = s_c[warp][L];
+        const int t = idx - (s_off[warp][L] - s_ntri[cL]);
+        const int iL = i - lane + L;
+        float plo[4], phi[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) { plo[u] = s_lo[warp][u][L]; phi[u] = s_hi[warp][u][L]; }
+        float* out = tris + 9 * ((long long)wbase + idx);
 #pragma unroll
         for (int m = 0; m < 3; ++m) {
-          const int e = s_tri[c][3 * t + m];
+          const int e = s_tri[cL][3 * t + m];
           const int v0 = s_edge[e][0], v1 = s_edge[e][1];
-          const float a0 = corner(lo, hi, v0), a1 = corner(lo, hi, v1);
+          const float a0 = corner(plo, phi, v0), a1 = corner(plo, phi, v1);
           const float tt = a0 / (a0 - a1);
-          const float p0x = axis[i + (v0 & 1)], p0y = axis[j + ((v0 >> 1) & 1)], p0z = axis[k + (v0 >> 2)];
-          const float p1x = axis[i + (v1 & 1)], p1y = axis[j + ((v1 >> 1) & 1)], p1z = axis[k + (v1 >> 2)];
+          const float p0x = axis[iL + (v0 & 1)], p0y = axis[j + ((v0 >> 1) & 1)], p0z = axis[k + (v0 >> 2)];
+          const float p1x = axis[iL + (v1 & 1)], p1y = axis[j + ((v1 >> 1) & 1)], p1z = axis[k + (v1 >> 2)];
           out[3 * m] = p0x + tt * (p1x - p0x);
           out[3 * m + 1] = p0y + tt * (p1y - p0y);
           out[3 * m + 2] = p0z + tt * (p1z - p0z);
         }
       }
+      __syncwarp();
     }
   }
 }
