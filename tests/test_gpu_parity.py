@@ -116,8 +116,8 @@ def test_C1_full_bf16():
 @pytest.mark.parametrize("name", ["C2", "C3"])
 def test_C2_C3_full_size_sampled(name):
     """configs[2] (512^3 grid, 134M points, level-7 octree) and configs[3] (8x336, 8M cloud) in the
-    bench's launch configuration: exit depths bit-exact on sampled z-slabs (C2) / all points (C3),
-    SDF on a stratified sample."""
+    bench's launch configuration: exit depths of all points bit-exact, SDF on a stratified
+    sample."""
     c = g.make_config(name)
     p = c.params()
     pts = c.points_fn()
@@ -125,14 +125,11 @@ def test_C2_C3_full_size_sampled(name):
         sdf, dep = run_engine(ctx, p, c.depthmap, pts)
         st = ctx.sand_get_stats()
     n = pts.shape[0]
-    if name == "C2":
-        R = c.grid_R
-        planes = np.arange(0, R, 37)
-        chk = (planes[:, None] * R * R + np.arange(R * R)[None, :]).ravel()
-    else:
-        chk = np.arange(n)
-    d_or, _, _ = oracle.lookup(c.depthmap, pts[chk])
-    np.testing.assert_array_equal(dep[chk], d_or)
+    # exit depths of every point, oracle lookup slab by slab (bounded host memory)
+    step = 1 << 24
+    for q0 in range(0, n, step):
+        d_or, _, _ = oracle.lookup(c.depthmap, pts[q0:q0 + step])
+        np.testing.assert_array_equal(dep[q0:q0 + step], d_or)
     idx = stratified_sample(dep, 4096, 1 << 15, seed=2)
     sdf_or, dep_or = oracle.query(p, c.depthmap, pts[idx])
     assert_parity(sdf, dep, sdf_or, dep_or, TOL_BF16, idx=idx)
