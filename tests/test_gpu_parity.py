@@ -340,10 +340,11 @@ def test_polynomial_sine_share(npoly):
 
 
 @pytest.mark.skipif(os.environ.get("SAND_FULL_PARITY") != "1",
-                    reason="opt-in (SAND_FULL_PARITY=1): the fp64 oracle on all 134M points takes ~30 min")
-def test_C2_full_sdf_all_points():
-    """SDF of EVERY C2 point against the oracle (the default suite samples it)."""
-    c = g.make_config("C2")
+                    reason="opt-in (SAND_FULL_PARITY=1): the fp64 oracle on every point (C2: ~20 min)")
+@pytest.mark.parametrize("name", ["C1", "C2", "C3"])
+def test_full_sdf_all_points(name):
+    """SDF of EVERY point of configs[1..3] against the oracle (the default suite samples it)."""
+    c = g.make_config(name)
     p = c.params()
     pts = c.points_fn()
     with make_ctx(c.spec, BF16) as ctx:
