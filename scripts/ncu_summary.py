@@ -33,7 +33,12 @@ srows = list(csv.reader(io.StringIO(src)))
 hh = srows[1]
 iS = hh.index("Warp Stall Sampling (All Samples)")
 iE = hh.index("Instructions Executed")
-data = srows[2:]
+# first kernel only: a multi-kernel report repeats the header row before each kernel's source table
+data = []
+for r in srows[2:]:
+    if len(r) <= max(iS, iE) or r[iS] == "Warp Stall Sampling (All Samples)":
+        break
+    data.append(r)
 tots = sum(float(r[iS] or 0) for r in data)
 print("top stalled instructions:")
 for r in sorted(data, key=lambda r: -float(r[iS] or 0))[:int(sys.argv[2]) if len(sys.argv) > 2 else 15]:
