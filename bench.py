@@ -96,6 +96,27 @@ def _dist():
     return ws, rank, local
 
 
+def _arm_config(args, c, ws, wl_desc, global_points):
+    """The `config` object of the bench line -- identical for this arm and the reference arm."""
+    return {"workload": wl_desc if ws == 1 else f"{args.config} weak-scaled: {c.grid_R}x{c.grid_R}x{c.grid_R * ws} grid, "
+            "work-balanced z-slabs" if c.grid_R is not None else f"{args.config} x {ws} ranks",
+            "model": f"{c.spec.L}x{c.spec.H} SIREN T-MLP (seeded SIREN init), linear tails",
+            "depth_map": "level-7 sphere-union octree (baked 128^3)" if args.config == "C2" else args.config,
+            "global_points": global_points, "parallelism": f"dp{ws} (z-slab shards)",
+            "l2": (f"inputs {12 * global_points / ws / 1e9:.2f} GB per rank > 126 MB L2; no flush needed"
+                   if 12 * global_points / ws > 126e6 else
+                   f"inputs {12 * global_points / ws / 1e6:.0f} MB per rank < 126 MB L2, not flushed between "
+                   "steps (side config; the N = 1 bench line is C2)"),
+            "full_depth_baseline": bool(args.full_depth)}
+
+
+def _n1_workload(args, c):
+    """The N = 1 workload description (rank 0 of one)."""
+    if c.grid_R is not None:
+        return f"{args.config}: {c.grid_R}x{c.grid_R}x{c.grid_R} grid, z-planes [0,{c.grid_R}) on rank 0"
+    return f"{args.config}: points [0,{c.points_fn().shape[0]})"
+
+
 def run_reference(args):
     """--impl reference: the oracle (oracle/), as it stands, on the host cores, on a bounded
     seeded sample of the same workload per step.  Rank 0 only."""
@@ -104,16 +125,21 @@ def run_reference(args):
         return 0
     import oracle
     import sandgen as g
-    c = g.make_config("C2")
+    c = g.make_config(args.config)
     p = c.params()
     R = c.grid_R
     n_step = args.ref_sample
     rng = np.random.default_rng(1234)
+    cloud = c.points_fn() if R is None else None
+    n_work = R ** 3 if R is not None else cloud.shape[0]
     times = []
     for it in range(args.warmup + args.steps):
-        lin = np.sort(rng.choice(R ** 3, n_step, replace=False))
-        ax = g.grid_axis(R)
-        pts = np.stack([ax[lin % R], ax[(lin // R) % R], ax[lin // (R * R)]], axis=1).astype(np.float32)
+        lin = np.sort(rng.choice(n_work, n_step, replace=False))
+        if R is not None:
+            ax = g.grid_axis(R)
+            pts = np.stack([ax[lin % R], ax[(lin // R) % R], ax[lin // (R * R)]], axis=1).astype(np.float32)
+        else:
+            pts = cloud[lin]
         t0 = time.perf_counter()
         oracle.query(p, c.depthmap, pts)
         dt = time.perf_counter() - t0
@@ -122,12 +148,12 @@ def run_reference(args):
     ms = 1e3 * float(np.mean(times))
     val = n_step / (ms / 1e3)
     cores = _cores()
-    sample = f"{n_step} seeded random vertices of the 512^3 grid per step"
+    sample = (f"{n_step} seeded random vertices of the {R}^3 grid per step" if R is not None else
+              f"{n_step} seeded random points of the {n_work}-point cloud per step")
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "C2: 512^3 grid, 8x256 SIREN T-MLP (seeded init), level-7 sphere-union octree",
-                       "sample_points_per_step": n_step},
+            "config": _arm_config(args, c, ws, _n1_workload(args, c), n_work * ws if R is not None else n_work),
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -635,12 +661,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32" if fp32 else "bf16", "data": "synthetic",
-            "config": {"workload": wl_desc if ws == 1 else f"{args.config} weak-scaled: 512x512x{Rz} grid, "
-                       "work-balanced z-slabs", "model": f"{c.spec.L}x{c.spec.H} SIREN T-MLP (seeded SIREN init), linear tails",
-                       "depth_map": "level-7 sphere-union octree (baked 128^3)" if args.config == "C2" else args.config,
-                       "global_points": summ["n_total"], "parallelism": f"dp{ws} (z-slab shards)",
-                       "l2": f"inputs {12 * n / 1e9:.2f} GB per rank > 126 MB L2; no flush needed",
-                       "full_depth_baseline": bool(args.full_depth)},
+            "config": _arm_config(args, c, ws, wl_desc, summ["n_total"]),
             "roofline": {"bound": "alu" if fp32 else "tensor",
                          "kernel": ("k_query_fp32 (FP32 register-blocked GEMM)" if fp32 else
                                     "k_tmlp_wide (K3 fused T-MLP, CTA pair, N-halves)" if c.spec.H == 336 else
