@@ -36,3 +36,20 @@ def test_sine_roofline_counts_every_evaluated_layer():
     assert r["achieved"] == pytest.approx(r["sines_per_launch"] / 2e-3 / 1e9)
     assert r["peak"] == pytest.approx(148 * 16 * 1e9 / 1e9)
     assert r["frac"] == pytest.approx(r["achieved"] / r["peak"])
+
+
+def test_reference_arm_config_equals_this_arms():
+    """The driver compares the two arms' lines: at N = 1 the reference arm's `config` must be the one
+    this arm prints (same workload string as the z-slab shard of rank 0 of 1)."""
+    import argparse
+    from paper_2604_25936_b200 import partition
+    import sandgen as g
+    args = argparse.Namespace(config="C2", full_depth=False)
+    c = g.make_config("C2")
+    k0, k1, Rz = partition.shard_planes(c.depthmap, c.grid_R, 1, 0, weak=True)
+    wl_this = f"C2: {c.grid_R}x{c.grid_R}x{Rz} grid, z-planes [{k0},{k1}) on rank 0"
+    assert bench._n1_workload(args, c) == wl_this
+    this = bench._arm_config(args, c, 1, wl_this, c.grid_R ** 3)
+    ref = bench._arm_config(args, c, 1, bench._n1_workload(args, c), c.grid_R ** 3)
+    assert this == ref
+    assert this["global_points"] == 512 ** 3 and "no flush needed" in this["l2"]
