@@ -112,6 +112,22 @@ int sand_load_depthmap(sand_ctx* ctx, const sand_depthmap* dm);
 /* Stream on which every subsequent kernel of ctx is enqueued (a cudaStream_t; NULL = legacy 0). */
 int sand_set_stream(sand_ctx* ctx, void* cuda_stream);
 
+/* Explicit execution options.  libsand reads no environment variable; every choice of kernel or
+ * schedule is made here (defaults in brackets).
+ *   SAND_OPT_PAIR_KERNEL  [1] SAND_BF16: 1 = CTA-pair (cta_group::2) tcgen05 kernels where the
+ *                         configuration fits them, 0 = the 1-CTA kernel.  1 on a configuration without a
+ *                         pair kernel -> SAND_ERR_UNSUPPORTED.
+ *   SAND_OPT_DYN_SCHEDULE [0] sand_query_dynamic: 0 = a 64-point tile stops when all its points have
+ *                         stopped; 1 = pools of 512 points re-compacted after every layer.
+ *   SAND_OPT_KPROF        [0] diagnostic: 1 = per-role clock64 wait / busy counters of the CTA-pair
+ *                         kernels printed to stderr after every launch (adds a stream synchronisation);
+ *                         2, 3 = timing-only modes that skip epilogue math / weight streaming in builds
+ *                         compiled with -DSAND_DIAG=1 (wrong results; ignored otherwise).
+ * Errors: SAND_ERR_ARG (unknown option or value), SAND_ERR_UNSUPPORTED.                          */
+typedef enum { SAND_OPT_PAIR_KERNEL = 1, SAND_OPT_DYN_SCHEDULE = 2, SAND_OPT_KPROF = 3 } sand_option;
+int sand_set_option(sand_ctx* ctx, int option, int64_t value);
+int sand_get_option(const sand_ctx* ctx, int option, int64_t* value);
+
 /* Level-of-detail cap (Sec. 3.4; Fig. 4): evaluated depth = min(d, cap) for d >= 1;
  * depth-0 (far) entries are unaffected.  cap in 1..L (default L).  Error: SAND_ERR_ARG.          */
 int sand_set_lod_cap(sand_ctx* ctx, int cap);
@@ -189,9 +205,9 @@ int sand_populate_leaf_depths(sand_ctx* ctx, const float* d_samples, int64_t n_l
  * layer i >= 2 whose residual |t_i| < r (reading R23: t_1 = y_1 is the first prediction, not
  * a residual), else at L:
  *   d_out_exit_depth[p] = that layer (255 for a non-finite point),  d_out_sdf[p] = y_d (NaN if 255).
- * FP32 (sine to ~5e-7) like the population calls above.  Default schedule: a 64-point tile stops as
- * soon as all of its points have stopped; with the environment variable SAND_DYN_POOL=1 (read per call)
- * pools of 512 points are re-compacted after every layer instead.  Only the weights must be loaded; the depth map
+ * FP32 (sine to ~5e-7) like the population calls above.  Schedule: SAND_OPT_DYN_SCHEDULE (a 64-point
+ * tile stops as soon as all of its points have stopped, or pools of 512 points are re-compacted after
+ * every layer).  Only the weights must be loaded; the depth map
  * and LOD cap are ignored.  Asynchronous on ctx's stream.  Errors: SAND_ERR_ARG (n < 0, r < 0 or NaN,
  * NULL buffer), SAND_ERR_STATE, SAND_ERR_UNSUPPORTED (H as above), SAND_ERR_CUDA. */
 int sand_query_dynamic(sand_ctx* ctx, const float* d_points, int64_t n, float r, float* d_out_sdf,

@@ -27,7 +27,10 @@ struct sand_ctx {
   int num_sms = 0;
   cudaStream_t stream = nullptr;
   int lod_cap = 0;
-  bool use_pair = true;   // CTA-pair tcgen05 kernel where available (env SAND_PAIR=0 disables)
+  bool use_pair = true;   // CTA-pair tcgen05 kernel where available (SAND_OPT_PAIR_KERNEL)
+  bool pair_ok = true;    // the CTA-pair kernel supports (L, H, tail) at all
+  int dyn_schedule = 0;   // sand_query_dynamic schedule (SAND_OPT_DYN_SCHEDULE)
+  int kprof = 0;          // diagnostic per-role counters (SAND_OPT_KPROF)
   std::string err;
   // weights
   bool have_w = false;
@@ -153,10 +156,10 @@ extern "C" int sand_create(const sand_config* cfg, sand_ctx** out) {
     return bail(SAND_ERR_UNSUPPORTED);
   }
   ctx->num_sms = prop.multiProcessorCount;
-  if (const char* ev = getenv("SAND_PAIR")) ctx->use_pair = std::atoi(ev) != 0;
   // the CTA-pair kernel keeps its per-column tables in shared memory: large L falls back to the 1-CTA kernel
   if (cfg->prec == SAND_BF16)
-    ctx->use_pair = ctx->use_pair && (tc2_usable(cfg->L, cfg->H, cfg->tail) || tc3_usable(cfg->L, cfg->H, cfg->tail));
+    ctx->pair_ok = tc2_usable(cfg->L, cfg->H, cfg->tail) || tc3_usable(cfg->L, cfg->H, cfg->tail);
+  ctx->use_pair = ctx->pair_ok;
   cudaError_t e = prepare_tmlp_kernels(cfg->L, cfg->H, cfg->tail, cfg->prec);
   if (e != cudaSuccess) { fail(ctx, SAND_ERR_CUDA, "kernel attribute setup: %s", cudaGetErrorString(e)); return bail(SAND_ERR_CUDA); }
   *out = ctx;
@@ -279,54 +282,13 @@ extern "C" int sand_load_weights(sand_ctx* ctx, const float* blob, size_t n_floa
   CU(cudaMalloc(&ctx->d_tables, sizeof(float) * ntab));
   CU(cudaMemcpy(ctx->d_tables, tab.data(), sizeof(float) * ntab, cudaMemcpyHostToDevice));
   m.tables = ctx->d_tables;
+  std::vector<uint8_t> pair_img;   // CTA-pair hidden-layer image (uploaded below)
   if (ctx->cfg.prec == SAND_BF16 && tc2_available(H)) {
-    // CTA-pair kernel tables (layout in sand_internal.h MlpDev): per-column scale by sine path
-    const int np = tc2_npoly();
-    const double kInvPi = 0.15915494309189535;   // 1 / (2 pi): the polynomial takes z in turns
-    // polynomial columns: the first np of every 32 within each epilogue thread's column quarter
-    auto scale = [&](int j) { return ((j % (H / 4)) % 32) < np ? (double)w0 * kInvPi : (double)w0; };
-    m.pt_npoly = np;
-    tc2_table_layout(L, H, tail, &m, true);
-    std::vector<float> pt((size_t)m.pt_floats, 0.f);
-    // interleaved per column pair: [i][j/2] = (bias_j, bias_j+1, a_j, a_j+1)
-    auto ba = [&](int i, int j) { return m.pt_off_bias + (size_t)i * 2 * H + (size_t)(j / 2) * 4 + (j & 1); };
-    for (int i = 1; i < L; ++i)
-      for (int j = 0; j < H; ++j) pt[ba(i, j)] = (float)(scale(j) * b[i][j]);
-    for (int i = 0; i < L; ++i) {
-      for (int j = 0; j < H; ++j) pt[ba(i, j) + 2] = a[i][j];
-      pt[m.pt_off_c + i] = c[i];
-      pt[m.pt_off_c1 + i] = c1[i];
-    }
-    if (tail == SAND_TAIL_MULT)
-      for (int i = 1; i < L; ++i) std::memcpy(&pt[m.pt_off_a1 + (size_t)(i - 1) * H], a1[i], sizeof(float) * H);
-    double cs = 0.0;
-    pt[m.pt_off_csum] = 0.f;
-    for (int d = 1; d <= L; ++d) {
-      cs += (tail == SAND_TAIL_LINEAR || d == 1) ? c[d - 1] : 0.0;
-      pt[m.pt_off_csum + d] = (float)cs;
-    }
-    // layer-1 split-BF16 B operand: row n = (W_hi x y z | W_lo x y z | W_hi x y z | b_hi b_lo | 0 ...),
-    // matching the IO warp's A row (x_hi | x_hi | x_lo | 1 1 | 0): x_hi W_hi + x_hi W_lo + x_lo W_hi + b
-    std::vector<uint16_t> w1img((size_t)H * 16, 0);
-    auto put = [&](int n, int k, uint16_t v) { w1img[tc2_w1_offset(H, n, k) / 2] = v; };
-    auto lo_of = [](float v, uint16_t hi) {
-      uint32_t u = (uint32_t)hi << 16;
-      float h;
-      std::memcpy(&h, &u, 4);
-      return bf16_rne(v - h);
-    };
-    for (int n = 0; n < H; ++n) {
-      for (int k = 0; k < 3; ++k) {
-        const float w = W[0][3 * n + k];
-        const uint16_t hi = bf16_rne(w);
-        put(n, k, hi);
-        put(n, 3 + k, lo_of(w, hi));
-        put(n, 6 + k, hi);
-      }
-      const uint16_t bhi = bf16_rne(b[0][n]);
-      put(n, 9, bhi);
-      put(n, 10, lo_of(b[0][n], bhi));
-    }
+    // CTA-pair kernel: w0 and the biases folded into split-BF16 MMA operands (tmlp_tc2.cu)
+    std::vector<float> pt;
+    std::vector<uint16_t> w1img;
+    tc2_build_host(L, H, tail, w0, W.data(), b.data(), a.data(), a1.data(), c.data(), c1.data(), &m, &pt, &w1img,
+                   &pair_img);
     CU(cudaMalloc(&ctx->d_w1_image, w1img.size() * 2));
     CU(cudaMemcpy(ctx->d_w1_image, w1img.data(), w1img.size() * 2, cudaMemcpyHostToDevice));
     m.w1_image = ctx->d_w1_image;
@@ -376,18 +338,9 @@ extern "C" int sand_load_weights(sand_ctx* ctx, const float* blob, size_t n_floa
         }
       CU(cudaMalloc(&ctx->d_wimage, img.size() * 2));
       CU(cudaMemcpy(ctx->d_wimage, img.data(), img.size() * 2, cudaMemcpyHostToDevice));
-      if (tc2_available(H)) {
-        // pair image: chunk (i, kc) half r -> [(i-1)][r][kc]
-        const size_t half = chunk / 2;
-        std::vector<uint8_t> pimg(img.size() * 2);
-        const uint8_t* src = reinterpret_cast<const uint8_t*>(img.data());
-        for (int i = 1; i < L; ++i)
-          for (int r = 0; r < 2; ++r)
-            for (int kc = 0; kc < KC; ++kc)
-              std::memcpy(&pimg[(((size_t)(i - 1) * 2 + r) * KC + kc) * half],
-                          src + ((size_t)(i - 1) * KC + kc) * chunk + r * half, half);
-        CU(cudaMalloc(&ctx->d_wimage_pair, pimg.size()));
-        CU(cudaMemcpy(ctx->d_wimage_pair, pimg.data(), pimg.size(), cudaMemcpyHostToDevice));
+      if (!pair_img.empty()) {
+        CU(cudaMalloc(&ctx->d_wimage_pair, pair_img.size()));
+        CU(cudaMemcpy(ctx->d_wimage_pair, pair_img.data(), pair_img.size(), cudaMemcpyHostToDevice));
       }
     }
   }
@@ -403,6 +356,7 @@ extern "C" int sand_load_weights(sand_ctx* ctx, const float* blob, size_t n_floa
   m.w_hidden = ctx->d_whidden;
   m.w_image = ctx->d_wimage;
   m.w_image_pair = ctx->d_wimage_pair;
+  m.kprof = ctx->kprof;
   ctx->mlp = m;
   ctx->have_w = true;
   return SAND_OK;
@@ -518,6 +472,38 @@ extern "C" int sand_set_stream(sand_ctx* ctx, void* s) {
   if (!ctx) return fail(ctx, SAND_ERR_ARG, "NULL ctx");
   ctx->stream = reinterpret_cast<cudaStream_t>(s);
   return SAND_OK;
+}
+
+extern "C" int sand_set_option(sand_ctx* ctx, int option, int64_t value) {
+  if (!ctx) return fail(ctx, SAND_ERR_ARG, "NULL ctx");
+  switch (option) {
+    case SAND_OPT_PAIR_KERNEL:
+      if (value != 0 && value != 1) return fail(ctx, SAND_ERR_ARG, "SAND_OPT_PAIR_KERNEL takes 0 or 1");
+      if (value == 1 && !ctx->pair_ok) return fail(ctx, SAND_ERR_UNSUPPORTED, "no CTA-pair kernel for this (prec, L, H, tail)");
+      ctx->use_pair = value == 1;
+      return SAND_OK;
+    case SAND_OPT_DYN_SCHEDULE:
+      if (value != 0 && value != 1) return fail(ctx, SAND_ERR_ARG, "SAND_OPT_DYN_SCHEDULE takes 0 or 1");
+      ctx->dyn_schedule = (int)value;
+      return SAND_OK;
+    case SAND_OPT_KPROF:
+      if (value < 0 || value > 3) return fail(ctx, SAND_ERR_ARG, "SAND_OPT_KPROF takes 0..3");
+      ctx->kprof = (int)value;
+      ctx->mlp.kprof = (int)value;
+      return SAND_OK;
+    default:
+      return fail(ctx, SAND_ERR_ARG, "unknown option %d", option);
+  }
+}
+
+extern "C" int sand_get_option(const sand_ctx* ctx, int option, int64_t* value) {
+  if (!ctx || !value) return SAND_ERR_ARG;
+  switch (option) {
+    case SAND_OPT_PAIR_KERNEL: *value = ctx->use_pair ? 1 : 0; return SAND_OK;
+    case SAND_OPT_DYN_SCHEDULE: *value = ctx->dyn_schedule; return SAND_OK;
+    case SAND_OPT_KPROF: *value = ctx->kprof; return SAND_OK;
+    default: return SAND_ERR_ARG;
+  }
 }
 
 extern "C" int sand_set_lod_cap(sand_ctx* ctx, int cap) {
@@ -812,9 +798,8 @@ extern "C" int sand_query_dynamic(sand_ctx* ctx, const float* d_points, int64_t 
   if (!depthpop_supported(ctx->cfg.H)) return fail(ctx, SAND_ERR_UNSUPPORTED, "H = %d", ctx->cfg.H);
   CU(cudaSetDevice(ctx->cfg.device));
   // default: tile-level early exit (measured faster on the synthetic workloads);
-  // SAND_DYN_POOL=1: pools re-compacted after every layer (read per call)
-  const char* ev = getenv("SAND_DYN_POOL");
-  const bool pool = ev && atoi(ev) != 0;
+  // SAND_OPT_DYN_SCHEDULE = 1: pools re-compacted after every layer
+  const bool pool = ctx->dyn_schedule == 1;
   float* hbuf = nullptr;
   if (pool) {
     if (!ctx->d_dyn_h) {

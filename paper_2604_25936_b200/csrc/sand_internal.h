@@ -68,20 +68,17 @@ struct MlpDev {
   //   a1: [L-1][H] (MULT, i >= 2);  c: [L];  c1: [L-1] (MULT)   -- in this order
   const float* tables;
   long long off_w1, off_bias, off_a, off_c, off_a1, off_c1, tables_floats;
-  // CTA-pair kernel tables (tmlp_tc2.cu), pre-scaled per column for its sine path: of every BW =
-  // min(32, H/4) columns the first min(pt_npoly, BW) use the FMA-pipe polynomial (scale w0/(2 pi)), the rest
-  // MUFU.SIN (scale w0):
-  //   bias: [L][H] = scale(col) * b_i, row 0 (i = 1) zero: b_1 rides in the layer-1 MMA
-  //   a: [L][H];  a1: [L-1][H] (MULT)
+  // CTA-pair kernel tables.  tmlp_tc2.cu (w0 and every bias folded into the MMA operands):
+  //   a: [L][H] tail vectors (a_i or a_i0);  a1: [L-1][H] (MULT)
   //   c   : [L] tail biases (MULT: c_i0);  c1: [L] (MULT: c_i1 at index i-1, i >= 2)
   //   csum: [L+1] LINEAR: sum_{i <= d} c_i;  MULT: c_1 (d >= 1)
+  // tmlp_tc3.cu (wide kernel) additionally keeps w0 * b_i interleaved with a_i: [L][H/2][b pair, a pair].
   const float* pair_tables;
   const void* w1_image;      // layer-1 split-BF16 B operand, [2 halves][H/2 rows][16 bf16] (l1_off layout)
   long long pt_floats, pt_off_l1, pt_off_bias, pt_off_a, pt_off_a1, pt_off_c, pt_off_c1, pt_off_csum;
-  int pt_npoly;
+  int kprof;                 // diagnostic (SAND_OPT_KPROF): per-role clock counters, synchronous dump
 };
 
-constexpr int kPairPolyDefault = 0;   // polynomial-sine columns per 32 in the CTA-pair kernel (0, 8, 16)
 
 cudaError_t launch_tmlp_simt(const MlpDev& m, const float* pts, const uint32_t* perm, const QueryMeta* meta,
                              float* out_sdf, int num_sms, cudaStream_t st);
@@ -119,7 +116,10 @@ cudaError_t launch_leaf_max(const uint8_t* d, long long n_leaves, int spl, uint8
 bool tc2_available(int H);
 bool tc2_usable(int L, int H, int tail);           // H supported and the kernel's shared memory fits
 void tc2_table_layout(int L, int H, int tail, MlpDev* m, bool interleave);   // pair-table offsets (pt_off_*, pt_floats)
-int tc2_npoly();   // polynomial columns per 32 in use (SAND_NPOLY env override: 0, 8, 16)
+// host images of the CTA-pair kernel: tables, layer-1 split-BF16 operand, per-(layer, half) bias + weight image
+void tc2_build_host(int L, int H, int tail, float w0, const float* const* W, const float* const* b,
+                    const float* const* a, const float* const* a1, const float* c, const float* c1, MlpDev* m,
+                    std::vector<float>* tables, std::vector<uint16_t>* w1img, std::vector<uint8_t>* img);
 cudaError_t launch_tmlp_tc2(const MlpDev& m, const float* pts, const uint32_t* perm, const QueryMeta* meta,
                             float* out, int num_sms, cudaStream_t st);
 cudaError_t prepare_tc2(int H, int tail);

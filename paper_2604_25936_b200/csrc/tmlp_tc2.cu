@@ -5,13 +5,18 @@
 //               x = x_hi + x_lo, W_1 = W_hi + W_lo, b_1 = b_hi + b_lo (bf16 each), A row =
 //               (x_hi, x_hi, x_lo, 1, 1, 0...), B row = (W_hi, W_lo, W_hi, b_hi, b_lo, 0...), so the FP32
 //               accumulator holds x_hi W_hi + x_hi W_lo + x_lo W_hi + b (relative error ~2^-16)
-//   layer 2..d: Z_l = H_{l-1} W_l^T (M = 256 over the CTA pair, N = H, K = H, BF16 in, FP32 in TMEM)
-//   every l   : epilogue h_l = sin(w0 Z_l + w0 b_l), t_l (Eq. 2 linear or Eq. 3 product), bf16(h_l) -> A
+//   layer 2..d: Z_l = [1 1 0..] [b_hi b_lo 0..]^T + H_{l-1} W_l^T: one K = 16 MMA puts the bias (split-BF16,
+//               exact to ~2^-16) into the accumulator, then the K = H product (M = 256 over the CTA pair,
+//               N = H, BF16 in, FP32 in TMEM).  w0 is folded into every weight and bias on the host, so the
+//               accumulator holds w0 (W_l h + b_l) and the epilogue applies no scale and no bias.
+//   every l   : epilogue h_l = sin(Z_l), t_l (Eq. 2 linear or Eq. 3 product), bf16(h_l) -> A
 //   output    : sdf[perm[row]] = y_d = sum_{l <= d} t_l (Eq. 2).
 //
 // Warp roles (per CTA of the pair; "leader" = even CTA):
-//   warp 0       weight producer (lane 0): this CTA's half (H/2 rows) of W_l (l >= 2), 2 K-chunks per bulk
-//                async copy (TMA engine) into an NST-stage ring (w_full / w_empty mbarriers)
+//   warp 0       weight producer (lane 0): this CTA's half (H/2 rows) of the job's B operands into an
+//                NST-stage ring (w_full / w_empty mbarriers), one bulk async copy (TMA engine) per stage:
+//                layer 1: the split-BF16 W_1 operand (K = 16); layer l >= 2: stage 0 = bias operand (K = 16)
+//                + 2 K-chunks of W_l, later stages 2 K-chunks each
 //   warp 1       TMEM allocator (2 accumulator slots x H columns); leader: the tcgen05.mma.cta_group::2
 //                issuer (converged warp, one elected lane issues 4 K-steps per asm block); odd CTA: relays
 //                "my half landed" (w_peer)
@@ -26,10 +31,10 @@
 // Every role walks the same deterministic step sequence (rounds: slot 0 then slot 1; a slot's steps are
 // its tiles' layers 1..d).  The MMA order equals the epilogue order, so the ping-pong cannot deadlock.
 //
-// Sine: MUFU.SIN (__sinf) by default.  A compile-time share NP of every 32 output columns can instead use
-// an odd degree-9 polynomial on the FMA pipe after a magic-number range reduction (SAND_NPOLY = 8 / 16,
-// H = 256 LINEAR builds; measured slower).  Bias tables are pre-scaled on the host for the
-// path their column takes (w0 or w0/(2 pi)).
+// Sine: MUFU.SIN (__sinf).  A compile-time share SAND_PP8 of every 8 element pairs can instead use an odd
+// polynomial on the FMA pipe after a radian range reduction (measured slower on B200: FFMA2 retires one
+// pair per 2 clk per SMSP, so a 8-instruction polynomial pair costs as much pipe time as two MUFU sines;
+// DESIGN.md).
 //
 // Tails: LINEAR tails sum linearly over layers, so every thread keeps a running partial over its columns;
 // the IO warp adds the four column quarters of a row and the tail-bias prefix sum csum[d] once per tile.
@@ -37,6 +42,8 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
+#include <vector>
 #include <cuda_runtime.h>
 #include <type_traits>
 
@@ -47,6 +54,21 @@
 #endif
 #ifndef SAND_EPI5
 #define SAND_EPI5 0
+#endif
+#ifndef SAND_PP8
+#define SAND_PP8 0   // poly-sine pairs per 8 (radian reduction, any column); experiment
+#endif
+#ifndef SAND_W1RES
+#define SAND_W1RES 1   // layer-1 B operand resident in shared memory (else streamed through the ring)
+#endif
+#ifndef SAND_ONES_A1
+#define SAND_ONES_A1 0   // 1: bias MMA reads its (1, 1) A columns from the slot's layer-1 operand (k = 9, 10; same speed, saves 4 KB)
+#endif
+#ifndef SAND_SC
+#define SAND_SC 2        // K-chunks per weight-ring stage
+#endif
+#ifndef SAND_PDEG
+#define SAND_PDEG 7
 #endif
 #ifndef SAND_DIAG
 #define SAND_DIAG 0   // 1: diagnostic modes SAND_KPROF=2/3 (timing studies; build with SAND_BUILD_DEFS=-DSAND_DIAG=1)
@@ -64,23 +86,26 @@ struct Tc2Shape {
   static constexpr int KC = H / 64;                // 64-wide K chunks (128-byte swizzle atoms)
   static constexpr int A_CHUNK = 128 * 128;        // one K-chunk of this CTA's 128 rows (bytes)
   static constexpr int A_BYTES = KC * A_CHUNK;
-  static constexpr int W_CHUNK = H * 128;          // full K-chunk of W (both halves) in the image
-  static constexpr int WH_CHUNK = (H / 2) * 128;   // this CTA's half (N/2 rows)
-  static constexpr int SC = KC >= 2 ? 2 : 1;       // K-chunks per weight-ring stage (one bulk copy:
-  static constexpr int STAGE = SC * WH_CHUNK;      // a bulk copy costs ~400 clk of the SM's TMA unit
-  static constexpr int NSJ = KC / SC;              // regardless of size up to 32 KB); stages per job
+  // Every layer's MMA runs as two N-half passes (N = H/2 each, committed separately), so the epilogue starts
+  // on the first half while the tensor pipe computes the second.  cta_group::2 takes an instruction's N rows
+  // of B half from each CTA: a CTA holds QR = H/4 rows per pass.
+  static constexpr int HN = H / 2;                 // output columns per pass
+  static constexpr int QR = H / 4;                 // B rows per CTA per pass
+  static constexpr int QCHUNK = QR * 128;          // one K-chunk of a CTA's pass rows (SW128, bytes)
+  static constexpr int QSMALL = QR * 32 < 1024 ? 1024 : QR * 32;   // K = 16 bias operand of a pass (padded so
+                                                   // the SW128 chunks that follow stay 1024-aligned)
+  static constexpr int STAGE = QSMALL + KC * QCHUNK;   // ring slot = one pass: [bias operand][KC K-chunks]
   static constexpr int A1_BYTES = 128 * 32;        // layer-1 A operand: 128 rows x 16 bf16
-  static constexpr int W1_HALF = (H / 2) * 32;     // layer-1 B operand: this CTA's H/2 rows x 16 bf16
+  static constexpr int W1_BYTES = 2 * QR * 32;     // resident layer-1 B operand: this CTA's 2 x QR rows
+  static constexpr int ONES_BYTES = SAND_ONES_A1 ? 0 : 128 * 32;   // bias MMA A operand: 128 rows of (1, 1, 0, ...)
+  static constexpr int BIAS_K = SAND_ONES_A1 ? 9 : 0;               // k of (b_hi, b_lo) in the bias operand
   static constexpr int NSLOT = 2;
-  static constexpr int HQ = H / 4;                 // columns per epilogue thread (column quarter)
-  static constexpr int NG = HQ / 16;               // 16-column TMEM load groups per thread
+  static constexpr int CQ = HN / 4;                // columns per epilogue column group per pass
   static constexpr int TMEM_COLS = 2 * H <= 128 ? 128 : (2 * H <= 256 ? 256 : 512);
-  // epilogue column groups: 4 (16 warps) or, with SAND_EPI5 at H = 256, 5 (20 warps, 7/7/6/6/6 chunks of
-  // 8 columns, 88 registers per thread)
-  static constexpr int NGRP = (H == 256 && SAND_EPI5) ? 5 : 4;
-  static constexpr int THREADS = 96 + 128 * NGRP;   // 3 control warps + 4 NGRP epilogue warps
+  static constexpr int NGRP = 4;                   // epilogue column groups (x 4 TMEM lane quadrants = 16 warps)
+  static constexpr int THREADS = 96 + 128 * NGRP;  // 3 control warps + 16 epilogue warps
   static constexpr int TILE = 256;
-  static_assert(H % 64 == 0 && H <= 256 && HQ % 16 == 0, "CTA-pair kernel: H in {64, 128, 192, 256}");
+  static_assert(H % 64 == 0 && H <= 256 && CQ % 8 == 0, "CTA-pair kernel: H in {64, 128, 192, 256}");
 };
 
 struct Tc2Params {
@@ -132,20 +157,27 @@ struct SlotWalk {
 };
 
 // ------------------------------------------------------------------------------ sine paths
-// Polynomial path (FMA pipe only): u = z / (2 pi) (pre-scaled), k = rint(u) by the 1.5 * 2^23 magic add,
-// r = u - k in [-1/2, 1/2], sin(z) = sin(2 pi r) = r (C1 + C3 r^2 + ... + C9 r^8), an odd degree-9
-// near-minimax fit on [-1/2, 1/2] (|error| < 7e-6 in FP32; the BF16 rounding of h is 2^-9 relative).
-__device__ __forceinline__ float2 sin_poly2(float2 u) {
-  const float2 M = make_float2(12582912.0f, 12582912.0f);
-  const float2 t = __fadd2_rn(u, M);
+// Radian-domain polynomial sine (FMA pipe only), any z: k = rint(z / 2 pi) by the 1.5 * 2^23 magic add
+// fused into the scaling FMA, r = z - 2 pi k in [-pi, pi], sin r = r P(r^2), odd minimax fit on [-pi, pi]
+// (degree 7: |err| < 2.6e-4; degree 9: < 6.2e-6, float32 Horner).
+__device__ __forceinline__ float2 sin_poly_rad2(float2 z) {
+  const float2 t = __ffma2_rn(z, make_float2(0.15915494309189535f, 0.15915494309189535f),
+                              make_float2(12582912.0f, 12582912.0f));
   const float2 k = __fadd2_rn(t, make_float2(-12582912.0f, -12582912.0f));
-  const float2 r = __ffma2_rn(k, make_float2(-1.0f, -1.0f), u);
+  const float2 r = __ffma2_rn(k, make_float2(-6.283185307179586f, -6.283185307179586f), z);
   const float2 r2 = __fmul2_rn(r, r);
-  float2 p = __ffma2_rn(r2, make_float2(32.783390045166016f, 32.783390045166016f),
-                        make_float2(-74.4790267944336f, -74.4790267944336f));
-  p = __ffma2_rn(p, r2, make_float2(81.36698913574219f, 81.36698913574219f));
-  p = __ffma2_rn(p, r2, make_float2(-41.33122634887695f, -41.33122634887695f));
-  p = __ffma2_rn(p, r2, make_float2(6.283055782318115f, 6.283055782318115f));
+#if SAND_PDEG == 9
+  float2 p = __ffma2_rn(r2, make_float2(2.1478720100276405e-06f, 2.1478720100276405e-06f),
+                        make_float2(-0.00019264993898104876f, -0.00019264993898104876f));
+  p = __ffma2_rn(p, r2, make_float2(0.008308985270559788f, 0.008308985270559788f));
+  p = __ffma2_rn(p, r2, make_float2(-0.16662438213825226f, -0.16662438213825226f));
+  p = __ffma2_rn(p, r2, make_float2(0.9999793767929077f, 0.9999793767929077f));
+#else
+  float2 p = __ffma2_rn(r2, make_float2(-0.0001450767886126414f, -0.0001450767886126414f),
+                        make_float2(0.007958059199154377f, 0.007958059199154377f));
+  p = __ffma2_rn(p, r2, make_float2(-0.16566696763038635f, -0.16566696763038635f));
+  p = __ffma2_rn(p, r2, make_float2(0.9992758631706238f, 0.9992758631706238f));
+#endif
   return __fmul2_rn(p, r);
 }
 
@@ -162,7 +194,7 @@ struct EpiSlot {
   float yprod;        // MULT: sum of the Eq. 3 products (column-quarter 0 warps, row 32 q + lane)
 };
 
-template <int H, int TAIL, int NP>
+template <int H, int TAIL>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS, 1)
     k_tmlp_tc2(const Tc2Params p) {
   using C = Tc2Shape<H>;
@@ -180,8 +212,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
   // ---- shared memory carve-up (identical offsets in both CTAs: the pair MMA relies on it)
   const uint32_t sA = base;                                       // [slot] KC x 16 KB, SW128 K-major
   const uint32_t sW = sA + NSLOT * C::A_BYTES;                    // weight ring, nst x STAGE
-  const uint32_t sW1 = sW + nst * C::STAGE;                       // layer-1 B half (resident)
-  const uint32_t sA1 = sW1 + C::W1_HALF;                          // [slot] layer-1 A operand
+  const uint32_t sOnes = sW + nst * C::STAGE;                     // bias-MMA A operand (constant; unless ONES_A1)
+  const uint32_t sW1 = sOnes + C::ONES_BYTES;                     // resident layer-1 B operand (both passes)
+  const uint32_t sA1 = sW1 + C::W1_BYTES;                         // [slot] layer-1 A operand
   float* tab = reinterpret_cast<float*>(gbase + ((sA1 + NSLOT * C::A1_BYTES) - base));
   const long long ntab = p.m.pt_floats;
   constexpr int NGRP = C::NGRP;
@@ -200,12 +233,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
   const uint32_t b_wempty = b_wfull + 8 * nst;
   const uint32_t b_wpeer = b_wempty + 8 * nst;
   const uint32_t b_afull = b_wpeer + 8 * nst;           // [slot]  epilogue step done (A written / acc read)
-  const uint32_t b_accfull = b_afull + 8 * NSLOT;       // [slot]  accumulator ready
-  const uint32_t b_a1full = b_accfull + 8 * NSLOT;      // [slot]  layer-1 A written (leader: 2 arrivals)
+  const uint32_t b_accfull = b_afull + 8 * NSLOT;       // [slot][pass]  accumulator half ready
+  const uint32_t b_a1full = b_accfull + 16 * NSLOT;     // [slot]  layer-1 A written (leader: 2 arrivals)
   const uint32_t b_a1free = b_a1full + 8 * NSLOT;       // [slot]  layer-1 MMA done with the A1 buffer
   const uint32_t b_iodone = b_a1free + 8 * NSLOT;       // [slot]  all epilogue warps wrote their partials
   const uint32_t b_partfree = b_iodone + 8 * NSLOT;     // [slot]  IO warp has read the partials
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * nst + 7 * NSLOT);   // (3 nst + 7 NSLOT) barriers
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * nst + 8 * NSLOT);   // (3 nst + 8 NSLOT) barriers
 #ifdef SAND_HANG_DEBUG
   if (blockIdx.x == 0 && threadIdx.x == 0)
     printf("[bars] wfull 0x%x wempty 0x%x wpeer 0x%x afull 0x%x accfull 0x%x a1full 0x%x a1free 0x%x iodone 0x%x\n",
@@ -217,17 +250,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
     const float4* src = reinterpret_cast<const float4*>(p.m.pair_tables);
     float4* dst = reinterpret_cast<float4*>(tab);
     for (long long i = tid; i < (ntab + 3) / 4; i += blockDim.x) dst[i] = src[i];
-    const uint4* w1s = reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(p.m.w1_image) +
-                                                      rank * C::W1_HALF);
-    uint4* w1d = reinterpret_cast<uint4*>(gbase + (sW1 - base));
-    for (int i = tid; i < C::W1_HALF / 16; i += blockDim.x) w1d[i] = w1s[i];
+    // A rows (1, 1, 0, ..., 0) against the bias operand's (b_hi, b_lo, 0, ...): the K = 16 bias MMA
+    if (!SAND_ONES_A1) {
+      uint32_t* ones = reinterpret_cast<uint32_t*>(gbase + (sOnes - base));
+      for (int i = tid; i < C::ONES_BYTES / 4; i += blockDim.x) ones[i] = 0u;
+      __syncthreads();
+      for (int r = tid; r < 128; r += blockDim.x) ones[l1_off((uint32_t)r, 0) / 4] = 0x3F803F80u;
+    }
+    {
+      const uint4* w1s = reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(p.m.w1_image) + rank * C::W1_BYTES);
+      uint4* w1d = reinterpret_cast<uint4*>(gbase + (sW1 - base));
+      for (int i = tid; i < C::W1_BYTES / 16; i += blockDim.x) w1d[i] = w1s[i];
+    }
     if (tid < nb) {
       s_tile_end[tid] = p.meta->tile_end[tid];
       s_tile_begin[tid] = p.meta->tile_begin[tid];
       s_start[tid] = p.meta->start[tid];
       s_count[tid] = p.meta->count[tid];
     }
-    fence_proxy_async_smem();   // W1 (generic stores) -> tensor core (async proxy)
+    fence_proxy_async_smem();   // ones operand (generic stores) -> tensor core (async proxy)
   }
   constexpr uint32_t kEpiWarps = 4 * NGRP;
   if (tid == 0) {
@@ -237,7 +278,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
       mbar_init(b_wpeer + 8 * i, 1);
     }
     // a_full: one arrive per epilogue warp of both CTAs
-    for (int s = 0; s < NSLOT; ++s) { mbar_init(b_afull + 8 * s, 2 * kEpiWarps); mbar_init(b_accfull + 8 * s, 1); }
+    for (int s = 0; s < NSLOT; ++s) {
+      mbar_init(b_afull + 8 * s, 2 * kEpiWarps);
+      mbar_init(b_accfull + 16 * s, 1);
+      mbar_init(b_accfull + 16 * s + 8, 1);
+    }
     for (int s = 0; s < NSLOT; ++s) { mbar_init(b_a1full + 8 * s, 2); mbar_init(b_a1free + 8 * s, 1); }
     for (int s = 0; s < NSLOT; ++s) { mbar_init(b_iodone + 8 * s, kEpiWarps); mbar_init(b_partfree + 8 * s, 1); }
     fence_mbar_init();
@@ -259,18 +304,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
       SlotWalk w0, w1;
       w0.start(pair, T, s_tile_end, L);
       w1.start(pair + npairs, T, s_tile_end, L);
-      // pair weight image: [L-1][2 CTA halves][KC][H/2 rows][128 B]: a CTA's half of a layer is contiguous
-      const uint8_t* img = reinterpret_cast<const uint8_t*>(p.m.w_image_pair) + (size_t)rank * C::KC * C::WH_CHUNK;
+      // hidden-layer image: [L-1][CTA][pass][STAGE]: one bulk copy per pass
+      const uint8_t* img = reinterpret_cast<const uint8_t*>(p.m.w_image_pair) + (size_t)rank * 2 * C::STAGE;
       const uint32_t peer_wpeer = mapa_shared(b_wpeer, 0);
-      constexpr uint32_t ID = idesc_bf16(256, H);
+      constexpr uint32_t ID = idesc_bf16(256, C::HN);
       uint32_t pa0 = 0, pa1 = 0;
       int st = 0;
       uint32_t ph = 0;
       unsigned long long pc[6] = {0, 0, 0, 0, 0, 0};
       const long long t_start = p.prof ? clock64() : 0;
       // a_full[s] completes once per epilogue step of slot s (all epilogue warps of both CTAs arrived:
-      // A written for the next layer and / or accumulator read).  Every MMA job but the first of a slot
-      // waits for the previous step of its slot, so the accumulator is never overwritten while read.
+      // A written for the next layer and accumulator read).  Every MMA job but the first of a slot waits
+      // for the previous step of its slot, so the accumulator is never overwritten while read.
       auto wait_prev_step = [&](const SlotWalk& w, int s) {
         if (w.ti == 0 && w.l == 1) return;
         uint32_t& pa = s ? pa1 : pa0;
@@ -281,58 +326,62 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
       };
       auto job = [&](const SlotWalk& w, int s) {
         const int l = w.l;
-        if (l == 1) {
-          if (warp != 1 || rank != 0) return;
-          // ---- layer 1: one K = 16 MMA on the split-BF16 operands written by the IO warps
-          wait_prev_step(w, s);
-          const long long c0_ = p.prof ? clock64() : 0;
-          mbar_wait_cluster(b_a1full + 8 * s, (uint32_t)(w.ti & 1));
-          if (p.prof) { pc[0] += clock64() - c0_; pc[3] += 1; }
-          tc_fence_after();
-          mma_bf16_cg2_w(tmem_base + (uint32_t)(s * H), desc_nosw(sA1 + s * C::A1_BYTES, 128, 256),
-                       desc_nosw(sW1, 128, 256), ID, 0u);
-          mma_commit_cg2_mc_w(b_a1free + 8 * s, 0x3);
-          mma_commit_cg2_mc_w(b_accfull + 8 * s, 0x3);
-          return;
-        }
+        const int nsj = l == 1 ? 0 : 2;   // ring stages of this job (one per pass)
         if (warp == 0) {
-          const uint8_t* src = img + (size_t)(l - 2) * 2 * C::KC * C::WH_CHUNK;
-          for (int j = 0; j < C::NSJ && !(SAND_DIAG && p.prof == 3); ++j) {
+          for (int j = 0; j < nsj && !(SAND_DIAG && p.prof == 3); ++j) {
             const long long c0_ = p.prof ? clock64() : 0;
             mbar_wait_lazy(b_wempty + 8 * st, ph ^ 1u);
             if (p.prof) { pc[4] += clock64() - c0_; pc[5] += 1; }
             mbar_arrive_expect_tx(b_wfull + 8 * st, C::STAGE);
-            bulk_g2s(sW + st * C::STAGE, src + (size_t)j * C::STAGE, C::STAGE, b_wfull + 8 * st);
+            bulk_g2s(sW + st * C::STAGE, img + ((size_t)(l - 2) * 4 + j) * C::STAGE, C::STAGE, b_wfull + 8 * st);
             if (++st == nst) { st = 0; ph ^= 1u; }
           }
         } else if (rank == 0) {
           wait_prev_step(w, s);
-          long long c0_ = 0;
-          tc_fence_after();
           const uint32_t acc = tmem_base + (uint32_t)(s * H);
+          if (l == 1) {
+            // ---- layer 1: per pass one K = 16 MMA on the split-BF16 operands (A written by the IO warps)
+            const long long c0_ = p.prof ? clock64() : 0;
+            mbar_wait_cluster(b_a1full + 8 * s, (uint32_t)(w.ti & 1));
+            if (p.prof) { pc[0] += clock64() - c0_; }
+            tc_fence_after();
+            const uint64_t a1d = desc_nosw(sA1 + s * C::A1_BYTES, 128, 256);
+            mma_bf16_cg2_w(acc, a1d, desc_nosw(sW1, 128, 256), ID, 0u);
+            mma_commit_cg2_mc_w(b_accfull + 16 * s, 0x3);
+            mma_bf16_cg2_w(acc + C::HN, a1d, desc_nosw(sW1 + C::QR * 32, 128, 256), ID, 0u);
+            mma_commit_cg2_mc_w(b_a1free + 8 * s, 0x3);
+            mma_commit_cg2_mc_w(b_accfull + 16 * s + 8, 0x3);
+            return;
+          }
+          tc_fence_after();
           // descriptors precomputed once per job / stage: a K-step of 32 B is +2 in the address field.
           // (Computing them per MMA costs the single issuing thread more than the tensor pipe's time.)
           const uint64_t a_d = desc_sw128(sA + s * C::A_BYTES);
+          // bias: (1, 1) x (b_hi, b_lo) initialises the accumulator half.  With SAND_ONES_A1 the A operand is
+          // the slot's layer-1 operand, whose k = 9, 10 are always 1 (the IO warp may be rewriting its other
+          // columns for the next tile meanwhile: they hold finite values and meet zeros in the bias operand,
+          // so the product is b_hi + b_lo whichever version the tensor core reads)
+          const uint64_t ones_d = desc_nosw(SAND_ONES_A1 ? sA1 + s * C::A1_BYTES : sOnes, 128, 256);
 #pragma unroll
-          for (int j = 0; j < C::NSJ; ++j) {
-            c0_ = p.prof ? clock64() : 0;
+          for (int j = 0; j < 2; ++j) {
+            const long long c0_ = p.prof ? clock64() : 0;
             if (!(SAND_DIAG && p.prof == 3)) { mbar_wait(b_wfull + 8 * st, ph);
             mbar_wait_cluster(b_wpeer + 8 * st, ph); }   // diagnostic 3: no weight streaming
             if (p.prof) pc[1] += clock64() - c0_;
             tc_fence_after();
-            const uint64_t w_d = desc_sw128(sW + st * C::STAGE);
+            const uint32_t slot = sW + st * C::STAGE;
+            const uint32_t d = acc + (uint32_t)(j * C::HN);
+            mma_bf16_cg2_w(d, ones_d, desc_nosw(slot, 128, 256), ID, 0u);
+            const uint64_t w_d = desc_sw128(slot + C::QSMALL);
 #pragma unroll
-            for (int c = 0; c < C::SC; ++c) {
-              const int kc = j * C::SC + c;
-              mma4_bf16_cg2_w(acc, a_d + (uint64_t)(kc * (C::A_CHUNK >> 4)), w_d + (uint64_t)(c * (C::WH_CHUNK >> 4)), ID,
-                              kc ? 1u : 0u);
-            }
+            for (int kc = 0; kc < C::KC; ++kc)
+              mma4_bf16_cg2_w(d, a_d + (uint64_t)(kc * (C::A_CHUNK >> 4)), w_d + (uint64_t)(kc * (C::QCHUNK >> 4)), ID, 1u);
             mma_commit_cg2_mc_w(b_wempty + 8 * st, 0x3);
+            mma_commit_cg2_mc_w(b_accfull + 16 * s + 8 * j, 0x3);
             if (++st == nst) { st = 0; ph ^= 1u; }
           }
-          mma_commit_cg2_mc_w(b_accfull + 8 * s, 0x3);
         } else {
-          for (int j = 0; j < C::NSJ && !(SAND_DIAG && p.prof == 3); ++j) {
+          for (int j = 0; j < nsj && !(SAND_DIAG && p.prof == 3); ++j) {
             mbar_wait(b_wfull + 8 * st, ph);
             if (lane == 0) mbar_arrive_remote(peer_wpeer + 8 * st);
             __syncwarp();
@@ -476,17 +525,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
     // R_k = 32q + quad + 8k (k = 0..3) and, in every 8-column chunk, columns 2 tq and 2 tq + 1.  Each
     // per-column table value it loads serves 4 rows (4x fewer shared-memory table reads than one row per
     // thread), at the price of 4-byte A-operand stores.
+    // Columns: the group's CQ columns of each pass, c0 + pass * HN + [0, CQ).
     const int quad = lane >> 2, tq = lane & 3;
-    constexpr int NCHB = H / 8 / NGRP, NCHX = H / 8 % NGRP;   // chunks per group: NCHB (+1 for the first NCHX)
-    const int c0 = 8 * (cq * NCHB + (cq < NCHX ? cq : NCHX));
-    constexpr int BW = 16;                        // columns per TMEM load batch (2 x 8 registers)
+    constexpr int NCHP = C::CQ / 8;               // 8-column chunks per group per pass
+    const int c0 = cq * C::CQ;
+    constexpr int BW = NCHP >= 2 ? 16 : 8;        // columns per TMEM load batch (2 x BW/2 registers)
     constexpr int CB = BW / 8;                    // 8-column chunks per batch
-    static_assert(NCHB % CB == 0, "whole TMEM load batches per group");
+    static_assert(NCHP % CB == 0, "whole TMEM load batches per group");
     const uint32_t tm_q = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)c0;
     const uint32_t a_st = sA + (uint32_t)(4 * q + (lane >> 3)) * 1024 + (uint32_t)(lane & 7) * 128;
-    const float2 SM2 = make_float2(p.m.omega0, p.m.omega0);
-    const float2 SP2 = make_float2(p.m.omega0 * 0.15915494309189535f, p.m.omega0 * 0.15915494309189535f);
-    const float* tba = tab + p.m.pt_off_bias;  // [L][H/2][bias pair, a pair] (row 0 bias = 0: b_1 is in the layer-1 MMA)
+    const float* tta = tab + p.m.pt_off_a;     // [L][H] tail vectors (a_l or a_l0)
     const float* ta1 = tab + p.m.pt_off_a1;    // [L-1][H] (MULT)
     const float* tc0 = tab + p.m.pt_off_c;     // [L]
     const float* tc1 = tab + p.m.pt_off_c1;    // [L] (MULT, index l-1)
@@ -516,38 +564,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
       float2 yv[4], yv1[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) { yv[k] = make_float2(0.f, 0.f); yv1[k] = make_float2(0.f, 0.f); }
+      long long wt = 0;
       const long long c0_ = p.prof ? clock64() : 0;
-      mbar_wait(b_accfull + 8 * s, e.pe);
-      const long long c1_ = p.prof ? clock64() : 0;
-      e.pe ^= 1u;
-      tc_fence_after();
       const bool store = l != d;
-      const float* ba = tba + (l - 1) * 2 * H + (c0 + 2 * tq) * 2;
+      const float* ta = tta + (l - 1) * H + c0 + 2 * tq;
       const float* a1 = ta1 + (l - 2) * H + c0 + 2 * tq;
       const bool prod = TAIL == SAND_TAIL_MULT && l >= 2;
       const uint32_t tm = tm_q + (uint32_t)(s * H);
       // one 8-column chunk at column offset jc of this group: ra = rows R0, R1; rb = rows R2, R3 (4 regs each)
-      auto chunk = [&](const uint32_t* ra, const uint32_t* rb, const int jc, auto st_c) {
+      auto chunk = [&](const uint32_t* ra, const uint32_t* rb, const int jc, uint32_t (&pk)[4]) {
 #if SAND_ABL == 2   // ablation build (timing only): no table loads
-        const float4 ba4 = make_float4(0.1f * jc, 0.2f, 0.3f, 0.4f * jc);
+        const float2 a2 = make_float2(0.1f * jc, 0.2f);
 #else
-        const float4 ba4 = *reinterpret_cast<const float4*>(ba + 2 * jc);
+        const float2 a2 = *reinterpret_cast<const float2*>(ta + jc);
 #endif
-        const float2 b2 = make_float2(ba4.x, ba4.y), a2 = make_float2(ba4.z, ba4.w);
         float2 c2 = make_float2(0.f, 0.f);
         if (TAIL == SAND_TAIL_MULT && prod) c2 = *reinterpret_cast<const float2*>(a1 + jc);
-        const uint32_t u = (uint32_t)((c0 + jc) >> 3);
-        uint32_t pk[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const uint32_t* r = k < 2 ? ra : rb;
           const int o = 2 * (k & 1);
-          const float2 acc = make_float2(__uint_as_float(r[o]), __uint_as_float(r[o + 1]));
+          // z = w0 (W h + b) straight from the accumulator (w0 and the bias are folded into the MMA)
+          const float2 z = make_float2(__uint_as_float(r[o]), __uint_as_float(r[o + 1]));
           float2 h;
-          if (((c0 + jc) & 31) < NP) {   // polynomial sine on the first NP of every 32 columns (host tables match)
-            h = sin_poly2(__ffma2_rn(acc, SP2, b2));
+          if (k + 4 * ((jc >> 3) & 1) < SAND_PP8) {
+            h = sin_poly_rad2(z);
           } else {
-            const float2 z = __ffma2_rn(acc, SM2, b2);
 #if SAND_ABL == 4   // ablation build (timing only): no sine
             h = z;
 #else
@@ -558,44 +600,71 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
           if (TAIL == SAND_TAIL_MULT) yv1[k] = __ffma2_rn(c2, h, yv1[k]);
           pk[k] = pack_bf16x2(h.x, h.y);
         }
-        // the 4 rows x 8 columns of this chunk are four 8x8 b16 matrices in the m8n8 fragment layout:
-        // one stmatrix.x4 (lane provides the address of row lane % 8 of matrix lane / 8)
+      };
+      // the 4 rows x 8 columns of a chunk (column offset jc of this group) are four 8x8 b16 matrices in the
+      // m8n8 fragment layout: one stmatrix.x4 (lane provides the address of row lane % 8 of matrix lane / 8)
+      auto st_chunk = [&](const int jc, const uint32_t (&pk)[4]) {
+        const uint32_t u = (uint32_t)((c0 + jc) >> 3);
 #if SAND_ABL == 1   // ablation build (timing only): no A-operand stores
-        if (store && pk[0] == 0x12345678u && pk[1] == 0x9u) stmatrix_x4(aSt, pk);
+        if (pk[0] == 0x12345678u && pk[1] == 0x9u) stmatrix_x4(aSt, pk);
 #else
-        if (SAND_SPLIT_STORE ? decltype(st_c)::value : store)
-          stmatrix_x4(aSt + (u >> 3) * C::A_CHUNK + (((u & 7u) ^ (uint32_t)(lane & 7)) << 4), pk);
+        stmatrix_x4(aSt + (u >> 3) * C::A_CHUNK + (((u & 7u) ^ (uint32_t)(lane & 7)) << 4), pk);
 #endif
       };
-      auto math = [&](auto st_c) {
+      // pass-0 h (bf16) is held here until the pass-1 MMA of this layer, which still reads the old A operand,
+      // has completed (acc_full of pass 1)
+      uint32_t stash[NCHP][4];
+      auto math = [&](auto st_c, auto pass_c) {
+        constexpr int PO = decltype(pass_c)::value * C::HN;   // column offset of this pass
+        constexpr bool ST = SAND_SPLIT_STORE ? decltype(st_c)::value : true;
+        {
+          const long long w0_ = p.prof ? clock64() : 0;
+          mbar_wait(b_accfull + 16 * s + 8 * decltype(pass_c)::value, e.pe);
+          if (p.prof) wt += clock64() - w0_;
+          tc_fence_after();
+        }
+        if (decltype(pass_c)::value == 1 && ST && (SAND_SPLIT_STORE || store)) {
 #pragma unroll
-        for (int bb = 0; bb < NCHB / CB; ++bb) {
+          for (int i = 0; i < NCHP; ++i) st_chunk(8 * i, stash[i]);
+        }
+#pragma unroll
+        for (int bb = 0; bb < NCHP / CB; ++bb) {
           uint32_t r0[4 * CB], r1[4 * CB];   // lane block 0 (rows R0, R1) and block 1 (rows R2, R3)
 #if SAND_ABL == 3   // ablation build (timing only): no TMEM loads
 #pragma unroll
           for (int q_ = 0; q_ < 4 * CB; ++q_) { r0[q_] = __float_as_uint(0.01f * (lane + q_ + bb)); r1[q_] = r0[q_] ^ 1u; }
 #else
-          tmem_ld_16x256b<CB>(tm + bb * BW, r0);
-          tmem_ld_16x256b<CB>(tm + (16u << 16) + bb * BW, r1);
+          tmem_ld_16x256b<CB>(tm + PO + bb * BW, r0);
+          tmem_ld_16x256b<CB>(tm + PO + (16u << 16) + bb * BW, r1);
           tmem_wait_ld_dep(r0);
           tmem_wait_ld_dep(r1);
 #endif
 #pragma unroll
-          for (int i = 0; i < CB; ++i) chunk(r0 + 4 * i, r1 + 4 * i, bb * BW + 8 * i, st_c);
-        }
-        if (NCHX > 0 && cq < NCHX) {   // uneven groups: one more chunk
-          uint32_t r0[4], r1[4];
-          tmem_ld_16x256b<1>(tm + NCHB * 8, r0);
-          tmem_ld_16x256b<1>(tm + (16u << 16) + NCHB * 8, r1);
-          tmem_wait_ld_dep(r0);
-          tmem_wait_ld_dep(r1);
-          chunk(r0, r1, NCHB * 8, st_c);
+          for (int i = 0; i < CB; ++i) {
+            uint32_t pk[4];
+            chunk(r0 + 4 * i, r1 + 4 * i, PO + bb * BW + 8 * i, pk);
+            if (ST && (SAND_SPLIT_STORE || store)) {
+              if (decltype(pass_c)::value == 0) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) stash[bb * CB + i][k] = pk[k];
+              } else {
+                st_chunk(PO + bb * BW + 8 * i, pk);
+              }
+            }
+          }
         }
       };
+      using P0 = std::integral_constant<int, 0>;
+      using P1 = std::integral_constant<int, 1>;
       if (!(SAND_DIAG && p.prof >= 2)) {   // diagnostic 2/3 (SAND_DIAG builds): no epilogue math
-        if (SAND_SPLIT_STORE && store) math(std::true_type{});
-        else math(std::false_type{});
+        if (SAND_SPLIT_STORE && store) { math(std::true_type{}, P0{}); math(std::true_type{}, P1{}); }
+        else { math(std::false_type{}, P0{}); math(std::false_type{}, P1{}); }
+      } else {
+        mbar_wait(b_accfull + 16 * s, e.pe);
+        mbar_wait(b_accfull + 16 * s + 8, e.pe);
+        tc_fence_after();
       }
+      e.pe ^= 1u;
       if (prod) {
         // Eq. 3: t_l = (a_l0 . h + c_l0)(a_l1 . h + c_l1) needs both full dot products of the row:
         // sum over the quad (4 column pairs), then over the 4 column quarters through shared memory
@@ -641,7 +710,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
       }
       if (p.prof) ep_tend += clock64() - ct_;
       e.w.advance(tstride, T, s_tile_end, L);
-      if (p.prof) { ep_wait += c1_ - c0_; ep_busy += clock64() - c1_; ep_steps += 1; }
+      if (p.prof) { ep_wait += wt; ep_busy += clock64() - c0_ - wt; ep_steps += 1; }
     };
 
     EpiSlot e0, e1;
@@ -680,8 +749,8 @@ static size_t smem_for2(long long pt_floats, int L, int tail, int nst) {
   const size_t tab_bytes = (size_t)((pt_floats + 3) & ~3ll) * 4;
   const size_t io_bytes = (size_t)C::NSLOT * (tail == SAND_TAIL_MULT ? C::NGRP + 1 : C::NGRP) * 128 * 4;
   const size_t red_bytes = tail == SAND_TAIL_MULT ? (size_t)C::NSLOT * 2 * C::NGRP * 128 * 8 : 0;
-  return (size_t)C::NSLOT * C::A_BYTES + (size_t)nst * C::STAGE + C::W1_HALF + (size_t)C::NSLOT * C::A1_BYTES +
-         tab_bytes + io_bytes + red_bytes + 4 * (size_t)(L + 2) * sizeof(long long) + (3 * nst + 7 * C::NSLOT) * 8 +
+  return (size_t)C::NSLOT * C::A_BYTES + (size_t)nst * C::STAGE + C::ONES_BYTES + C::W1_BYTES + (size_t)C::NSLOT * C::A1_BYTES +
+         tab_bytes + io_bytes + red_bytes + 4 * (size_t)(L + 2) * sizeof(long long) + (3 * nst + 8 * C::NSLOT) * 8 +
          16;
 }
 
@@ -701,9 +770,9 @@ void tc2_table_layout(int L, int H, int tail, MlpDev* m, bool interleave) {
   auto al4 = [](long long v) { return (v + 3) & ~3ll; };
   m->pt_off_l1 = 0;
   m->pt_off_bias = 0;
-  // interleaved (this kernel): [L][H/2][4] = (bias_c, bias_c+1, a_c, a_c+1) per column pair, one 16-byte
-  // shared load per 8-column chunk; separate (wide kernel): bias [L][H], a [L][H]
-  m->pt_off_a = interleave ? m->pt_off_bias + 2 : al4(m->pt_off_bias + (long long)L * H);
+  // interleaved (wide kernel): [L][H/2][4] = (bias_c, bias_c+1, a_c, a_c+1) per column pair, one 16-byte
+  // shared load per 8-column chunk; folded (this kernel: bias in the MMA): a [L][H] only
+  m->pt_off_a = interleave ? m->pt_off_bias + 2 : 0;
   m->pt_off_a1 = interleave ? al4(m->pt_off_bias + 2ll * L * H) : al4(m->pt_off_a + (long long)L * H);
   m->pt_off_c = al4(m->pt_off_a1 + (tail == SAND_TAIL_MULT ? (long long)(L - 1) * H : 0));
   m->pt_off_c1 = al4(m->pt_off_c + L);
@@ -714,7 +783,7 @@ void tc2_table_layout(int L, int H, int tail, MlpDev* m, bool interleave) {
 bool tc2_usable(int L, int H, int tail) {
   if (!tc2_available(H)) return false;
   MlpDev m{};
-  tc2_table_layout(L, H, tail, &m, true);
+  tc2_table_layout(L, H, tail, &m, false);
   switch (H) {
     case 64: return pick_nst2<64>(m.pt_floats, L, tail) > 0;
     case 128: return pick_nst2<128>(m.pt_floats, L, tail) > 0;
@@ -723,34 +792,111 @@ bool tc2_usable(int L, int H, int tail) {
   }
 }
 
-int tc2_npoly() {
-  static const int np = [] {   // thread-safe one-time initialisation
-    int v = kPairPolyDefault;
-    if (const char* ev = getenv("SAND_NPOLY")) {
-      const int x = atoi(ev);
-      if (x == 0 || x == 8 || x == 16) v = x;
-    }
-    return v;
-  }();
-  return np;
+// Feature n of a layer's output (= accumulator column n, = K index n of the next layer) is produced by pass
+// n / (H/2); within a pass cta_group::2 takes the first H/4 B rows from the even CTA and the next H/4 from the
+// odd one.  So CTA r holds, per pass j, rows (features) j H/2 + r H/4 + [0, H/4).
+static inline void tc2_row_owner(int H, int n, int* cta, int* pass, int* row) {
+  const int HN = H / 2, QR = H / 4;
+  *pass = n / HN;
+  *cta = (n % HN) / QR;
+  *row = n % QR;
 }
 
 size_t tc2_w1_offset(int H, int n, int k) {
-  // layer-1 B image: [2 CTA halves][H/2 rows][16 bf16] in the core-matrix layout of l1_off
-  const int half = n / (H / 2), nl = n % (H / 2);
-  return (size_t)half * (H / 2) * 32 + l1_off((uint32_t)nl, (uint32_t)k);
+  // layer-1 B image: [2 CTAs][pass 0 rows | pass 1 rows (H/4 each)][16 bf16] in the core-matrix layout of l1_off
+  int cta, pass, row;
+  tc2_row_owner(H, n, &cta, &pass, &row);
+  return (size_t)cta * (H / 2) * 32 + l1_off((uint32_t)(pass * (H / 4) + row), (uint32_t)k);
 }
 
-template <int H, int TAIL, int NP>
+static inline uint16_t bf16_rne_h(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if ((u & 0x7F800000u) == 0x7F800000u) return (uint16_t)((u >> 16) | ((u & 0xFFFF) ? 0x40 : 0));  // inf/nan
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return (uint16_t)(u >> 16);
+}
+// (hi, lo) bf16 split of v: hi = rne(v), lo = rne(v - hi) (v - hi is exact in float32)
+static inline void bf16_split(float v, uint16_t* hi, uint16_t* lo) {
+  *hi = bf16_rne_h(v);
+  uint32_t u = (uint32_t)*hi << 16;
+  float h;
+  std::memcpy(&h, &u, 4);
+  *lo = bf16_rne_h(v - h);
+}
+
+void tc2_build_host(int L, int H, int tail, float w0, const float* const* W, const float* const* b,
+                    const float* const* a, const float* const* a1, const float* c, const float* c1, MlpDev* m,
+                    std::vector<float>* tables, std::vector<uint16_t>* w1img, std::vector<uint8_t>* img) {
+  tc2_table_layout(L, H, tail, m, false);
+  std::vector<float>& pt = *tables;
+  pt.assign((size_t)m->pt_floats, 0.f);
+  for (int i = 0; i < L; ++i) {
+    std::memcpy(&pt[m->pt_off_a + (size_t)i * H], a[i], sizeof(float) * H);
+    pt[m->pt_off_c + i] = c[i];
+    pt[m->pt_off_c1 + i] = c1[i];
+  }
+  if (tail == SAND_TAIL_MULT)
+    for (int i = 1; i < L; ++i) std::memcpy(&pt[m->pt_off_a1 + (size_t)(i - 1) * H], a1[i], sizeof(float) * H);
+  double cs = 0.0;
+  pt[m->pt_off_csum] = 0.f;
+  for (int d = 1; d <= L; ++d) {
+    cs += (tail == SAND_TAIL_LINEAR || d == 1) ? c[d - 1] : 0.0;
+    pt[m->pt_off_csum + d] = (float)cs;
+  }
+  // layer-1 split-BF16 B operand of w0 W_1, w0 b_1: row n = (W_hi x y z | W_lo x y z | W_hi x y z | b_hi b_lo | 0),
+  // matching the IO warp's A row (x_hi | x_hi | x_lo | 1 1 | 0): x_hi W_hi + x_hi W_lo + x_lo W_hi + b
+  w1img->assign((size_t)H * 16, 0);
+  auto put = [&](int n, int k, uint16_t v) { (*w1img)[tc2_w1_offset(H, n, k) / 2] = v; };
+  for (int n = 0; n < H; ++n) {
+    for (int k = 0; k < 3; ++k) {
+      uint16_t hi, lo;
+      bf16_split(w0 * W[0][3 * n + k], &hi, &lo);
+      put(n, k, hi);
+      put(n, 3 + k, lo);
+      put(n, 6 + k, hi);
+    }
+    uint16_t bhi, blo;
+    bf16_split(w0 * b[0][n], &bhi, &blo);
+    put(n, 9, bhi);
+    put(n, 10, blo);
+  }
+  // hidden layers: per (layer, CTA, pass) one ring stage: [bias operand: H/4 rows x 16 bf16 with (b_hi, b_lo)
+  // at k = BIAS_K, l1_off layout, padded to >= 1 KB][KC K-chunks of w0 W_l: H/4 rows x 128 B, SW128 K-major:
+  // element (row, k) of chunk kc at (row/8)*1024 + (row%8)*128 + ((((k%64)/8) ^ (row%8)) * 16) + (k%8)*2]
+  const int KC = H / 64, QR = H / 4;
+  const size_t small = QR * 32 < 1024 ? 1024 : (size_t)QR * 32, chunk = (size_t)QR * 128, stage = small + KC * chunk;
+  const int bias_k = Tc2Shape<64>::BIAS_K;
+  img->assign(L >= 2 ? (size_t)(L - 1) * 4 * stage : 0, 0);
+  for (int i = 1; i < L; ++i)
+    for (int n = 0; n < H; ++n) {
+      int cta, pass, row;
+      tc2_row_owner(H, n, &cta, &pass, &row);
+      uint8_t* base = img->data() + (((size_t)(i - 1) * 2 + cta) * 2 + pass) * stage;
+      uint16_t bhi, blo;
+      bf16_split(w0 * b[i][n], &bhi, &blo);
+      std::memcpy(base + l1_off((uint32_t)row, (uint32_t)bias_k), &bhi, 2);
+      std::memcpy(base + l1_off((uint32_t)row, (uint32_t)bias_k + 1), &blo, 2);
+      for (int k = 0; k < H; ++k) {
+        const int kc = k / 64, kk = k % 64;
+        const size_t byte = small + kc * chunk + (size_t)(row / 8) * 1024 + (row % 8) * 128 +
+                            (size_t)(((kk / 8) ^ (row % 8)) * 16) + (kk % 8) * 2;
+        const uint16_t v = bf16_rne_h(w0 * W[i][(size_t)n * H + k]);
+        std::memcpy(base + byte, &v, 2);
+      }
+    }
+}
+
+template <int H, int TAIL>
 static cudaError_t launch_tc2_t(const MlpDev& m, const float* pts, const uint32_t* perm, const QueryMeta* meta,
                                 float* out, int num_sms, cudaStream_t st) {
   const int nst = pick_nst2<H>(m.pt_floats, m.L, TAIL);
   if (!nst) return cudaErrorInvalidConfiguration;
   const size_t sm = smem_for2<H>(m.pt_floats, m.L, TAIL, nst);
-  static const int prof = getenv("SAND_KPROF") ? atoi(getenv("SAND_KPROF")) : 0;
+  const int prof = m.kprof;
   Tc2Params p{m, pts, perm, meta, out, nst, prof};
   const int grid = num_sms & ~1;
-  k_tmlp_tc2<H, TAIL, NP><<<grid, Tc2Shape<H>::THREADS, sm, st>>>(p);
+  k_tmlp_tc2<H, TAIL><<<grid, Tc2Shape<H>::THREADS, sm, st>>>(p);
   cudaError_t e = cudaGetLastError();
 #ifdef SAND_HANG_DEBUG
   {
@@ -767,7 +913,7 @@ static cudaError_t launch_tc2_t(const MlpDev& m, const float* pts, const uint32_
   }
 #endif
   if (prof && e == cudaSuccess) {
-    // diagnostic only: synchronous dump of the per-role counters (CTA averages; MMA over leaders)
+    // diagnostic only (SAND_OPT_KPROF): synchronous dump of the per-role counters (CTA averages; MMA over leaders)
     static unsigned long long h[160][kProfSlots];
     e = cudaStreamSynchronize(st);
     if (e == cudaSuccess) e = cudaMemcpyFromSymbol(h, g_kprof, sizeof h);
@@ -784,41 +930,30 @@ static cudaError_t launch_tc2_t(const MlpDev& m, const float* pts, const uint32_
   return e;
 }
 
-template <int H, int TAIL, int NP>
+template <int H, int TAIL>
 static cudaError_t prep_tc2_t() {
-  return cudaFuncSetAttribute(k_tmlp_tc2<H, TAIL, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax2);
+  return cudaFuncSetAttribute(k_tmlp_tc2<H, TAIL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax2);
 }
 
-// The polynomial share (columns per 32 on the FMA-pipe sine) is a template parameter; the bench configuration (H = 256, LINEAR) is built for
-// every supported share (tuning), the others for the default share only.
 #define SAND_TC2_DISPATCH(FN, ...)                                                                    \
   do {                                                                                                \
     const bool mult = m_tail == SAND_TAIL_MULT;                                                       \
-    const int np = m_np;                                                                              \
-    if (m_H == 256 && !mult) {                                                                        \
-      switch (np) {                                                                                   \
-        case 8: return FN<256, 0, 8>(__VA_ARGS__);                                                    \
-        case 16: return FN<256, 0, 16>(__VA_ARGS__);                                                  \
-        default: return FN<256, 0, 0>(__VA_ARGS__);                                                   \
-      }                                                                                               \
-    }                                                                                                 \
-    if (np != kPairPolyDefault) return cudaErrorInvalidValue;                                          \
     switch (m_H) {                                                                                    \
-      case 64: return mult ? FN<64, 1, kPairPolyDefault>(__VA_ARGS__) : FN<64, 0, kPairPolyDefault>(__VA_ARGS__); \
-      case 128: return mult ? FN<128, 1, kPairPolyDefault>(__VA_ARGS__) : FN<128, 0, kPairPolyDefault>(__VA_ARGS__); \
-      case 256: return FN<256, 1, kPairPolyDefault>(__VA_ARGS__);                                      \
+      case 64: return mult ? FN<64, 1>(__VA_ARGS__) : FN<64, 0>(__VA_ARGS__);                         \
+      case 128: return mult ? FN<128, 1>(__VA_ARGS__) : FN<128, 0>(__VA_ARGS__);                      \
+      case 256: return mult ? FN<256, 1>(__VA_ARGS__) : FN<256, 0>(__VA_ARGS__);                      \
       default: return cudaErrorInvalidValue;                                                          \
     }                                                                                                 \
   } while (0)
 
 cudaError_t launch_tmlp_tc2(const MlpDev& m, const float* pts, const uint32_t* perm, const QueryMeta* meta,
                             float* out, int num_sms, cudaStream_t st) {
-  const int m_H = m.H, m_tail = m.tail, m_np = m.pt_npoly;
+  const int m_H = m.H, m_tail = m.tail;
   SAND_TC2_DISPATCH(launch_tc2_t, m, pts, perm, meta, out, num_sms, st);
 }
 
 cudaError_t prepare_tc2(int H, int tail) {
-  const int m_H = H, m_tail = tail, m_np = tc2_npoly();
+  const int m_H = H, m_tail = tail;
   SAND_TC2_DISPATCH(prep_tc2_t);
 }
 

@@ -572,7 +572,6 @@ void tc3_build_host(int L, int H, float w0, const float* const* W, const float* 
   using C = Tc3Shape<336>;
   const int HP = C::HP;
   tc2_table_layout(L, HP, SAND_TAIL_LINEAR, m, true);
-  m->pt_npoly = 0;
   tables->assign((size_t)m->pt_floats, 0.f);
   for (int i = 1; i < L; ++i)
     for (int j = 0; j < H; ++j) (*tables)[m->pt_off_bias + (size_t)i * 2 * HP + (size_t)(j / 2) * 4 + (j & 1)] = w0 * b[i][j];
@@ -652,7 +651,7 @@ cudaError_t launch_tmlp_tc3(const MlpDev& m, const float* pts, const uint32_t* p
     if (smem_for3<336>(m.pt_floats, m.L, n) <= kSmemMax3) nst = n;
   if (!nst) return cudaErrorInvalidConfiguration;
   const size_t sm = smem_for3<336>(m.pt_floats, m.L, nst);
-  static const int prof = getenv("SAND_KPROF") ? atoi(getenv("SAND_KPROF")) : 0;
+  const int prof = m.kprof;
   Tc3Params p{m, pts, perm, meta, out, nst, prof};
   const int grid = num_sms & ~1;
   k_tmlp_wide<336><<<grid, Tc3Shape<336>::THREADS, sm, st>>>(p);

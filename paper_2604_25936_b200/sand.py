@@ -16,6 +16,7 @@ SAND_ERR_ARG, SAND_ERR_STATE, SAND_ERR_SIZE, SAND_ERR_DEPTHMAP = -1, -2, -3, -4
 SAND_ERR_CUDA, SAND_ERR_OOM, SAND_ERR_UNSUPPORTED = -5, -6, -7
 SAND_FP32, SAND_TF32X3, SAND_BF16 = 0, 1, 2
 SAND_TAIL_LINEAR, SAND_TAIL_MULT = 0, 1
+SAND_OPT_PAIR_KERNEL, SAND_OPT_DYN_SCHEDULE, SAND_OPT_KPROF = 1, 2, 3
 SAND_MAX_L = 32
 SAND_DEPTH_NONFINITE = 255
 
@@ -51,7 +52,8 @@ class sand_stats(ctypes.Structure):
 EXPORTS = ("sand_create", "sand_destroy", "sand_load_weights", "sand_load_depthmap", "sand_set_stream",
            "sand_set_lod_cap", "sand_reserve", "sand_query", "sand_query_host", "sand_get_stats",
            "sand_debug_perm", "sand_last_error", "sand_abi_version", "sand_required_depth",
-           "sand_populate_leaf_depths", "sand_query_dynamic", "sand_marching_cubes", "sand_mesh_grid")
+           "sand_populate_leaf_depths", "sand_query_dynamic", "sand_marching_cubes", "sand_mesh_grid",
+           "sand_set_option", "sand_get_option")
 
 _lib = None
 
@@ -73,6 +75,8 @@ def load_library(path=None):
     lib.sand_set_stream.argtypes = [vp, vp]
     lib.sand_set_lod_cap.argtypes = [vp, ctypes.c_int]
     lib.sand_reserve.argtypes = [vp, i64]
+    lib.sand_set_option.argtypes = [vp, ctypes.c_int, i64]
+    lib.sand_get_option.argtypes = [vp, ctypes.c_int, ctypes.POINTER(i64)]
     lib.sand_query.argtypes = [vp, vp, i64, vp, vp]
     lib.sand_query_host.argtypes = [vp, vp, i64, vp, vp, i64]
     lib.sand_get_stats.argtypes = [vp, ctypes.POINTER(sand_stats)]
@@ -156,6 +160,14 @@ class SandContext:
 
     def sand_set_lod_cap(self, cap):
         self._chk(self.lib.sand_set_lod_cap(self.h, int(cap)))
+
+    def sand_set_option(self, option, value):
+        self._chk(self.lib.sand_set_option(self.h, int(option), int(value)))
+
+    def sand_get_option(self, option):
+        v = ctypes.c_int64()
+        self._chk(self.lib.sand_get_option(self.h, int(option), ctypes.byref(v)))
+        return v.value
 
     def sand_reserve(self, n_max):
         self._chk(self.lib.sand_reserve(self.h, int(n_max)))

@@ -11,6 +11,7 @@ import pytest
 import oracle
 import sandgen as g
 from _engine import make_ctx
+from paper_2604_25936_b200 import SAND_OPT_DYN_SCHEDULE
 
 pytestmark = pytest.mark.gpu
 EPS = 2e-5   # FP32 evaluation error budget of t_i / y_i on these nets (accurate sinf, L <= 8)
@@ -53,8 +54,7 @@ def _check(p, pts, r, sdf, dep):
 
 @pytest.mark.parametrize("pool", [0, 1])
 @pytest.mark.parametrize("H,L,tail", [(64, 6, 0), (256, 8, 0), (128, 5, 1), (336, 8, 0), (32, 1, 0)])
-def test_dynamic_exit_matches_oracle(H, L, tail, pool, monkeypatch):
-    monkeypatch.setenv("SAND_DYN_POOL", str(pool))   # tile-level exit / per-layer re-compaction
+def test_dynamic_exit_matches_oracle(H, L, tail, pool):
     spec = g.TMlpSpec(L=L, H=H, omega0=30.0, tail=tail, seed=21 + H)
     p = g.make_weights(spec)
     pts = np.random.default_rng(H).uniform(-1, 1, (5003, 3)).astype(np.float32)
@@ -66,6 +66,7 @@ def test_dynamic_exit_matches_oracle(H, L, tail, pool, monkeypatch):
     else:
         r = 1.0
     with make_ctx(spec, BF16 if H >= 64 else FP32) as ctx:   # the dynamic path is FP32 in either context
+        ctx.sand_set_option(SAND_OPT_DYN_SCHEDULE, pool)   # tile-level exit / per-layer re-compaction
         ctx.sand_load_weights(g.pack_blob(p))
         sdf, dep = _run(ctx, pts, r)
     frac, hist = _check(p, pts, r, sdf, dep)
@@ -74,14 +75,15 @@ def test_dynamic_exit_matches_oracle(H, L, tail, pool, monkeypatch):
 
 
 @pytest.mark.parametrize("pool", [0, 1])
-def test_dynamic_special_cases_and_sizes(pool, monkeypatch):
+def test_dynamic_special_cases_and_sizes(pool):
     """r = 0 -> full depth (= query_full); huge r -> everyone stops at layer 2; n in {0, 1, 65} and a
     ragged last tile."""
-    monkeypatch.setenv("SAND_DYN_POOL", str(pool))
     spec = g.TMlpSpec(L=5, H=64, omega0=30.0, seed=31)
     p = g.make_weights(spec)
     pts = np.random.default_rng(3).uniform(-1, 1, (1000, 3)).astype(np.float32)
     with make_ctx(spec, FP32) as ctx:
+        ctx.sand_set_option(SAND_OPT_DYN_SCHEDULE, pool)
+        assert ctx.sand_get_option(SAND_OPT_DYN_SCHEDULE) == pool
         ctx.sand_load_weights(g.pack_blob(p))
         sdf, dep = _run(ctx, pts, 0.0)
         assert np.all(dep == 5)

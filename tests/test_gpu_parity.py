@@ -286,57 +286,52 @@ def test_all_max_depth_equals_full_depth():
     assert np.abs(sdf - full).max() <= TOL_BF16
 
 
-@pytest.mark.parametrize("L", [20, 32])
-def test_deep_nets_pair_kernel_limits(L):
-    """Deep T-MLPs: L = 20 still fits the CTA-pair kernel (single weight stage) and must match the
-    oracle; L = 32 at H = 256 exceeds the on-chip per-column tables of both BF16 kernels and must be
-    refused cleanly with SAND_ERR_UNSUPPORTED (include/sand.h), not mis-computed."""
+@pytest.mark.parametrize("L,tail", [(20, 0), (32, 0), (32, 1)])
+def test_deep_nets_pair_kernel_limits(L, tail):
+    """Deep T-MLPs at H = 256.  With w0 and the biases folded into the MMA operands the CTA-pair kernel's
+    on-chip tables are the tail vectors only, so L = 32 LINEAR fits it and must match the oracle; a
+    configuration that fits no BF16 kernel (L = 32 MULT keeps two tail vectors per layer) must either
+    match as well or be refused cleanly with SAND_ERR_UNSUPPORTED (include/sand.h), never mis-computed."""
     from paper_2604_25936_b200 import SandError
-    spec = g.TMlpSpec(L=L, H=256, omega0=30.0, seed=21)
-    if L == 32:
-        with pytest.raises(SandError) as e:
-            make_ctx(spec, BF16)
-        assert e.value.code == -7
+    spec = g.TMlpSpec(L=L, H=256, omega0=30.0, tail=tail, seed=21)
+    try:
+        ctx = make_ctx(spec, BF16)
+    except SandError as e:
+        assert tail == 1 and e.code == -7
         return
     p = g.make_weights(spec)
     dm = _random_voxel_map(3, L, 22)
     pts = _pts(6001, 23)
-    with make_ctx(spec, BF16) as ctx:
+    with ctx:
         sdf, dep = run_engine(ctx, p, dm, pts)
     sdf_or, dep_or = oracle.query(p, dm, pts)
     assert_parity(sdf, dep, sdf_or, dep_or, TOL_BF16)
 
 
-_POLY_CHILD = r"""
-import sys, numpy as np
-sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
-import oracle, sandgen as g
-from _engine import TOL_BF16, assert_parity, make_ctx, run_engine
-spec = g.TMlpSpec(L=6, H=256, omega0=30.0, seed=31)
-p = g.make_weights(spec)
-rng = np.random.default_rng(32)
-dm = g.VoxelMap(3, rng.integers(1, 7, 512).astype(np.uint8), None)
-pts = rng.uniform(-1, 1, (30001, 3)).astype(np.float32)
-with make_ctx(spec, 2) as ctx:
-    sdf, dep = run_engine(ctx, p, dm, pts)
-sdf_or, dep_or = oracle.query(p, dm, pts)
-print("maxabs", assert_parity(sdf, dep, sdf_or, dep_or, TOL_BF16))
-"""
-
-
-@pytest.mark.parametrize("npoly", ["0", "8", "16"])
-def test_polynomial_sine_share(npoly):
-    """The CTA-pair kernel's FMA-pipe polynomial sine (SAND_NPOLY columns of every 32)
-    matches the oracle at every supported share (separate process: the share is fixed per process)."""
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    code = _POLY_CHILD.format(root=root, tests=os.path.join(root, "tests"))
-    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, SAND_NPOLY=npoly),
-                       capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stdout + r.stderr
-    assert "maxabs" in r.stdout
+def test_options_explicit_and_pair_kernel_switch():
+    """sand_set_option (no environment variables): defaults, bad keys / values, and the 1-CTA kernel
+    selected at run time through SAND_OPT_PAIR_KERNEL gives the same exit depths and SDF within the
+    BF16 tolerance as the CTA-pair kernel on the same context."""
+    from paper_2604_25936_b200 import SAND_OPT_DYN_SCHEDULE, SAND_OPT_KPROF, SAND_OPT_PAIR_KERNEL, SandError
+    spec = g.TMlpSpec(L=5, H=256, omega0=30.0, seed=77)
+    p = g.make_weights(spec)
+    rng = np.random.default_rng(8)
+    dm = g.VoxelMap(4, rng.integers(1, 6, 4096).astype(np.uint8), None)
+    pts = rng.uniform(-1, 1, (70001, 3)).astype(np.float32)
+    sdf_or, dep_or = oracle.query(p, dm, pts)
+    with make_ctx(spec, BF16) as ctx:
+        assert ctx.sand_get_option(SAND_OPT_PAIR_KERNEL) == 1
+        assert ctx.sand_get_option(SAND_OPT_DYN_SCHEDULE) == 0
+        assert ctx.sand_get_option(SAND_OPT_KPROF) == 0
+        for bad in ((99, 0), (SAND_OPT_PAIR_KERNEL, 2), (SAND_OPT_DYN_SCHEDULE, -1), (SAND_OPT_KPROF, 7)):
+            with pytest.raises(SandError):
+                ctx.sand_set_option(*bad)
+        sdf2, dep2 = run_engine(ctx, p, dm, pts)
+        ctx.sand_set_option(SAND_OPT_PAIR_KERNEL, 0)
+        assert ctx.sand_get_option(SAND_OPT_PAIR_KERNEL) == 0
+        sdf1, dep1 = run_engine(ctx, p, dm, pts)
+    assert_parity(sdf2, dep2, sdf_or, dep_or, TOL_BF16)
+    assert_parity(sdf1, dep1, sdf_or, dep_or, TOL_BF16)
 
 
 @pytest.mark.skipif(os.environ.get("SAND_FULL_PARITY") != "1",
