@@ -8,6 +8,15 @@ TOL_FP32 = 1e-4   # BASELINE.json north_star: FP32/TF32 path max-abs
 SIGN_EPS = 5e-3   # sign must agree wherever |f_oracle| > 5e-3
 
 
+def oracle_query(params, depthmap, points, lod_cap=None):
+    """The GPU parity reference: the plain FP32 C oracle (oracle/sand_oracle_fp32.c, BASELINE.json's
+    north-star oracle; pinned against the float64 numpy oracle by tests/test_oracle_fp32.py).  Returns
+    (sdf float64 [n], exit depth u8 [n]) like oracle.query."""
+    from oracle import fp32
+    sdf, dep = fp32.query_fp32(params, depthmap, points, lod_cap=lod_cap)
+    return sdf.astype(np.float64), dep
+
+
 def make_ctx(spec, precision, device=0):
     from paper_2604_25936_b200 import SandContext
     return SandContext(spec.L, spec.H, spec.omega0, precision, spec.tail, device)

@@ -10,7 +10,8 @@ import pytest
 
 import oracle
 import sandgen as g
-from _engine import (TOL_BF16, TOL_FP32, assert_parity, make_ctx, run_engine, stratified_sample)
+from _engine import (TOL_BF16, TOL_FP32, assert_parity, make_ctx, oracle_query, run_engine,
+                     stratified_sample)
 
 pytestmark = pytest.mark.gpu
 
@@ -41,7 +42,7 @@ def test_bf16_random_depths_small(H, tail):
     pts = _pts(7001, 2)
     with make_ctx(spec, BF16) as ctx:
         sdf, dep = run_engine(ctx, p, dm, pts)
-    sdf_or, dep_or = oracle.query(p, dm, pts)
+    sdf_or, dep_or = oracle_query(p, dm, pts)
     assert_parity(sdf, dep, sdf_or, dep_or, TOL_BF16)
 
 
@@ -55,7 +56,7 @@ def test_bf16_wide_pair_kernel(L):
     pts = _pts(60007, 12)
     with make_ctx(spec, BF16) as ctx:
         sdf, dep = run_engine(ctx, p, dm, pts)
-    sdf_or, dep_or = oracle.query(p, dm, pts)
+    sdf_or, dep_or = oracle_query(p, dm, pts)
     assert_parity(sdf, dep, sdf_or, dep_or, TOL_BF16)
 
 
@@ -69,7 +70,7 @@ def test_fp32_random_depths_small(H, tail):
     pts = _pts(5003, 4)
     with make_ctx(spec, FP32) as ctx:
         sdf, dep = run_engine(ctx, p, dm, pts)
-    sdf_or, dep_or = oracle.query(p, dm, pts)
+    sdf_or, dep_or = oracle_query(p, dm, pts)
     assert_parity(sdf, dep, sdf_or, dep_or, TOL_FP32)
 
 
@@ -82,7 +83,7 @@ def test_fp32_wide_deep_net():
     pts = _pts(40011, 6)
     with make_ctx(spec, FP32) as ctx:
         sdf, dep = run_engine(ctx, p, dm, pts)
-    sdf_or, dep_or = oracle.query(p, dm, pts)
+    sdf_or, dep_or = oracle_query(p, dm, pts)
     assert_parity(sdf, dep, sdf_or, dep_or, TOL_FP32)
 
 
@@ -94,7 +95,7 @@ def test_C0_full_fp32():
     with make_ctx(c.spec, FP32) as ctx:
         sdf, dep = run_engine(ctx, p, c.depthmap, pts)
         st = ctx.sand_get_stats()
-    sdf_or, dep_or = oracle.query(p, c.depthmap, pts)
+    sdf_or, dep_or = oracle_query(p, c.depthmap, pts)
     assert_parity(sdf, dep, sdf_or, dep_or, TOL_FP32)
     assert sum(st["per_depth"]) + st["n_nonfinite"] == pts.shape[0]
     np.testing.assert_array_equal(st["per_depth"], np.bincount(dep_or, minlength=c.spec.L + 1))
@@ -111,7 +112,7 @@ def test_C1_full_bf16():
     d_or, _, _ = oracle.lookup(c.depthmap, pts)
     np.testing.assert_array_equal(dep, d_or)
     idx = stratified_sample(dep, 4096, 1 << 16, seed=1)
-    sdf_or, dep_or = oracle.query(p, c.depthmap, pts[idx])
+    sdf_or, dep_or = oracle_query(p, c.depthmap, pts[idx])
     assert_parity(sdf, dep, sdf_or, dep_or, TOL_BF16, idx=idx)
 
 
@@ -133,7 +134,7 @@ def test_C2_C3_full_size_sampled(name):
         d_or, _, _ = oracle.lookup(c.depthmap, pts[q0:q0 + step])
         np.testing.assert_array_equal(dep[q0:q0 + step], d_or)
     idx = stratified_sample(dep, 4096, 1 << 15, seed=2)
-    sdf_or, dep_or = oracle.query(p, c.depthmap, pts[idx])
+    sdf_or, dep_or = oracle_query(p, c.depthmap, pts[idx])
     assert_parity(sdf, dep, sdf_or, dep_or, TOL_BF16, idx=idx)
     assert sum(st["per_depth"]) + st["n_nonfinite"] == n
     assert st["per_depth"][0] == 0   # BJ configs have no far leaves
@@ -151,7 +152,7 @@ def test_far_field_and_lod_caps(prec, H):
     with make_ctx(spec, prec) as ctx:
         for cap in (1, 2, 3, L):
             sdf, dep = run_engine(ctx, p, dm, pts, cap=cap)
-            sdf_or, dep_or = oracle.query(p, dm, pts, lod_cap=cap)
+            sdf_or, dep_or = oracle_query(p, dm, pts, lod_cap=cap)
             assert_parity(sdf, dep, sdf_or, dep_or, tol)
     far = dep_or == 0
     assert far.any()
@@ -173,7 +174,7 @@ def test_octree_descent_and_baked_paths():
                             subdivide_factor=0.3)
         with make_ctx(spec, BF16) as ctx:
             sdf, dep = run_engine(ctx, p, oc, pts)
-        sdf_or, dep_or = oracle.query(p, oc, pts)
+        sdf_or, dep_or = oracle_query(p, oc, pts)
         assert_parity(sdf, dep, sdf_or, dep_or, TOL_BF16)
 
 
@@ -193,7 +194,7 @@ def test_nonfinite_and_edge_sizes():
         ctx.sand_load_depthmap(dm)
         for n in (0, 1, 3, 129, 200):
             pts = base[:n]
-            sdf_or, dep_or = oracle.query(p, dm, pts)
+            sdf_or, dep_or = oracle_query(p, dm, pts)
             sdf, dep = run_engine(ctx, p, dm, pts) if n else (np.zeros(0, np.float32), np.zeros(0, np.uint8))
             if n:
                 assert_parity(sdf, dep, sdf_or, dep_or, TOL_BF16)
@@ -204,7 +205,7 @@ def test_nonfinite_and_edge_sizes():
         ctx.sand_set_stream(torch.cuda.current_stream().cuda_stream)
         ctx.sand_query(flat.data_ptr() + 4, 200, sdf_t.data_ptr(), dep_t.data_ptr() + 1)
         torch.cuda.synchronize()
-        sdf_or, dep_or = oracle.query(p, dm, base)
+        sdf_or, dep_or = oracle_query(p, dm, base)
         assert_parity(sdf_t.cpu().numpy(), dep_t.cpu().numpy()[1:], sdf_or, dep_or, TOL_BF16)
 
 
@@ -219,7 +220,7 @@ def test_binning_is_stable_depth_partition():
     with make_ctx(spec, BF16) as ctx:
         _, dep = run_engine(ctx, p, dm, pts)
         perm = ctx.sand_debug_perm()
-    _, dep_or = oracle.query(p, dm, pts)
+    _, dep_or = oracle_query(p, dm, pts)
     expect = np.concatenate([np.nonzero(dep_or == d)[0] for d in range(L, 0, -1)])
     np.testing.assert_array_equal(perm, expect.astype(np.uint32))
 
@@ -304,7 +305,7 @@ def test_deep_nets_pair_kernel_limits(L, tail):
     pts = _pts(6001, 23)
     with ctx:
         sdf, dep = run_engine(ctx, p, dm, pts)
-    sdf_or, dep_or = oracle.query(p, dm, pts)
+    sdf_or, dep_or = oracle_query(p, dm, pts)
     assert_parity(sdf, dep, sdf_or, dep_or, TOL_BF16)
 
 
@@ -318,7 +319,7 @@ def test_options_explicit_and_pair_kernel_switch():
     rng = np.random.default_rng(8)
     dm = g.VoxelMap(4, rng.integers(1, 6, 4096).astype(np.uint8), None)
     pts = rng.uniform(-1, 1, (70001, 3)).astype(np.float32)
-    sdf_or, dep_or = oracle.query(p, dm, pts)
+    sdf_or, dep_or = oracle_query(p, dm, pts)
     with make_ctx(spec, BF16) as ctx:
         assert ctx.sand_get_option(SAND_OPT_PAIR_KERNEL) == 1
         assert ctx.sand_get_option(SAND_OPT_DYN_SCHEDULE) == 0
@@ -334,18 +335,23 @@ def test_options_explicit_and_pair_kernel_switch():
     assert_parity(sdf1, dep1, sdf_or, dep_or, TOL_BF16)
 
 
-@pytest.mark.skipif(os.environ.get("SAND_FULL_PARITY") != "1",
-                    reason="opt-in (SAND_FULL_PARITY=1): the fp64 oracle on every point (C2: ~20 min)")
-@pytest.mark.parametrize("name", ["C1", "C2", "C3"])
+@pytest.mark.parametrize("name", [
+    "C1",
+    pytest.param("C2", marks=pytest.mark.skipif(os.environ.get("SAND_FULL_PARITY") != "1",
+                                                reason="opt-in (SAND_FULL_PARITY=1): 134M points on the CPU oracle")),
+    pytest.param("C3", marks=pytest.mark.skipif(os.environ.get("SAND_FULL_PARITY") != "1",
+                                                reason="opt-in (SAND_FULL_PARITY=1)")),
+])
 def test_full_sdf_all_points(name):
-    """SDF of EVERY point of configs[1..3] against the oracle (the default suite samples it)."""
+    """SDF of EVERY point of configs[1..3] against the FP32 C oracle (OpenMP on the host
+    cores).  C1 (16.8M points) runs in the default suite; C2 / C3 are opt-in (their default tests sample)."""
     c = g.make_config(name)
     p = c.params()
     pts = c.points_fn()
     with make_ctx(c.spec, BF16) as ctx:
         sdf, dep = run_engine(ctx, p, c.depthmap, pts)
-    step = 1 << 20
+    step = 1 << 22
     for q0 in range(0, pts.shape[0], step):
         idx = np.arange(q0, min(q0 + step, pts.shape[0]))
-        sdf_or, dep_or = oracle.query(p, c.depthmap, pts[idx])
+        sdf_or, dep_or = oracle_query(p, c.depthmap, pts[idx])
         assert_parity(sdf, dep, sdf_or, dep_or, TOL_BF16, idx=idx)
