@@ -99,14 +99,25 @@ def _dist():
 
 def _arm_config(args, c, ws, wl_desc, global_points):
     """The `config` object of the bench line -- identical for this arm and the reference arm."""
-    return {"workload": wl_desc if ws == 1 else f"{args.config} weak-scaled: {c.grid_R}x{c.grid_R}x{c.grid_R * ws} grid, "
-            "work-balanced z-slabs" if c.grid_R is not None else f"{args.config} x {ws} ranks",
+    weak = args.scaling == "weak"
+    if ws == 1:
+        wl = wl_desc
+    elif c.grid_R is not None:
+        R = c.grid_R
+        wl = (f"{args.config} weak-scaled: {R}x{R}x{R * ws} grid" if weak else
+              f"{args.config} strong-scaled: the fixed {R}x{R}x{R} grid") + f", work-balanced z-slabs over {ws} ranks"
+    else:
+        wl = f"{args.config} x {ws} ranks" if weak else f"{args.config} split over {ws} ranks"
+    dmap = {"C0": "32^3 voxel sphere map", "C1": "128^3 voxel 16-sphere map",
+            "C2": "level-7 sphere-union octree (baked 128^3)", "C3": "level-7 sphere-union octree (baked 128^3)",
+            "C4": "level-8 sphere-union octree (baked 256^3)"}[args.config]
+    per_rank = 12 * global_points / (1 if weak else ws)
+    return {"workload": wl,
             "model": f"{c.spec.L}x{c.spec.H} SIREN T-MLP (seeded SIREN init), linear tails",
-            "depth_map": "level-7 sphere-union octree (baked 128^3)" if args.config == "C2" else args.config,
-            "global_points": global_points, "parallelism": f"dp{ws} (z-slab shards)",
-            "l2": (f"inputs {12 * global_points / ws / 1e9:.2f} GB per rank > 126 MB L2; no flush needed"
-                   if 12 * global_points / ws >= 126e6 else
-                   f"inputs {12 * global_points / ws / 1e6:.0f} MB per rank < 126 MB L2: a 256 MB buffer is "
+            "depth_map": dmap, "global_points": global_points, "parallelism": f"dp{ws} (z-slab shards)",
+            "l2": (f"inputs {per_rank / 1e9:.2f} GB per rank > 126 MB L2; no flush needed"
+                   if per_rank >= 126e6 else
+                   f"inputs {per_rank / 1e6:.0f} MB per rank < 126 MB L2: a 256 MB buffer is "
                    "written before every step (outside the per-step CUDA events)"),
             "full_depth_baseline": bool(args.full_depth)}
 
@@ -119,13 +130,13 @@ def _n1_workload(args, c):
 
 
 def run_reference(args):
-    """--impl reference: the oracle (oracle/), as it stands, on the host cores, on a bounded
-    seeded sample of the same workload per step.  Rank 0 only."""
+    """--impl reference: the plain FP32 C oracle (oracle/sand_oracle_fp32.c, OpenMP over the host cores), as it
+    stands, on a bounded seeded sample of the same workload per step.  Rank 0 only."""
     ws, rank, _ = _dist()
     if rank != 0:
         return 0
-    import oracle
     import sandgen as g
+    from oracle import fp32 as ofp
     c = g.make_config(args.config)
     p = c.params()
     R = c.grid_R
@@ -135,36 +146,40 @@ def run_reference(args):
     n_work = R ** 3 if R is not None else cloud.shape[0]
     times = []
     for it in range(args.warmup + args.steps):
-        lin = np.sort(rng.choice(n_work, n_step, replace=False))
         if R is not None:
-            ax = g.grid_axis(R)
-            pts = np.stack([ax[lin % R], ax[(lin // R) % R], ax[lin // (R * R)]], axis=1).astype(np.float32)
+            pts = _sample_grid_points(R, 0, R, R, n_step, rng)
         else:
-            pts = cloud[lin]
+            pts = cloud[np.sort(rng.choice(n_work, n_step, replace=False))]
         t0 = time.perf_counter()
-        oracle.query(p, c.depthmap, pts)
+        ofp.query_fp32(p, c.depthmap, pts)
         dt = time.perf_counter() - t0
         if it >= args.warmup:
             times.append(dt)
     ms = 1e3 * float(np.mean(times))
     val = n_step / (ms / 1e3)
-    cores = _cores()
     sample = (f"{n_step} seeded random vertices of the {R}^3 grid per step" if R is not None else
               f"{n_step} seeded random points of the {n_work}-point cloud per step")
+    global_points = n_work * ws if (R is not None and args.scaling == "weak") else n_work
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": _arm_config(args, c, ws, _n1_workload(args, c), n_work * ws if R is not None else n_work),
-            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak" if args.scaling == "weak" else "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": _arm_config(args, c, ws, _n1_workload(args, c), global_points),
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": ofp.threads(), "cpu": ofp.cpu_model(),
+                             "kind": "oracle (plain FP32 C, OpenMP, -ffp-contract=off)", "sample": sample},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
+TRAFFIC_FILE = "r02_k3_traffic.json"
+TRAFFIC_SRC = f"profiles/{TRAFFIC_FILE} (ncu --set full of this round's kernel, dram read+write per launch)"
+
+
 def _traffic():
     """DRAM bytes per K3 launch from the committed ncu --set full capture (profiles/), or None."""
     try:
-        t = json.load(open(os.path.join(ROOT, "profiles", "r01_k3_traffic.json")))
+        t = json.load(open(os.path.join(ROOT, "profiles", TRAFFIC_FILE)))
         return t["dram_bytes_per_launch"]
     except Exception:
         return None
@@ -203,19 +218,19 @@ def _cores():
     return os.cpu_count()
 
 
-def cpu_baseline(p, depthmap, pts, budget_s):
-    """Oracle timed on host cores on a bounded seeded sample of this workload (rank 0, N = 1)."""
-    import oracle
-    rng = np.random.default_rng(99)
+def cpu_baseline(p, depthmap, sampler, budget_s):
+    """The plain FP32 C oracle timed on the host cores (OpenMP, all usable cores) on bounded seeded samples of
+    this workload (rank 0, N = 1): chunks of 2^15 points drawn by `sampler(m)` until ~budget_s of oracle time."""
+    from oracle import fp32 as ofp
     done, t_used, chunk = 0, 0.0, 1 << 15
-    while t_used < budget_s and done < (1 << 21):
-        idx = np.sort(rng.choice(pts.shape[0], chunk, replace=False))
-        s = pts[idx]
+    while t_used < budget_s and done < (1 << 22):
+        s = sampler(chunk)
         t0 = time.perf_counter()
-        oracle.query(p, depthmap, s)
+        ofp.query_fp32(p, depthmap, s)
         t_used += time.perf_counter() - t0
-        done += chunk
-    return {"value": done / t_used, "unit": UNIT, "cores": _cores(), "kind": "oracle",
+        done += s.shape[0]
+    return {"value": done / t_used, "unit": UNIT, "cores": ofp.threads(), "cpu": ofp.cpu_model(),
+            "kind": "oracle (plain FP32 C, OpenMP, -ffp-contract=off)",
             "sample": f"{done} seeded random points of the workload ({t_used:.1f} s of oracle time)"}
 
 
@@ -269,7 +284,8 @@ def run_populate(args):
         t0 = time.perf_counter()
         oracle.populate_leaf_depths(p, samples[:k], r)
         dt = time.perf_counter() - t0
-        cpu = {"value": k * spl / dt, "unit": "samples/s", "cores": _cores(), "kind": "oracle",
+        cpu = {"value": k * spl / dt, "unit": "samples/s", "cores": _cores(), "kind": "oracle (numpy float64)",
+               "cores_note": "BLAS pool for the matmuls; sin, lookup and the Eq. 5 decision on one core",
                "sample": f"first {k} leaves x {spl} samples"}
     line = {"task": "populate", "metric": "depth-map population samples/sec (Eq. 5 + Eq. 6)",
             "value": ns / (ms / 1e3), "unit": "samples/s", "n_gpus": 1, "steps": args.steps,
@@ -421,7 +437,8 @@ def run_dynamic(args):
         t0 = time.perf_counter()
         oracle.query_dynamic(p, pts_np[:k], r30)
         dt = time.perf_counter() - t0
-        cpu = {"value": k / dt, "unit": UNIT, "cores": _cores(), "kind": "oracle",
+        cpu = {"value": k / dt, "unit": UNIT, "cores": _cores(), "kind": "oracle (numpy float64)",
+               "cores_note": "BLAS pool for the matmuls; sin and the exit test on one core",
                "sample": f"first {k} grid points, r = {r30:.3e}"}
     line = {"task": "dynamic", "metric": "dynamic-exit (no octree) SDF queries/sec vs the octree path",
             "unit": UNIT, "n_gpus": 1, "steps": steps, "warmup": args.warmup, "higher_is_better": True,
@@ -496,45 +513,54 @@ def run_mesh(args):
     return 0
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", default="sand", choices=["sand", "reference"])
-    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4"])
-    ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--e2e-chunk", type=int, default=0, help="points per host-pipeline chunk (0: library default)")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--ref-sample", type=int, default=1 << 15)
-    ap.add_argument("--full-depth", action="store_true", help="all-L depth map (non-adaptive GPU baseline)")
-    ap.add_argument("--kprof", type=int, default=0, help="diagnostic SAND_OPT_KPROF (per-role counters, stderr)")
-    ap.add_argument("--prec", default="bf16", choices=["bf16", "fp32"],
-                    help="fp32: the accurate FP32 path (register-blocked SIMT GEMM), reported against the FP32 ALU peak")
-    ap.add_argument("--task", default="query", choices=["query", "populate", "sweep", "dynamic", "mesh"],
-                    help="query: the adaptive SDF query path (BASELINE metric); populate: depth-map "
-                         "population (Eq. 5/6, SURVEY 8(f) NEXT #1) on the config's finest octree leaves")
-    args = ap.parse_args()
-    if args.warmup < 3:
-        args.warmup = 3  # timing rule: at least 3 warm-up steps
-    if args.impl == "reference":
-        return run_reference(args)
-    if args.task == "populate":
-        return run_populate(args)
-    if args.task == "sweep":
-        return run_sweep(args)
-    if args.task == "dynamic":
-        return run_dynamic(args)
-    if args.task == "mesh":
-        return run_mesh(args)
+def _free_port():
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
 
+
+def _relaunch(args):
+    """`--gpus N` (N > 1) without a torchrun environment: re-exec this command under
+    torch.distributed.run with one rank per GPU (rendezvous on 127.0.0.1)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    print(f"[bench] --gpus {args.gpus}: launching {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
+def _grid_slab_device(R, k0, k1, Rz, dev):
+    """Points of z-planes [k0, k1) of the R x R x Rz vertex grid, generated on the device from the same float32
+    axis values as sandgen.grid_points_slab (x fastest): float32 [n][3]."""
+    import torch
+    import sandgen as g
+    ax = torch.from_numpy(g.grid_axis(R)).to(dev)
+    az = torch.from_numpy(g.grid_axis(Rz)[k0:k1].copy()).to(dev)
+    nz = k1 - k0
+    out = torch.empty((nz, R, R, 3), dtype=torch.float32, device=dev)
+    out[..., 0] = ax.view(1, 1, R)
+    out[..., 1] = ax.view(1, R, 1)
+    out[..., 2] = az.view(nz, 1, 1)
+    return out.view(-1, 3)
+
+
+def _sample_grid_points(R, k0, k1, Rz, n, rng):
+    """n seeded random vertices of z-planes [k0, k1) of the R x R x Rz grid (host, float32 [n][3])."""
+    import sandgen as g
+    tot = (k1 - k0) * R * R
+    lin = np.sort(rng.choice(tot, min(n, tot), replace=False))
+    ax, az = g.grid_axis(R), g.grid_axis(Rz)
+    return np.stack([ax[lin % R], ax[(lin // R) % R], az[k0 + lin // (R * R)]], axis=1).astype(np.float32)
+
+
+def run_query(args):
+    """The BASELINE metric: sand_query over the configuration's points, one rank per GPU."""
     import torch
     import torch.distributed as dist
 
     import sandgen as g
-    from paper_2604_25936_b200 import SAND_BF16, SandContext, partition
+    from paper_2604_25936_b200 import SAND_BF16, SAND_FP32, SandContext, partition
 
     ws, rank, local = _dist()
     # one process per GPU; SAND_BENCH_SHARE_GPU=1 (test only) maps several ranks onto the visible GPUs
@@ -544,34 +570,46 @@ def main():
     dev_index = local % torch.cuda.device_count() if share else local
     torch.cuda.set_device(dev_index)
     dev = torch.device("cuda", dev_index)
+    comm = None
     if ws > 1:
         if share:
             dist.init_process_group("gloo")
         else:
+            os.environ.setdefault("NCCL_DEBUG", "INFO")            # NCCL logs its communicator (nranks) init
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
+        comm = {"backend": dist.get_backend(), "nranks": dist.get_world_size(),
+                "collective": f"all_gather_into_tensor of {partition.RECORD_FIELDS} int64 per rank (after the timed region)"}
+        if rank == 0:
+            print(f"[bench] communicator: backend={comm['backend']} nranks={comm['nranks']}", file=sys.stderr, flush=True)
 
     c = g.make_config(args.config)
     p = c.params()
     dm = c.depthmap
+    fp32 = args.prec == "fp32" or (args.prec is None and c.precision == SAND_FP32)
     if args.full_depth:
         dm = g.VoxelMap(1, np.full(8, c.spec.L, np.uint8), None)
+    weak = args.scaling == "weak"
     if c.grid_R is not None:
-        k0, k1, Rz = partition.shard_planes(c.depthmap, c.grid_R, ws, rank, weak=True)
-        pts_np = g.grid_points_slab(c.grid_R, k0, k1, Rz)
+        k0, k1, Rz = partition.shard_planes(c.depthmap, c.grid_R, ws, rank, weak=weak)
+        pts = _grid_slab_device(c.grid_R, k0, k1, Rz, dev)
         wl_desc = f"{args.config}: {c.grid_R}x{c.grid_R}x{Rz} grid, z-planes [{k0},{k1}) on rank {rank}"
+        base_index = k0 * c.grid_R * c.grid_R
     else:
         pts_all = c.points_fn()
         n_all = pts_all.shape[0]
-        k0, k1, Rz = n_all * rank // ws, n_all * (rank + 1) // ws, None
-        pts_np = pts_all[k0:k1]
+        if weak:   # every rank queries the whole cloud (global indices offset by rank)
+            k0, k1, Rz = rank * n_all, (rank + 1) * n_all, None
+            pts = torch.from_numpy(pts_all).to(dev)
+        else:
+            k0, k1, Rz = n_all * rank // ws, n_all * (rank + 1) // ws, None
+            pts = torch.from_numpy(np.ascontiguousarray(pts_all[k0:k1])).to(dev)
         wl_desc = f"{args.config}: points [{k0},{k1})"
-    n = pts_np.shape[0]
-    pts = torch.from_numpy(pts_np).to(dev)
+        base_index = k0
+    n = pts.shape[0]
     sdf = torch.empty(n, dtype=torch.float32, device=dev)
     dep = torch.empty(n, dtype=torch.uint8, device=dev)
 
-    from paper_2604_25936_b200 import SAND_FP32
-    fp32 = args.prec == "fp32"
     ctx = SandContext(c.spec.L, c.spec.H, c.spec.omega0, SAND_FP32 if fp32 else SAND_BF16, c.spec.tail, dev_index)
     if args.kprof:
         from paper_2604_25936_b200 import SAND_OPT_KPROF
@@ -582,46 +620,73 @@ def main():
     stream = torch.cuda.current_stream(dev)
     ctx.sand_set_stream(stream.cuda_stream)
 
-    for _ in range(args.warmup):
+    def query():
         ctx.sand_query(pts.data_ptr(), n, sdf.data_ptr(), dep.data_ptr())
-    st0 = ctx.sand_get_stats()          # synchronises; resets the per-query event sums
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    # inputs smaller than L2 (side configs such as C0, C3): flush L2 before every step by writing a buffer
+    # larger than it, and time the steps one by one (the flush outside the events)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if 12 * n < 126e6 else None
+
+    def timed(k):
+        """k steps, CUDA events on the launching stream; returns device ms summed over the steps."""
+        if flush is None:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(k):
+                query()
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            return e0.elapsed_time(e1)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k)]
+        for a_, b_ in evs:
+            flush.fill_(1)
+            a_.record(stream)
+            query()
+            b_.record(stream)
+        torch.cuda.synchronize(dev)
+        return sum(a_.elapsed_time(b_) for a_, b_ in evs)
+
+    for _ in range(args.warmup):
+        query()
+    ctx.sand_get_stats()          # synchronises; resets the per-query event sums
     clk = ClockSampler(dev_index)
     torch.cuda.synchronize(dev)
     if ws > 1:
         dist.barrier()
-    # inputs smaller than L2 (side configs such as C3): flush L2 before every step by writing a buffer
-    # larger than it, and time the steps one by one (the flush outside the events)
-    flush = None
-    if 12 * n < 126e6:
-        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     clk.start()
-    if flush is None:
-        e0.record(stream)
-        for _ in range(args.steps):
-            ctx.sand_query(pts.data_ptr(), n, sdf.data_ptr(), dep.data_ptr())
-        e1.record(stream)
-    else:
-        for a_, b_ in evs:
-            flush.fill_(1)
-            a_.record(stream)
-            ctx.sand_query(pts.data_ptr(), n, sdf.data_ptr(), dep.data_ptr())
-            b_.record(stream)
-    torch.cuda.synchronize(dev)
+    ms_total = timed(args.steps)
     if ws > 1:
         dist.barrier()
     clocks = clk.stop()
-    ms_total = e0.elapsed_time(e1) if flush is None else sum(a_.elapsed_time(b_) for a_, b_ in evs)
     st = ctx.sand_get_stats()
     ms_mlp = st["ms_mlp_sum"] / max(st["queries"], 1)
     ms_lookup = st["ms_lookup_sum"] / max(st["queries"], 1)
     ms_bin = st["ms_bin_sum"] / max(st["queries"], 1)
 
-    # per-rank record -> NCCL all-gather (the only collective)
-    sdf_sum = float(torch.nan_to_num(sdf.double(), nan=0.0).sum().item())
-    dhash = float((dep.to(torch.int64) * (torch.arange(n, device=dev, dtype=torch.int64) % 8191 + 1)).sum().item())
-    rec = partition.make_record(n, st["per_depth"], ms_total, sdf_sum, dhash, k0, k1, st["queries"])
+    # order-independent per-rank checksums (SURVEY 8(e)): fixed-point SDF sum and a position-weighted depth
+    # hash over GLOBAL point indices, so the sum over ranks is identical for any N
+    fin = torch.isfinite(sdf)
+    sdf_fx = int(torch.round(torch.where(fin, sdf.double(), torch.zeros_like(sdf, dtype=torch.float64))
+                             * float(1 << 24)).to(torch.int64).sum().item())
+    gidx = torch.arange(n, device=dev, dtype=torch.int64) + int(base_index)
+    dhash = int((dep.to(torch.int64) * (gidx % 8191 + 1)).sum().item())
+
+    # the non-adaptive GPU baseline on the same points: an all-L depth map, same kernels (not in the timed region)
+    ms_full = 0.0
+    if not args.full_depth and not args.no_full_depth and not fp32 and args.task == "query":
+        ctx.sand_load_depthmap(g.VoxelMap(1, np.full(8, c.spec.L, np.uint8), None))
+        k_fd = max(1, min(args.steps, 5))
+        query()
+        torch.cuda.synchronize(dev)
+        if ws > 1:
+            dist.barrier()
+        ms_full = timed(k_fd) / k_fd * args.steps
+        if ws > 1:
+            dist.barrier()
+        ctx.sand_load_depthmap(dm)
+        ctx.sand_get_stats()
+
+    rec = partition.make_record(n, st["per_depth"], ms_total, sdf_fx, dhash, k0, k1, st["queries"], ms_full)
     if ws > 1:
         cdev = torch.device("cpu") if share else dev   # gloo gathers host tensors
         t = torch.from_numpy(rec).to(cdev)
@@ -634,7 +699,7 @@ def main():
     # end-to-end through the public API with host buffers (pinned), copies inside the timed region
     e2e = None
     if not args.no_e2e:
-        hp = torch.from_numpy(pts_np).pin_memory()
+        hp = pts.cpu().pin_memory()
         hs = torch.empty(n, dtype=torch.float32).pin_memory()
         hd = torch.empty(n, dtype=torch.uint8).pin_memory()
         ctx.sand_query_host(hp.data_ptr(), n, hs.data_ptr(), hd.data_ptr(), args.e2e_chunk)  # warm
@@ -652,13 +717,20 @@ def main():
             t_e2e = float(tt.item())
         e2e = {"value": summ["n_total"] / t_e2e, "unit": UNIT, "h2d_bytes_per_step": 12 * summ["n_total"],
                "d2h_bytes_per_step": 5 * summ["n_total"],
-               "chunk_points": args.e2e_chunk or min(max(n // 8, 1 << 21), 1 << 23),
+               "chunk_points": args.e2e_chunk or min(max(n // 8, 1 << 21), 1 << 23), "steps": args.e2e_steps,
                "timing": "host wall clock around the synchronous sand_query_host, max over ranks"}
+        del hp, hs, hd
         ctx.sand_get_stats()
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
-        cpu = cpu_baseline(p, c.depthmap, pts_np, args.cpu_seconds)
+        rng = np.random.default_rng(99)
+        if c.grid_R is not None:
+            sampler = lambda m: _sample_grid_points(c.grid_R, k0, k1, Rz, m, rng)
+        else:
+            host = pts.cpu().numpy()
+            sampler = lambda m: host[np.sort(rng.choice(n, min(m, n), replace=False))]
+        cpu = cpu_baseline(p, c.depthmap, sampler, args.cpu_seconds)
 
     if rank == 0:
         pk = _peaks()
@@ -674,15 +746,23 @@ def main():
             sm_mhz = (clocks or {}).get("sm_mhz") or 1965.0
             pk = dict(pk, bf16=148 * 128 * 2 * sm_mhz * 1e6 / 1e12, bf16_sus=148 * 128 * 2 * sm_mhz * 1e6 / 1e12,
                       src="derived FP32 ALU (148 SM x 128 lanes x 2 FLOP x median clock);")
+        kname = ("k_query_simt (FP32, one thread per point)" if fp32 and H <= 64 else
+                 "k_query_fp32 (FP32 register-blocked GEMM)" if fp32 else
+                 "k_tmlp_wide (K3 fused T-MLP, CTA pair, N-halves)" if H == 336 else
+                 "k_tmlp_tc2 (K3 fused T-MLP, CTA pair)")
+        full = None
+        if summ["ms_full_max"] > 0:
+            ms_fd = summ["ms_full_max"] / args.steps
+            full = {"value": summ["n_total"] / (ms_fd / 1e3), "unit": UNIT, "ms_per_step": ms_fd,
+                    "speedup": ms_fd / ms_step,
+                    "how": "same points and kernels, all-L depth map (every point at depth L), max over ranks"}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak" if weak else "strong",
             "vs_baseline": None, "dtype": "f32" if fp32 else "bf16", "data": "synthetic",
             "config": _arm_config(args, c, ws, wl_desc, summ["n_total"]),
-            "roofline": {"bound": "alu" if fp32 else "tensor",
-                         "kernel": ("k_query_fp32 (FP32 register-blocked GEMM)" if fp32 else
-                                    "k_tmlp_wide (K3 fused T-MLP, CTA pair, N-halves)" if c.spec.H == 336 else
-                                    "k_tmlp_tc2 (K3 fused T-MLP, CTA pair)"), "achieved": ach,
+            "roofline": {"bound": "alu" if fp32 else "tensor", "kernel": kname, "achieved": ach,
                          "peak": pk["bf16"], "unit": "TFLOP/s", "frac": ach / pk["bf16"],
                          "peak_source": pk["src"] + ("" if fp32 else " bf16_tflops (burst)"),
                          "frac_vs_sustained": ach / pk["bf16_sus"],
@@ -690,7 +770,7 @@ def main():
                          "algorithmic_flops_per_launch": f_exec_rank0,
                          "flops_formula": "executed H x H FLOPs sum_p (d_p - 1) * 2 H^2 (Eq. 2 reading R3)",
                          "ms_per_launch": ms_mlp,
-                         "traffic_source": "profiles/r01_k3_traffic.json (ncu --set full, dram read+write per launch)"},
+                         "traffic_source": TRAFFIC_SRC if (args.config == "C2" and not fp32) else None},
             # the other pipe the step needs: one sine per hidden unit per evaluated layer (Eq. 2), MUFU.SIN
             "sine_roofline": None if fp32 else _sine_roofline(st["per_depth"], H, ms_mlp, clocks),
             "tensor_frac_step": f_exec / (ms_step / 1e3) / 1e12 / pk["bf16"],
@@ -699,6 +779,10 @@ def main():
             "padding_waste": _padding_waste(st["per_depth"], H, fp32),
             "stage_ms": {"lookup": ms_lookup, "bin": ms_bin, "mlp": ms_mlp},
             "per_depth": per_depth,
+            "full_depth_speedup": full,
+            "checksums": {"sdf_fixed_point_2^24": summ["sdf_fx"], "depth_hash": summ["depth_hash"],
+                          "note": "int64 sums over all ranks: identical for any number of GPUs"},
+            "shards": summ["ranges"], "comm": comm,
             "e2e": e2e, "cpu_baseline": cpu,
             "gpu_launches": 6 * args.steps * ws,   # lookup, scan x3, scatter, T-MLP per query
             "clocks": clocks,
@@ -710,6 +794,55 @@ def main():
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="sand", choices=["sand", "reference"])
+    ap.add_argument("--config", default=None, choices=["C0", "C1", "C2", "C3", "C4"],
+                    help="BASELINE.json configs[i]; default C2 on 1 GPU (the metric's config), C4 on N > 1")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: the config's fixed grid cut into work-balanced z-slabs; weak: the grid refined "
+                         "along z to R x R x RN so every rank holds ~R^3 points")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-chunk", type=int, default=0, help="points per host-pipeline chunk (0: library default)")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-full-depth", action="store_true", help="skip the all-L (non-adaptive) comparison run")
+    ap.add_argument("--ref-sample", type=int, default=1 << 15)
+    ap.add_argument("--full-depth", action="store_true", help="all-L depth map (non-adaptive GPU baseline)")
+    ap.add_argument("--kprof", type=int, default=0, help="diagnostic SAND_OPT_KPROF (per-role counters, stderr)")
+    ap.add_argument("--prec", default=None, choices=["bf16", "fp32"],
+                    help="default: the config's precision (C0 FP32, others BF16); fp32: the accurate FP32 path "
+                         "(SIMT), reported against the FP32 ALU peak")
+    ap.add_argument("--task", default="query", choices=["query", "populate", "sweep", "dynamic", "mesh"],
+                    help="query: the adaptive SDF query path (BASELINE metric); populate: depth-map "
+                         "population (Eq. 5/6, SURVEY 8(f) NEXT #1) on the config's finest octree leaves")
+    args = ap.parse_args()
+    ws_env = os.environ.get("WORLD_SIZE")
+    if ws_env is None and args.gpus > 1:
+        _relaunch(args)
+    if ws_env is not None and int(ws_env) != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws_env} (launch one rank per GPU)")
+    if args.config is None:
+        args.config = "C2" if args.gpus == 1 or args.task != "query" else "C4"
+    if args.warmup < 3:
+        args.warmup = 3  # timing rule: at least 3 warm-up steps
+    if args.impl == "reference":
+        return run_reference(args)
+    if args.task == "populate":
+        return run_populate(args)
+    if args.task == "sweep":
+        return run_sweep(args)
+    if args.task == "dynamic":
+        return run_dynamic(args)
+    if args.task == "mesh":
+        return run_mesh(args)
+    return run_query(args)
 
 
 if __name__ == "__main__":

@@ -80,17 +80,22 @@ def shard_planes(depthmap, R, world, rank, weak=True):
 RECORD_FIELDS = 8 + 33
 
 
-def make_record(n, per_depth, ms, sdf_checksum, depth_hash, k0, k1, queries):
-    """Fixed-size float64 record a rank contributes to the NCCL all-gather."""
-    rec = np.zeros(RECORD_FIELDS, np.float64)
-    rec[:8] = [n, ms, sdf_checksum, depth_hash, k0, k1, queries, 0]
-    pd = np.asarray(per_depth, np.float64)
+def make_record(n, per_depth, ms, sdf_fx, depth_hash, k0, k1, queries, ms_full=0.0):
+    """Fixed-size int64 record a rank contributes to the NCCL all-gather: point count, timed-region device
+    time (ns), fixed-point SDF checksum sum(round(sdf * 2^24)), position-weighted depth hash, shard range,
+    query count, full-depth comparison time (ns), per-depth counts.  Integer sums are exact and
+    order-independent, so the totals over ranks are identical for any number of GPUs."""
+    rec = np.zeros(RECORD_FIELDS, np.int64)
+    rec[:8] = [int(n), int(round(ms * 1e6)), int(sdf_fx), int(depth_hash), int(k0), int(k1), int(queries),
+               int(round(ms_full * 1e6))]
+    pd = np.asarray(per_depth, np.int64)
     rec[8:8 + pd.size] = pd
     return rec
 
 
 def summarize(records):
-    r = np.asarray(records, np.float64).reshape(-1, RECORD_FIELDS)
-    return dict(n_total=int(r[:, 0].sum()), ms_max=float(r[:, 1].max()), ms_min=float(r[:, 1].min()),
-                checksum=float(r[:, 2].sum()), per_depth=r[:, 8:].sum(0).astype(np.int64).tolist(),
+    r = np.asarray(records, np.int64).reshape(-1, RECORD_FIELDS)
+    return dict(n_total=int(r[:, 0].sum()), ms_max=float(r[:, 1].max()) / 1e6, ms_min=float(r[:, 1].min()) / 1e6,
+                sdf_fx=int(r[:, 2].sum()), depth_hash=int(r[:, 3].sum()), ms_full_max=float(r[:, 7].max()) / 1e6,
+                per_depth=r[:, 8:].sum(0).astype(np.int64).tolist(),
                 ranges=[(int(a), int(b)) for a, b in r[:, 4:6]])

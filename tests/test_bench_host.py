@@ -44,12 +44,42 @@ def test_reference_arm_config_equals_this_arms():
     import argparse
     from paper_2604_25936_b200 import partition
     import sandgen as g
-    args = argparse.Namespace(config="C2", full_depth=False)
+    args = argparse.Namespace(config="C2", full_depth=False, scaling="strong")
     c = g.make_config("C2")
-    k0, k1, Rz = partition.shard_planes(c.depthmap, c.grid_R, 1, 0, weak=True)
+    k0, k1, Rz = partition.shard_planes(c.depthmap, c.grid_R, 1, 0, weak=False)
     wl_this = f"C2: {c.grid_R}x{c.grid_R}x{Rz} grid, z-planes [{k0},{k1}) on rank 0"
     assert bench._n1_workload(args, c) == wl_this
     this = bench._arm_config(args, c, 1, wl_this, c.grid_R ** 3)
     ref = bench._arm_config(args, c, 1, bench._n1_workload(args, c), c.grid_R ** 3)
     assert this == ref
     assert this["global_points"] == 512 ** 3 and "no flush needed" in this["l2"]
+
+
+def test_c4_strong_config_line():
+    """N > 1 default: C4's fixed 1024^3 grid (global_points 1024^3 for any N), strong-scaled."""
+    import argparse
+    import sandgen as g
+    args = argparse.Namespace(config="C4", full_depth=False, scaling="strong")
+    c = g.make_config("C4")
+    cfg = bench._arm_config(args, c, 8, "unused", c.grid_R ** 3)
+    assert cfg["global_points"] == 1024 ** 3 and "strong-scaled" in cfg["workload"]
+    assert cfg["parallelism"] == "dp8 (z-slab shards)" and "level-8" in cfg["depth_map"]
+
+
+def test_gpus_flag_relaunches_and_rejects_mismatch(monkeypatch):
+    """--gpus N without a torchrun environment re-executes under torch.distributed.run with N ranks; a
+    torchrun environment whose WORLD_SIZE differs from --gpus is an error (never a silent 1-rank run)."""
+    calls = []
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    monkeypatch.setattr(bench.os, "execv", lambda exe, cmd: calls.append(cmd) or (_ for _ in ()).throw(SystemExit(0)))
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "2"])
+    with pytest.raises(SystemExit):
+        bench.main()
+    cmd = calls[0]
+    assert "torch.distributed.run" in cmd and "--nproc-per-node=4" in cmd and "--master-addr=127.0.0.1" in cmd
+    assert cmd[-4:] == ["--gpus", "4", "--steps", "2"]
+    monkeypatch.setenv("WORLD_SIZE", "2")
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4"])
+    with pytest.raises(SystemExit) as e:
+        bench.main()
+    assert "WORLD_SIZE" in str(e.value)

@@ -52,13 +52,17 @@ def test_plane_work_matches_exact_per_plane_depth_sums():
 def _worker(rank, world, port, R, out):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import fp32 as ofp
     c = g.make_config("C0")
+    p = c.params()
     k0, k1, Rz = partition.shard_planes(c.depthmap, R, world, rank, weak=False)
     pts = g.grid_points_slab(R, k0, k1, Rz)
-    d, _, _ = oracle.lookup(c.depthmap, pts)
+    sdf, d = ofp.query_fp32(p, c.depthmap, pts)
     per_depth = np.bincount(d, minlength=c.spec.L + 1)
-    rec = partition.make_record(pts.shape[0], per_depth, 1.0 + rank, float(pts.astype(np.float64).sum()),
-                                float(d.sum()), k0, k1, 1)
+    gidx = np.arange(pts.shape[0], dtype=np.int64) + k0 * R * R
+    sdf_fx = int(np.round(sdf.astype(np.float64) * (1 << 24)).astype(np.int64).sum())
+    dhash = int((d.astype(np.int64) * (gidx % 8191 + 1)).sum())
+    rec = partition.make_record(pts.shape[0], per_depth, 1.0 + rank, sdf_fx, dhash, k0, k1, 1)
     t = torch.from_numpy(rec)
     allr = torch.empty(world * t.numel(), dtype=t.dtype)
     dist.all_gather_into_tensor(allr, t)
@@ -68,8 +72,7 @@ def _worker(rank, world, port, R, out):
     dist.destroy_process_group()
 
 
-def test_gloo_world2_shards_tile_grid_and_gather_matches_single_process():
-    R, world = 64, 2
+def _run_world(world, R):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -80,15 +83,47 @@ def test_gloo_world2_shards_tile_grid_and_gather_matches_single_process():
     for p in procs:
         p.join(timeout=300)
         assert p.exitcode == 0
-    ranges = summ["ranges"]
+    return summ
+
+
+def test_gloo_world2_shards_tile_grid_and_checksums_match_one_rank():
+    """Strong sharding of C0's 64^3 grid over 2 gloo ranks: the shards tile the grid once, the gathered
+    per-depth counts equal the single-process lookup's, and the int64 fixed-point SDF checksum and the
+    global-index depth hash summed over ranks are bit-identical to the 1-rank run (SURVEY 8(e) pin)."""
+    R = 64
+    summ2 = _run_world(2, R)
+    summ1 = _run_world(1, R)
+    ranges = summ2["ranges"]
     assert ranges[0][0] == 0 and ranges[-1][1] == R and ranges[0][1] == ranges[1][0]
     c = g.make_config("C0")
-    pts = c.points_fn()
-    d, _, _ = oracle.lookup(c.depthmap, pts)
-    assert summ["n_total"] == R ** 3
-    np.testing.assert_array_equal(summ["per_depth"][:c.spec.L + 1], np.bincount(d, minlength=c.spec.L + 1))
-    assert summ["ms_max"] == 2.0 and summ["ms_min"] == 1.0
-    np.testing.assert_allclose(summ["checksum"], pts.astype(np.float64).sum(), rtol=1e-12)
+    d, _, _ = oracle.lookup(c.depthmap, c.points_fn())
+    assert summ2["n_total"] == R ** 3
+    np.testing.assert_array_equal(summ2["per_depth"][:c.spec.L + 1], np.bincount(d, minlength=c.spec.L + 1))
+    assert summ2["ms_max"] == 2.0 and summ2["ms_min"] == 1.0
+    assert summ2["sdf_fx"] == summ1["sdf_fx"] and summ2["depth_hash"] == summ1["depth_hash"]
+    assert summ2["per_depth"] == summ1["per_depth"]
+
+
+def test_record_is_int64_and_exact():
+    rec = partition.make_record(10, [1, 2, 3], 1.5, -(1 << 60), 123456789012345, 3, 7, 2, 4.25)
+    assert rec.dtype == np.int64
+    s = partition.summarize(np.concatenate([rec, rec]))
+    assert s["sdf_fx"] == -(1 << 61) and s["depth_hash"] == 2 * 123456789012345
+    assert s["ms_max"] == 1.5 and s["ms_full_max"] == 4.25 and s["n_total"] == 20
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_c4_strong_partition_balanced(world):
+    """BASELINE.json configs[4]: the fixed 1024^3 grid cut into `world` z-slabs by estimated work: every plane
+    once, and the estimated max/mean work <= 1.01 (equal-thickness slabs: 1.16 at 8 ranks)."""
+    c = g.make_config("C4")
+    R = c.grid_R
+    w = partition.plane_work(c.depthmap, R, R)
+    sl = [partition.shard_planes(c.depthmap, R, world, r, weak=False) for r in range(world)]
+    assert all(Rz == R for _, _, Rz in sl)
+    assert sl[0][0] == 0 and sl[-1][1] == R and all(sl[r][1] == sl[r + 1][0] for r in range(world - 1))
+    per = np.array([w[k0:k1].sum() for k0, k1, _ in sl])
+    assert per.max() / per.mean() <= 1.01
 
 
 def test_weak_scaling_shards_hold_about_R3_points_each():
