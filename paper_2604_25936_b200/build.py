@@ -17,8 +17,20 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
          "-I", os.path.join(ROOT, "include")]
 
 
+STAMP = LIB + ".flags"
+
+
+def _flag_line():
+    # path-independent (the repo is copied elsewhere on the GPU box): the include dir is written relatively
+    return " ".join(["nvcc", *FLAGS, *EXTRA]).replace(ROOT, "<repo>")
+
+
 def _stale():
-    if not os.path.exists(LIB):
+    """Rebuild when the .so is missing, older than a source, or built with other flags / defines (a
+    diagnostic SAND_BUILD_DEFS build is never silently reused by a default build, and vice versa)."""
+    if not os.path.exists(LIB) or not os.path.exists(STAMP):
+        return True
+    if open(STAMP).read().strip() != _flag_line():
         return True
     t = os.path.getmtime(LIB)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.join(ROOT, "include", "sand.h")]
@@ -49,6 +61,8 @@ def build(force=False, verbose=True, ptxas_v=False):
     subprocess.check_call([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", tmp,
                            "-cudart", "static"])
     os.replace(tmp, LIB)
+    with open(STAMP, "w") as f:
+        f.write(_flag_line() + "\n")
     for o in objs:
         os.remove(o)
     return LIB

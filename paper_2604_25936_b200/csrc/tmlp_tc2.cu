@@ -67,6 +67,22 @@
 #ifndef SAND_SC
 #define SAND_SC 2        // K-chunks per weight-ring stage
 #endif
+#ifndef SAND_SMR
+#define SAND_SMR 0   // 1: 4 control warps (one warpgroup) shrink to SAND_SMR_CTL registers, the 16 epilogue warps grow to SAND_SMR_EPI
+#endif
+#ifndef SAND_SMR_CTL
+#define SAND_SMR_CTL 64
+#endif
+#ifndef SAND_SMR_EPI
+#define SAND_SMR_EPI 104
+#endif
+// setmaxnreg.inc only draws on registers the CTA released with .dec: the launch gives every one of the 640
+// threads 96 registers (65536 / 640, rounded down to 8), so 16 epilogue warps may grow by at most what 4
+// control warps give back, else the .inc waits forever.
+static_assert(!SAND_SMR || 4 * (SAND_SMR_EPI - 96) <= 96 - SAND_SMR_CTL, "setmaxnreg budget");
+#ifndef SAND_BW
+#define SAND_BW 16   // accumulator columns per TMEM load batch (8, 16 or 32)
+#endif
 #ifndef SAND_PDEG
 #define SAND_PDEG 7
 #endif
@@ -103,7 +119,8 @@ struct Tc2Shape {
   static constexpr int CQ = HN / 4;                // columns per epilogue column group per pass
   static constexpr int TMEM_COLS = 2 * H <= 128 ? 128 : (2 * H <= 256 ? 256 : 512);
   static constexpr int NGRP = 4;                   // epilogue column groups (x 4 TMEM lane quadrants = 16 warps)
-  static constexpr int THREADS = 96 + 128 * NGRP;  // 3 control warps + 16 epilogue warps
+  static constexpr int NCTL = SAND_SMR ? 4 : 3;    // control warps (a whole warpgroup when registers are rebalanced)
+  static constexpr int THREADS = 32 * NCTL + 128 * NGRP;  // control warps + 16 epilogue warps
   static constexpr int TILE = 256;
   static_assert(H % 64 == 0 && H <= 256 && CQ % 8 == 0, "CTA-pair kernel: H in {64, 128, 192, 256}");
 };
@@ -115,7 +132,7 @@ struct Tc2Params {
   const QueryMeta* meta;
   float* out;
   int nst;
-  int prof;   // diagnostic (env SAND_KPROF=1): per-role clock64 wait/busy counters -> g_kprof
+  int prof;   // diagnostic (SAND_OPT_KPROF, -DSAND_DIAG=1 builds only): per-role clock64 counters -> g_kprof
 };
 
 // Diagnostic counters (only written when Tc2Params::prof != 0), per CTA:
@@ -296,6 +313,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
   const long long T = p.meta->total_tiles;
   const long long tstride = 2ll * npairs;
 
+  // Register rebalancing (setmaxnreg is per warpgroup, issued by all its threads at the top of their role
+  // branch so that ptxas applies the new limit to the whole role): the control warpgroup (warps 0-3) gives
+  // registers back, the epilogue warpgroups take them (per SMSP: 1 control + 4 epilogue warps).
+  if (warp < C::NCTL) {
+  if (SAND_SMR) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(SAND_SMR_CTL));
   if ((warp == 0 && lane == 0) || warp == 1) {
     {
       // warp 0: producer (lane 0); warp 1: MMA issuer (leader CTA) / relay (odd CTA), all 32 lanes converged,
@@ -312,16 +334,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
       int st = 0;
       uint32_t ph = 0;
       unsigned long long pc[6] = {0, 0, 0, 0, 0, 0};
-      const long long t_start = p.prof ? clock64() : 0;
+      const long long t_start = (SAND_DIAG && p.prof) ? clock64() : 0;
       // a_full[s] completes once per epilogue step of slot s (all epilogue warps of both CTAs arrived:
       // A written for the next layer and accumulator read).  Every MMA job but the first of a slot waits
       // for the previous step of its slot, so the accumulator is never overwritten while read.
       auto wait_prev_step = [&](const SlotWalk& w, int s) {
         if (w.ti == 0 && w.l == 1) return;
         uint32_t& pa = s ? pa1 : pa0;
-        const long long c0_ = p.prof ? clock64() : 0;
+        const long long c0_ = (SAND_DIAG && p.prof) ? clock64() : 0;
         mbar_wait_cluster(b_afull + 8 * s, pa);
-        if (p.prof) { pc[0] += clock64() - c0_; pc[3] += 1; }
+        if (SAND_DIAG && p.prof) { pc[0] += clock64() - c0_; pc[3] += 1; }
         pa ^= 1u;
       };
       auto job = [&](const SlotWalk& w, int s) {
@@ -329,9 +351,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
         const int nsj = l == 1 ? 0 : 2;   // ring stages of this job (one per pass)
         if (warp == 0) {
           for (int j = 0; j < nsj && !(SAND_DIAG && p.prof == 3); ++j) {
-            const long long c0_ = p.prof ? clock64() : 0;
+            const long long c0_ = (SAND_DIAG && p.prof) ? clock64() : 0;
             mbar_wait_lazy(b_wempty + 8 * st, ph ^ 1u);
-            if (p.prof) { pc[4] += clock64() - c0_; pc[5] += 1; }
+            if (SAND_DIAG && p.prof) { pc[4] += clock64() - c0_; pc[5] += 1; }
             mbar_arrive_expect_tx(b_wfull + 8 * st, C::STAGE);
             bulk_g2s(sW + st * C::STAGE, img + ((size_t)(l - 2) * 4 + j) * C::STAGE, C::STAGE, b_wfull + 8 * st);
             if (++st == nst) { st = 0; ph ^= 1u; }
@@ -341,9 +363,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
           const uint32_t acc = tmem_base + (uint32_t)(s * H);
           if (l == 1) {
             // ---- layer 1: per pass one K = 16 MMA on the split-BF16 operands (A written by the IO warps)
-            const long long c0_ = p.prof ? clock64() : 0;
+            const long long c0_ = (SAND_DIAG && p.prof) ? clock64() : 0;
             mbar_wait_cluster(b_a1full + 8 * s, (uint32_t)(w.ti & 1));
-            if (p.prof) { pc[0] += clock64() - c0_; }
+            if (SAND_DIAG && p.prof) { pc[0] += clock64() - c0_; }
             tc_fence_after();
             const uint64_t a1d = desc_nosw(sA1 + s * C::A1_BYTES, 128, 256);
             mma_bf16_cg2_w(acc, a1d, desc_nosw(sW1, 128, 256), ID, 0u);
@@ -362,18 +384,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
           // columns for the next tile meanwhile: they hold finite values and meet zeros in the bias operand,
           // so the product is b_hi + b_lo whichever version the tensor core reads)
           const uint64_t ones_d = desc_nosw(SAND_ONES_A1 ? sA1 + s * C::A1_BYTES : sOnes, 128, 256);
-#pragma unroll
+#pragma unroll 1
           for (int j = 0; j < 2; ++j) {
-            const long long c0_ = p.prof ? clock64() : 0;
+            const long long c0_ = (SAND_DIAG && p.prof) ? clock64() : 0;
             if (!(SAND_DIAG && p.prof == 3)) { mbar_wait(b_wfull + 8 * st, ph);
             mbar_wait_cluster(b_wpeer + 8 * st, ph); }   // diagnostic 3: no weight streaming
-            if (p.prof) pc[1] += clock64() - c0_;
+            if (SAND_DIAG && p.prof) pc[1] += clock64() - c0_;
             tc_fence_after();
             const uint32_t slot = sW + st * C::STAGE;
             const uint32_t d = acc + (uint32_t)(j * C::HN);
             mma_bf16_cg2_w(d, ones_d, desc_nosw(slot, 128, 256), ID, 0u);
             const uint64_t w_d = desc_sw128(slot + C::QSMALL);
-#pragma unroll
+#pragma unroll 1
             for (int kc = 0; kc < C::KC; ++kc)
               mma4_bf16_cg2_w(d, a_d + (uint64_t)(kc * (C::A_CHUNK >> 4)), w_d + (uint64_t)(kc * (C::QCHUNK >> 4)), ID, 1u);
             mma_commit_cg2_mc_w(b_wempty + 8 * st, 0x3);
@@ -394,7 +416,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
         if (!w0.done) { job(w0, 0); w0.advance(tstride, T, s_tile_end, L); }
         if (!w1.done) { job(w1, 1); w1.advance(tstride, T, s_tile_end, L); }
       }
-      if (p.prof) {
+      if (SAND_DIAG && p.prof) {
         pc[2] = clock64() - t_start;
         if (warp == 1 && rank == 0 && lane == 0)
           for (int k = 0; k < 4; ++k) g_kprof[blockIdx.x][k] = pc[k];
@@ -473,21 +495,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
       if (t0 + tstride < T) load_perm(t0 + tstride, q.nxt);
     }
     auto io_step = [&](const SlotWalk& w, int s, IoSlot& q) {
-      const long long c0_ = p.prof ? clock64() : 0;
+      const long long c0_ = (SAND_DIAG && p.prof) ? clock64() : 0;
       long long waited = 0;
       if (w.l == 1) {
         const long long t1 = w.t + tstride;
         if (t1 < T) {
           mbar_wait_lazy(b_a1free + 8 * s, (uint32_t)(w.ti & 1));   // this tile's layer-1 MMA read A1
-          if (p.prof) waited += clock64() - c0_;
+          if (SAND_DIAG && p.prof) waited += clock64() - c0_;
           fill(s, q.nxt);
           if (t1 + tstride < T) load_perm(t1 + tstride, q.pre);
         }
       }
       if (w.l == w.d) {
-        const long long c1_ = p.prof ? clock64() : 0;
+        const long long c1_ = (SAND_DIAG && p.prof) ? clock64() : 0;
         mbar_wait_lazy(b_iodone + 8 * s, (uint32_t)(w.ti & 1));
-        if (p.prof) waited += clock64() - c1_;
+        if (SAND_DIAG && p.prof) waited += clock64() - c1_;
         const float* pl = part + s * NPL * 128;
         const float cs = tcs[w.d];
         float y[4];
@@ -508,17 +530,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
 #pragma unroll
         for (int k = 0; k < 4; ++k) { q.cur[k] = q.nxt[k]; q.nxt[k] = q.pre[k]; }
       }
-      if (p.prof) { io_wait += waited; io_busy += clock64() - c0_ - waited; }
+      if (SAND_DIAG && p.prof) { io_wait += waited; io_busy += clock64() - c0_ - waited; }
     };
 #pragma unroll 1
     while (!(w0.done && w1.done)) {
       if (!w0.done) { io_step(w0, 0, q0); w0.advance(tstride, T, s_tile_end, L); }
       if (!w1.done) { io_step(w1, 1, q1); w1.advance(tstride, T, s_tile_end, L); }
     }
-    if (p.prof && lane == 0) { g_kprof[blockIdx.x][10] = io_wait; g_kprof[blockIdx.x][11] = io_busy; }
-  } else if (warp >= 3) {
+    if (SAND_DIAG && p.prof && lane == 0) { g_kprof[blockIdx.x][10] = io_wait; g_kprof[blockIdx.x][11] = io_busy; }
+  }
+  } else {
+    if (SAND_SMR) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(SAND_SMR_EPI));
     // =========================== epilogue (16 warps, both slots, step by step)
-    const int ew = warp - 3;
+    const int ew = warp - C::NCTL;
     const int q = warp & 3;                  // TMEM lane quadrant = warp % 4
     const int cq = ew >> 2;                  // column group (quarter when NGRP = 4)
     // TMEM access in the 16x256b shape: thread (quad = lane / 4, tq = lane % 4) owns rows
@@ -529,7 +553,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
     const int quad = lane >> 2, tq = lane & 3;
     constexpr int NCHP = C::CQ / 8;               // 8-column chunks per group per pass
     const int c0 = cq * C::CQ;
-    constexpr int BW = NCHP >= 2 ? 16 : 8;        // columns per TMEM load batch (2 x BW/2 registers)
+    constexpr int BW = NCHP * 8 >= SAND_BW ? SAND_BW : NCHP * 8;   // columns per TMEM load batch (2 x BW/2 registers)
     constexpr int CB = BW / 8;                    // 8-column chunks per batch
     static_assert(NCHP % CB == 0, "whole TMEM load batches per group");
     const uint32_t tm_q = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)c0;
@@ -565,7 +589,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
 #pragma unroll
       for (int k = 0; k < 4; ++k) { yv[k] = make_float2(0.f, 0.f); yv1[k] = make_float2(0.f, 0.f); }
       long long wt = 0;
-      const long long c0_ = p.prof ? clock64() : 0;
+      const long long c0_ = (SAND_DIAG && p.prof) ? clock64() : 0;
       const bool store = l != d;
       const float* ta = tta + (l - 1) * H + c0 + 2 * tq;
       const float* a1 = ta1 + (l - 2) * H + c0 + 2 * tq;
@@ -618,9 +642,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
         constexpr int PO = decltype(pass_c)::value * C::HN;   // column offset of this pass
         constexpr bool ST = SAND_SPLIT_STORE ? decltype(st_c)::value : true;
         {
-          const long long w0_ = p.prof ? clock64() : 0;
+          const long long w0_ = (SAND_DIAG && p.prof) ? clock64() : 0;
           mbar_wait(b_accfull + 16 * s + 8 * decltype(pass_c)::value, e.pe);
-          if (p.prof) wt += clock64() - w0_;
+          if (SAND_DIAG && p.prof) wt += clock64() - w0_;
           tc_fence_after();
         }
         if (decltype(pass_c)::value == 1 && ST && (SAND_SPLIT_STORE || store)) {
@@ -687,10 +711,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
 #pragma unroll
         for (int k = 0; k < 4; ++k) e.ylin[k] += yv[k].x + yv[k].y;
       }
-      const long long cp_ = p.prof ? clock64() : 0;
+      const long long cp_ = (SAND_DIAG && p.prof) ? clock64() : 0;
       publish(s, store);
-      if (p.prof) ep_pub += clock64() - cp_;
-      const long long ct_ = p.prof ? clock64() : 0;
+      if (SAND_DIAG && p.prof) ep_pub += clock64() - cp_;
+      const long long ct_ = (SAND_DIAG && p.prof) ? clock64() : 0;
       if (l == d) {
         // tile end: every row reduced over its quad (shuffles); each warp hands its column quarter's
         // partials to the IO warp (which adds the 4 quarters and the tail-bias prefix sum).  No barrier
@@ -708,9 +732,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
         __syncwarp();
         if (lane == 0) mbar_arrive(b_iodone + 8 * s);
       }
-      if (p.prof) ep_tend += clock64() - ct_;
+      if (SAND_DIAG && p.prof) ep_tend += clock64() - ct_;
       e.w.advance(tstride, T, s_tile_end, L);
-      if (p.prof) { ep_wait += wt; ep_busy += clock64() - c0_ - wt; ep_steps += 1; }
+      if (SAND_DIAG && p.prof) { ep_wait += wt; ep_busy += clock64() - c0_ - wt; ep_steps += 1; }
     };
 
     EpiSlot e0, e1;
@@ -720,13 +744,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
     e0.yprod = e1.yprod = 0.f;
 #pragma unroll
     for (int k = 0; k < 4; ++k) e0.ylin[k] = e1.ylin[k] = 0.f;
-    const long long t_start = p.prof ? clock64() : 0;
+    const long long t_start = (SAND_DIAG && p.prof) ? clock64() : 0;
 #pragma unroll 1
     while (!(e0.w.done && e1.w.done)) {
       if (!e0.w.done) step(e0, 0);
       if (!e1.w.done) step(e1, 1);
     }
-    if (p.prof && warp == 3 && lane == 0) {
+    if (SAND_DIAG && p.prof && warp == 3 && lane == 0) {
       g_kprof[blockIdx.x][6] = ep_wait;
       g_kprof[blockIdx.x][7] = ep_busy;
       g_kprof[blockIdx.x][8] = clock64() - t_start;
@@ -912,7 +936,7 @@ static cudaError_t launch_tc2_t(const MlpDev& m, const float* pts, const uint32_
     }
   }
 #endif
-  if (prof && e == cudaSuccess) {
+  if (SAND_DIAG && prof && e == cudaSuccess) {
     // diagnostic only (SAND_OPT_KPROF): synchronous dump of the per-role counters (CTA averages; MMA over leaders)
     static unsigned long long h[160][kProfSlots];
     e = cudaStreamSynchronize(st);

@@ -3,7 +3,7 @@
 tag=$1; shift
 mkdir -p gpurun_out
 for name in "$@"; do
-  SAND_LIB=abl/libsand_$name.so timeout 200 python bench.py --no-cpu --no-e2e --steps 10 ${BENCH_ARGS} > gpurun_out/${tag}_$name.log 2>&1
+  SAND_LIB=abl/libsand_$name.so timeout ${VAR_TIMEOUT:-200} python bench.py --no-cpu --no-e2e --steps 10 ${BENCH_ARGS} > gpurun_out/${tag}_$name.log 2>&1
   python - "$tag" "$name" <<'PY'
 import json, sys
 tag, name = sys.argv[1], sys.argv[2]

@@ -112,3 +112,22 @@ def test_populate_edge_sizes():
         torch.cuda.synchronize()
         exp = oracle.populate_leaf_depths(p, pts, 1e-3)
         assert np.mean(out.cpu().numpy() == exp) >= 6 / 7
+
+
+def test_leaf_max_pooling_hand_case_gpu():
+    """SPEC S:304 / Eq. 6 on the GPU: the hand-built net of tests/test_oracle_depthpop.py (padded to H = 16 with
+    zero units) gives per-sample depths {1, 3, 2} and the leaf depth 3."""
+    import torch
+    from paper_2604_25936_b200 import SandContext
+    from test_oracle_depthpop import HAND_D, hand_pool_net, hand_pool_samples
+    p = hand_pool_net(H=16)
+    s = hand_pool_samples()
+    with SandContext(3, 16, 1.0, 0, 0, 0) as ctx:
+        ctx.sand_load_weights(g.pack_blob(p))
+        d = _run_required(ctx, s, 0.05, True)
+        np.testing.assert_array_equal(d, HAND_D)
+        t = torch.from_numpy(np.ascontiguousarray(s)).cuda()
+        out = torch.empty(1, dtype=torch.uint8, device="cuda")
+        ctx.sand_populate_leaf_depths(t.data_ptr(), 1, 3, 0.05, out.data_ptr())
+        torch.cuda.synchronize()
+        assert int(out.item()) == 3

@@ -143,3 +143,40 @@ def test_edge_grids_match_oracle():
         To = oracle.marching_cubes(sdf.astype(np.float64), R)
         assert T.shape == To.shape
         np.testing.assert_allclose(_canon(T), _canon(To), rtol=0, atol=1e-6)
+
+
+def test_fused_mesh_matches_oracle_mc_of_oracle_query():
+    """The whole mesh pipeline against the oracle end to end: sand_mesh_grid on C0's
+    T-MLP (FP32 path, grid R = 33, slabs of 8 cube planes) vs oracle.marching_cubes applied to the FP32 C
+    oracle's SDF of the same grid.  Corner signs must agree wherever |sdf_oracle| exceeds the FP32 tolerance;
+    then the triangle sets must match one to one, vertices within interpolation error."""
+    import torch
+    from scipy.spatial import cKDTree
+    from oracle import fp32 as ofp
+    c = g.make_config("C0")
+    p = c.params()
+    R = 33
+    pts = g.grid_points(R)
+    s_or, _ = ofp.query_fp32(p, c.depthmap, pts)
+    T_or = oracle.marching_cubes(s_or.astype(np.float64), R).reshape(-1, 3, 3)
+    with make_ctx(c.spec, 0) as ctx:
+        ctx.sand_load_weights(g.pack_blob(p))
+        ctx.sand_load_depthmap(c.depthmap)
+        sdf, _ = ctx.query_tensor(torch.from_numpy(pts).cuda())
+        m = ctx.sand_mesh_grid(R, 8, 0, 0)
+        b = torch.empty(9 * max(m, 1), device="cuda")
+        assert ctx.sand_mesh_grid(R, 8, b.data_ptr(), m) == m
+        torch.cuda.synchronize()
+        s_gpu = sdf.cpu().numpy()
+        T_gpu = b[: 9 * m].cpu().numpy().reshape(-1, 3, 3).astype(np.float64)
+    robust = np.abs(s_or) > 1e-4
+    assert np.array_equal(np.sign(s_gpu[robust]), np.sign(s_or[robust]))
+    flips = int((np.sign(s_gpu) != np.sign(s_or)).sum())
+    assert flips == 0, f"{flips} near-zero corners changed sign: triangulations differ locally"
+    assert m == T_or.shape[0] > 5000
+    # R24 fixes each triangle's vertex order, so triangles are compared as points in R^9
+    tree = cKDTree(T_or.reshape(-1, 9))
+    _, j = tree.query(T_gpu.reshape(-1, 9))
+    d = np.linalg.norm(T_gpu - T_or[j], axis=-1).max(axis=1)
+    assert np.unique(j).size == m, "one-to-one triangle correspondence"
+    assert d.max() <= 1e-3 and np.median(d) <= 1e-5, (d.max(), np.median(d))

@@ -62,14 +62,45 @@ def test_depth_range_and_limits():
     assert np.all(oracle.required_depth(p, X, 0.0) == 6)
 
 
+def hand_pool_net(H=1):
+    """L = 3 net whose per-point Eq. 5 depth is set by the sign of y_1 = sin(x_0) (omega0 = 1, W_1 = (1, 0, 0),
+    b_1 = 0, a_1 = 1, c_1 = 0) against constant residuals t_2 = t_3 = -0.01 (W_2 = W_3 = 0, b = pi/2, so
+    h_2 = h_3 = sin(pi/2) = 1, a_2 = a_3 = -0.01).  Units beyond the first (H > 1, for kernels with a
+    minimum width) have zero weights, biases and tail entries, so they contribute nothing."""
+    z = lambda *s: np.zeros(s, np.float32)
+    W = [z(H, 3), z(H, H), z(H, H)]
+    W[0][0, 0] = 1.0
+    b = [z(H), z(H), z(H)]
+    b[1][0] = b[2][0] = np.float32(np.pi / 2)
+    a = [z(H), z(H), z(H)]
+    a[0][0], a[1][0], a[2][0] = 1.0, -0.01, -0.01
+    spec = SimpleNamespace(L=3, H=H, omega0=1.0, tail=0)
+    return SimpleNamespace(spec=spec, W=W, b=b, a=a, c=[0.0, 0.0, 0.0], a1=[], c1=[])
+
+
+# y_1 = s, y_2 = s - 0.01, y_3 = s - 0.02; with r = 0.05 every |y_3 - y_i| <= 0.02 < r, so Eq. 5 reduces to the
+# sign gate: s = 0.5 -> all signs agree -> d = 1; s = 0.015 -> y_3 < 0 < y_2 < y_1 -> d = 3;
+# s = 0.005 -> y_1 > 0 > y_2, y_3 -> d = 2.  (Worked by hand from Eq. 5; margins >= 0.005 >> float error.)
+HAND_S = (0.5, 0.015, 0.005)
+HAND_D = (1, 3, 2)
+
+
+def hand_pool_samples():
+    x0 = np.arcsin(np.array(HAND_S)).astype(np.float32)
+    return np.stack([x0, np.full(3, 0.25, np.float32), np.full(3, -0.5, np.float32)], 1)
+
+
 def test_leaf_max_pooling_hand_case():
-    """Eq. 6: d(N) is the max of the per-sample depths (SPEC S:304 example {1, 3, 2} -> 3, here with two
-    hand-built constant nets mixed through a leaf whose samples straddle x = 0 via W_1's sign)."""
-    # the oracle's pooling equals the max of its per-point depths on a real net
-    p = g.make_weights(g.TMlpSpec(L=5, H=16, seed=4))
-    s = np.random.default_rng(5).uniform(-1, 1, (11, 6, 3)).astype(np.float32)
-    per = oracle.required_depth(p, s.reshape(-1, 3), 2e-3).reshape(11, 6)
-    np.testing.assert_array_equal(oracle.populate_leaf_depths(p, s, 2e-3), per.max(axis=1))
+    """Eq. 6 max pooling, SPEC S:304's example: one leaf whose three samples have required depths
+    {1, 3, 2} (worked by hand above) gets depth 3; leaves holding one sample each keep that sample's depth."""
+    p = hand_pool_net()
+    s = hand_pool_samples()
+    np.testing.assert_array_equal(oracle.required_depth(p, s, 0.05), HAND_D)
+    assert oracle.populate_leaf_depths(p, s[None, :, :], 0.05).tolist() == [3]
+    np.testing.assert_array_equal(oracle.populate_leaf_depths(p, s[:, None, :], 0.05), HAND_D)
+    # two-sample leaves: {1, 2} -> 2, {2, 1} -> 2, {1, 1} -> 1
+    pairs = np.stack([s[[0, 2]], s[[2, 0]], s[[0, 0]]])
+    assert oracle.populate_leaf_depths(p, pairs, 0.05).tolist() == [2, 2, 1]
 
 
 def test_leaf_samples_geometry_and_determinism():
