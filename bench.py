@@ -254,29 +254,51 @@ def run_populate(args):
     ts = torch.from_numpy(np.ascontiguousarray(samples.reshape(-1, 3))).to(dev)
     out = torch.empty(n, dtype=torch.uint8, device=dev)
     r = 1.5e-4
+    from paper_2604_25936_b200 import SAND_OPT_FP32_TENSOR
+    H, L = c.spec.H, c.spec.L
+    ns = n * spl
     with SandContext(c.spec.L, c.spec.H, c.spec.omega0, SAND_BF16, c.spec.tail, 0) as ctx:
         ctx.sand_load_weights(g.pack_blob(p))
         st = torch.cuda.current_stream(dev)
         ctx.sand_set_stream(st.cuda_stream)
-        for _ in range(args.warmup):
-            ctx.sand_populate_leaf_depths(ts.data_ptr(), n, spl, r, out.data_ptr())
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize(dev)
+
+        def timed(tensor, steps):
+            ctx.sand_set_option(SAND_OPT_FP32_TENSOR, tensor)
+            for _ in range(args.warmup):
+                ctx.sand_populate_leaf_depths(ts.data_ptr(), n, spl, r, out.data_ptr())
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize(dev)
+            e0.record(st)
+            for _ in range(steps):
+                ctx.sand_populate_leaf_depths(ts.data_ptr(), n, spl, r, out.data_ptr())
+            e1.record(st)
+            torch.cuda.synchronize(dev)
+            return e0.elapsed_time(e1) / steps
+
+        ms_simt = timed(0, max(1, min(args.steps, 3)))          # the FP32 SIMT kernel, for comparison
+        d_simt = out.cpu().numpy().copy()
         clk = ClockSampler(0)
         clk.start()
-        e0.record(st)
-        for _ in range(args.steps):
-            ctx.sand_populate_leaf_depths(ts.data_ptr(), n, spl, r, out.data_ptr())
-        e1.record(st)
-        torch.cuda.synchronize(dev)
+        ms = timed(1, args.steps)                                # split-FP16 tensor cores where H allows
         clocks = clk.stop()
-        ms = e0.elapsed_time(e1) / args.steps
-    H, L = c.spec.H, c.spec.L
-    ns = n * spl
+        tensor_used = H in (64, 128, 256)
     flops = ns * (6.0 * H + (L - 1) * 2.0 * H * H + L * 2.0 * H)
     sm_mhz = (clocks or {}).get("sm_mhz") or 1965.0
-    peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12   # FP32 FMA lanes x 2 FLOP x clock (B200_PROFILING.md units)
     ach = flops / (ms / 1e3) / 1e12
+    if tensor_used:
+        # executed tensor work: three H x H products per hidden layer (split operands) + the split-bias MMA
+        pk = _peaks()
+        exec_flops = ns * (L - 1) * (3.0 * 2 * H * H + 2.0 * 16 * H)
+        roof = {"bound": "tensor", "kernel": "k_tmlp_x3 (split-FP16 x3, Eq. 5 mode)",
+                "achieved": exec_flops / (ms / 1e3) / 1e12, "peak": pk["bf16"], "unit": "TFLOP/s",
+                "frac": exec_flops / (ms / 1e3) / 1e12 / pk["bf16"],
+                "peak_source": pk["src"] + " bf16_tflops (burst; FP16 kind::f16 has the BF16 rate)",
+                "flops_formula": "executed: samples x (L-1) x (3 x 2H^2 + 2 x 16 H)", "traffic": None}
+    else:
+        peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12   # FP32 FMA lanes x 2 FLOP x clock (B200_PROFILING.md units)
+        roof = {"bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                "peak_source": "derived: 148 SM x 128 FP32 FMA lanes x 2 FLOP x median SM clock", "traffic": None}
+    d_tc = out.cpu().numpy()
     cpu = None
     if not args.no_cpu:
         import oracle
@@ -293,11 +315,12 @@ def run_populate(args):
             "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"{c.name} octree finest leaves: {n} leaves x {spl} samples, r = 1.5e-4",
                        "model": f"{L}x{H} SIREN T-MLP (seeded init)"},
-            "roofline": {"bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
-                         "peak_source": "derived: 148 SM x 128 FP32 FMA lanes x 2 FLOP x median SM clock",
-                         "traffic": None},
+            "roofline": roof, "algorithmic_tflops": ach,
+            "fp32_simt": {"value": ns / (ms_simt / 1e3), "unit": "samples/s", "ms_per_step": ms_simt,
+                          "speedup_of_tensor_path": ms_simt / ms,
+                          "leaf_depth_agreement": float(np.mean(d_simt == d_tc))},
             "cpu_baseline": cpu, "clocks": clocks,
-            "depth_hist": np.bincount(out.cpu().numpy(), minlength=L + 1).tolist()}
+            "depth_hist": np.bincount(d_tc, minlength=L + 1).tolist()}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -560,7 +583,7 @@ def run_query(args):
     import torch.distributed as dist
 
     import sandgen as g
-    from paper_2604_25936_b200 import SAND_BF16, SAND_FP32, SandContext, partition
+    from paper_2604_25936_b200 import SAND_BF16, SAND_F16X3, SAND_FP32, SandContext, partition
 
     ws, rank, local = _dist()
     # one process per GPU; SAND_BENCH_SHARE_GPU=1 (test only) maps several ranks onto the visible GPUs
@@ -587,6 +610,8 @@ def run_query(args):
     p = c.params()
     dm = c.depthmap
     fp32 = args.prec == "fp32" or (args.prec is None and c.precision == SAND_FP32)
+    x3 = args.prec == "f16x3"
+    prec_code = SAND_F16X3 if x3 else SAND_FP32 if fp32 else SAND_BF16
     if args.full_depth:
         dm = g.VoxelMap(1, np.full(8, c.spec.L, np.uint8), None)
     weak = args.scaling == "weak"
@@ -610,7 +635,7 @@ def run_query(args):
     sdf = torch.empty(n, dtype=torch.float32, device=dev)
     dep = torch.empty(n, dtype=torch.uint8, device=dev)
 
-    ctx = SandContext(c.spec.L, c.spec.H, c.spec.omega0, SAND_FP32 if fp32 else SAND_BF16, c.spec.tail, dev_index)
+    ctx = SandContext(c.spec.L, c.spec.H, c.spec.omega0, prec_code, c.spec.tail, dev_index)
     if args.kprof:
         from paper_2604_25936_b200 import SAND_OPT_KPROF
         ctx.sand_set_option(SAND_OPT_KPROF, args.kprof)
@@ -673,7 +698,7 @@ def run_query(args):
 
     # the non-adaptive GPU baseline on the same points: an all-L depth map, same kernels (not in the timed region)
     ms_full = 0.0
-    if not args.full_depth and not args.no_full_depth and not fp32 and args.task == "query":
+    if not args.full_depth and not args.no_full_depth and not fp32 and not x3 and args.task == "query":
         ctx.sand_load_depthmap(g.VoxelMap(1, np.full(8, c.spec.L, np.uint8), None))
         k_fd = max(1, min(args.steps, 5))
         query()
@@ -746,7 +771,12 @@ def run_query(args):
             sm_mhz = (clocks or {}).get("sm_mhz") or 1965.0
             pk = dict(pk, bf16=148 * 128 * 2 * sm_mhz * 1e6 / 1e12, bf16_sus=148 * 128 * 2 * sm_mhz * 1e6 / 1e12,
                       src="derived FP32 ALU (148 SM x 128 lanes x 2 FLOP x median clock);")
-        kname = ("k_query_simt (FP32, one thread per point)" if fp32 and H <= 64 else
+        if x3:   # executed tensor work: 3 products of split FP16 operands per H x H layer (+ the split-bias MMA)
+            f_exec_rank0 = st["flops_exec"] * 3.0 + sum(st["per_depth"][d] * (d - 1) * 2.0 * 16 * H
+                                                         for d in range(2, c.spec.L + 1))
+            ach = f_exec_rank0 / (ms_mlp / 1e3) / 1e12
+        kname = ("k_tmlp_x3 (split-FP16 x3, CTA pair)" if x3 else
+                 "k_query_simt (FP32, one thread per point)" if fp32 and H <= 64 else
                  "k_query_fp32 (FP32 register-blocked GEMM)" if fp32 else
                  "k_tmlp_wide (K3 fused T-MLP, CTA pair, N-halves)" if H == 336 else
                  "k_tmlp_tc2 (K3 fused T-MLP, CTA pair)")
@@ -760,7 +790,7 @@ def run_query(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "weak" if weak else "strong",
-            "vs_baseline": None, "dtype": "f32" if fp32 else "bf16", "data": "synthetic",
+            "vs_baseline": None, "dtype": "f16x3" if x3 else "f32" if fp32 else "bf16", "data": "synthetic",
             "config": _arm_config(args, c, ws, wl_desc, summ["n_total"]),
             "roofline": {"bound": "alu" if fp32 else "tensor", "kernel": kname, "achieved": ach,
                          "peak": pk["bf16"], "unit": "TFLOP/s", "frac": ach / pk["bf16"],
@@ -768,7 +798,8 @@ def run_query(args):
                          "frac_vs_sustained": ach / pk["bf16_sus"],
                          "traffic": _traffic() if (args.config == "C2" and not fp32) else None,
                          "algorithmic_flops_per_launch": f_exec_rank0,
-                         "flops_formula": "executed H x H FLOPs sum_p (d_p - 1) * 2 H^2 (Eq. 2 reading R3)",
+                         "flops_formula": ("executed tensor FLOPs: 3 x sum_p (d_p - 1) 2 H^2 + split-bias MMAs" if x3 else
+                                           "executed H x H FLOPs sum_p (d_p - 1) * 2 H^2 (Eq. 2 reading R3)"),
                          "ms_per_launch": ms_mlp,
                          "traffic_source": TRAFFIC_SRC if (args.config == "C2" and not fp32) else None},
             # the other pipe the step needs: one sine per hidden unit per evaluated layer (Eq. 2), MUFU.SIN
@@ -816,7 +847,7 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=1 << 15)
     ap.add_argument("--full-depth", action="store_true", help="all-L depth map (non-adaptive GPU baseline)")
     ap.add_argument("--kprof", type=int, default=0, help="diagnostic SAND_OPT_KPROF (per-role counters, stderr)")
-    ap.add_argument("--prec", default=None, choices=["bf16", "fp32"],
+    ap.add_argument("--prec", default=None, choices=["bf16", "fp32", "f16x3"],
                     help="default: the config's precision (C0 FP32, others BF16); fp32: the accurate FP32 path "
                          "(SIMT), reported against the FP32 ALU peak")
     ap.add_argument("--task", default="query", choices=["query", "populate", "sweep", "dynamic", "mesh"],

@@ -53,8 +53,15 @@ typedef enum {
  *                the sine in FP32; supported H in {64, 128, 256, 336}; the per-column tables stay on
  *                chip, which bounds L (e.g. L <= 24 at H = 256; larger -> SAND_ERR_UNSUPPORTED).
  *                Tolerance 5e-3.
- *   SAND_TF32X3: reserved (returns SAND_ERR_UNSUPPORTED in this build).                        */
-typedef enum { SAND_FP32 = 0, SAND_TF32X3 = 1, SAND_BF16 = 2 } sand_precision;
+ *   SAND_TF32X3: reserved (returns SAND_ERR_UNSUPPORTED in this build): 3xTF32 operands take 4 bytes
+ *                per element, so a 256-row tile's split A operand (hi + lo) would not fit in shared memory.
+ *   SAND_F16X3 : FP32-accurate tensor-core path (tmlp_x3.cu): every H x H layer as three tcgen05 kind::f16
+ *                products of split operands, v = v_hi + v_lo (FP16 each, 22 significant bits):
+ *                A_hi W_hi + A_lo W_hi + A_hi W_lo, FP32 accumulate in TMEM; layer 1 in FP32 SIMT; sine with
+ *                a Cody-Waite reduction (~5e-7).  H in {64, 128, 256}.  Tolerance 1e-4 like SAND_FP32.
+ *                The same kernel evaluates the Eq. 5 population calls below whatever ctx's precision
+ *                (SAND_OPT_FP32_TENSOR).                                                            */
+typedef enum { SAND_FP32 = 0, SAND_TF32X3 = 1, SAND_BF16 = 2, SAND_F16X3 = 3 } sand_precision;
 
 /* Tail form: LINEAR t_i = a_i . h_i + c_i for every layer (BASELINE.json configs);
  * MULT t_1 linear, t_i = (a_i0 . h_i + c_i0) * (a_i1 . h_i + c_i1) for i >= 2 (Eq. 3).        */
@@ -119,12 +126,14 @@ int sand_set_stream(sand_ctx* ctx, void* cuda_stream);
  *                         pair kernel -> SAND_ERR_UNSUPPORTED.
  *   SAND_OPT_DYN_SCHEDULE [0] sand_query_dynamic: 0 = a 64-point tile stops when all its points have
  *                         stopped; 1 = pools of 512 points re-compacted after every layer.
- *   SAND_OPT_KPROF        [0] diagnostic: 1 = per-role clock64 wait / busy counters of the CTA-pair
- *                         kernels printed to stderr after every launch (adds a stream synchronisation);
- *                         2, 3 = timing-only modes that skip epilogue math / weight streaming in builds
- *                         compiled with -DSAND_DIAG=1 (wrong results; ignored otherwise).
+ *   SAND_OPT_KPROF        [0] diagnostic, -DSAND_DIAG=1 builds only (ignored otherwise): 1 = per-role
+ *                         clock64 wait / busy counters of the CTA-pair kernels printed to stderr after every
+ *                         launch (adds a stream synchronisation); 2, 3 = timing-only modes that skip epilogue
+ *                         math / weight streaming (wrong results).
+ *   SAND_OPT_FP32_TENSOR  [1] sand_required_depth / sand_populate_leaf_depths at H in {64, 128, 256}: 1 = the
+ *                         split-FP16 tensor-core kernel (SAND_F16X3 arithmetic), 0 = the FP32 SIMT kernel.
  * Errors: SAND_ERR_ARG (unknown option or value), SAND_ERR_UNSUPPORTED.                          */
-typedef enum { SAND_OPT_PAIR_KERNEL = 1, SAND_OPT_DYN_SCHEDULE = 2, SAND_OPT_KPROF = 3 } sand_option;
+typedef enum { SAND_OPT_PAIR_KERNEL = 1, SAND_OPT_DYN_SCHEDULE = 2, SAND_OPT_KPROF = 3, SAND_OPT_FP32_TENSOR = 4 } sand_option;
 int sand_set_option(sand_ctx* ctx, int option, int64_t value);
 int sand_get_option(const sand_ctx* ctx, int option, int64_t* value);
 
@@ -179,8 +188,9 @@ int sand_debug_perm(sand_ctx* ctx, uint32_t* host_perm, int64_t cap, int64_t* n_
 
 /* ---------------------------------------------------------------------------------------------------
  * Volumetric network-depth map population (the step before the query path; Sec. 3.2).
- * Both calls evaluate the full L-layer T-MLP in FP32 (sine to ~5e-7: Cody-Waite reduction to [-pi, pi],
- * then MUFU.SIN) whatever ctx's precision, because
+ * Both calls evaluate the full L-layer T-MLP in FP32 accuracy (sine to ~5e-7: Cody-Waite reduction to [-pi, pi],
+ * then MUFU.SIN) whatever ctx's precision -- on the tensor cores with split-FP16 operands (SAND_F16X3
+ * arithmetic) for H in {64, 128, 256}, else FP32 SIMT (SAND_OPT_FP32_TENSOR) -- because
  * Eq. 5 compares cumulative outputs against r (1.5e-4 in the paper).  Only the weights must be
  * loaded.  Asynchronous on ctx's stream.  Errors: SAND_ERR_ARG, SAND_ERR_STATE, SAND_ERR_UNSUPPORTED
  * (H not in {16, 32, 64, 128, 256, 336}), SAND_ERR_CUDA, SAND_ERR_OOM.                              */

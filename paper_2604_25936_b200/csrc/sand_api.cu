@@ -41,6 +41,10 @@ struct sand_ctx {
   void* d_wimage_pair = nullptr;
   float* d_whidden = nullptr;
   float* d_wt_f32 = nullptr;      // FP32 hidden weights transposed [L-1][k][j] (depth-map population)
+  void* d_x3_image = nullptr;     // split-FP16 hidden-layer image (tmlp_x3.cu)
+  float* d_x3_tables = nullptr;
+  bool have_x3 = false;
+  int fp32_tensor = 1;            // SAND_OPT_FP32_TENSOR
   uint8_t* d_dp_tmp = nullptr;    // per-sample depths of sand_populate_leaf_depths
   long long cap_dp = 0;
   // marching cubes (mesh.cu): grid axis, slab buffers of the fused extraction, triangle counter
@@ -118,6 +122,7 @@ static bool supported(const sand_config& c) {
   if (c.prec == SAND_BF16)
     return tc_supported_H(c.H) && (tc2_usable(c.L, c.H, c.tail) || tc3_usable(c.L, c.H, c.tail) ||
                                    tc_smem_bytes(c.L, c.H, c.tail) > 0);
+  if (c.prec == SAND_F16X3) return x3_usable(c.L, c.H, c.tail, 0);
   return false;
 }
 
@@ -134,7 +139,7 @@ extern "C" int sand_create(const sand_config* cfg, sand_ctx** out) {
   if (!(cfg->omega0 > 0.0f) || !std::isfinite(cfg->omega0)) return fail(nullptr, SAND_ERR_ARG, "omega0 must be > 0");
   if (cfg->H < 1) return fail(nullptr, SAND_ERR_ARG, "H must be positive");
   if (cfg->tail != SAND_TAIL_LINEAR && cfg->tail != SAND_TAIL_MULT) return fail(nullptr, SAND_ERR_ARG, "bad tail mode");
-  if (cfg->prec != SAND_FP32 && cfg->prec != SAND_BF16 && cfg->prec != SAND_TF32X3)
+  if (cfg->prec != SAND_FP32 && cfg->prec != SAND_BF16 && cfg->prec != SAND_TF32X3 && cfg->prec != SAND_F16X3)
     return fail(nullptr, SAND_ERR_ARG, "bad precision");
   if (!supported(*cfg))
     return fail(nullptr, SAND_ERR_UNSUPPORTED, "unsupported (precision %d, L %d, H %d, tail %d)", (int)cfg->prec,
@@ -176,6 +181,7 @@ static void free_depthmap(sand_ctx* c) {
 }
 static void free_weights(sand_ctx* c) {
   dfree(c->d_tables); dfree(c->d_pair_tables); dfree(c->d_w1_image); dfree(c->d_wimage); dfree(c->d_wimage_pair); dfree(c->d_whidden); dfree(c->d_wt_f32);
+  dfree(c->d_x3_image); dfree(c->d_x3_tables); c->have_x3 = false;
   c->have_w = false;
 }
 static void free_hostpipe(sand_ctx* c) {
@@ -344,6 +350,21 @@ extern "C" int sand_load_weights(sand_ctx* ctx, const float* blob, size_t n_floa
       }
     }
   }
+  if (x3_available(H)) {
+    // split-FP16 x3 kernel (F16X3 queries and the FP32-accurate Eq. 5 population on tensor cores)
+    std::vector<float> xt;
+    std::vector<uint8_t> ximg;
+    x3_build_host(L, H, tail, w0, W.data(), b.data(), a.data(), a1.data(), c.data(), c1.data(), &m, &xt, &ximg);
+    CU(cudaMalloc(&ctx->d_x3_tables, sizeof(float) * xt.size()));
+    CU(cudaMemcpy(ctx->d_x3_tables, xt.data(), sizeof(float) * xt.size(), cudaMemcpyHostToDevice));
+    m.x3_tables = ctx->d_x3_tables;
+    if (!ximg.empty()) {
+      CU(cudaMalloc(&ctx->d_x3_image, ximg.size()));
+      CU(cudaMemcpy(ctx->d_x3_image, ximg.data(), ximg.size(), cudaMemcpyHostToDevice));
+    }
+    m.x3_image = ctx->d_x3_image;
+    ctx->have_x3 = true;
+  }
   if (L >= 2) {
     // FP32 W^T for the depth-map population kernels (Eq. 5 needs FP32 whatever the query precision)
     std::vector<float> wt((size_t)(L - 1) * H * H);
@@ -474,6 +495,11 @@ extern "C" int sand_set_stream(sand_ctx* ctx, void* s) {
   return SAND_OK;
 }
 
+// Eq. 5 population on the split-FP16 tensor-core kernel when the width and shared memory allow it
+static bool use_x3_population(const sand_ctx* ctx) {
+  return ctx->fp32_tensor && ctx->have_x3 && x3_usable(ctx->cfg.L, ctx->cfg.H, ctx->cfg.tail, 1);
+}
+
 extern "C" int sand_set_option(sand_ctx* ctx, int option, int64_t value) {
   if (!ctx) return fail(ctx, SAND_ERR_ARG, "NULL ctx");
   switch (option) {
@@ -485,6 +511,10 @@ extern "C" int sand_set_option(sand_ctx* ctx, int option, int64_t value) {
     case SAND_OPT_DYN_SCHEDULE:
       if (value != 0 && value != 1) return fail(ctx, SAND_ERR_ARG, "SAND_OPT_DYN_SCHEDULE takes 0 or 1");
       ctx->dyn_schedule = (int)value;
+      return SAND_OK;
+    case SAND_OPT_FP32_TENSOR:
+      if (value != 0 && value != 1) return fail(ctx, SAND_ERR_ARG, "SAND_OPT_FP32_TENSOR takes 0 or 1");
+      ctx->fp32_tensor = (int)value;
       return SAND_OK;
     case SAND_OPT_KPROF:
       if (value < 0 || value > 3) return fail(ctx, SAND_ERR_ARG, "SAND_OPT_KPROF takes 0..3");
@@ -502,6 +532,7 @@ extern "C" int sand_get_option(const sand_ctx* ctx, int option, int64_t* value) 
     case SAND_OPT_PAIR_KERNEL: *value = ctx->use_pair ? 1 : 0; return SAND_OK;
     case SAND_OPT_DYN_SCHEDULE: *value = ctx->dyn_schedule; return SAND_OK;
     case SAND_OPT_KPROF: *value = ctx->kprof; return SAND_OK;
+    case SAND_OPT_FP32_TENSOR: *value = ctx->fp32_tensor; return SAND_OK;
     default: return SAND_ERR_ARG;
   }
 }
@@ -565,7 +596,9 @@ extern "C" int sand_query(sand_ctx* ctx, const float* d_points, int64_t n, float
                  ctx->d_meta, ctx->d_scan, st));
   CU(launch_scatter(d_depth, n, ctx->cfg.L, ctx->d_offs, ctx->d_perm, nblk, st));
   CU(cudaEventRecord(ev[2], st));
-  if (ctx->cfg.prec == SAND_FP32 && !simt_supported_H(ctx->cfg.H))
+  if (ctx->cfg.prec == SAND_F16X3)
+    CU(launch_tmlp_x3(ctx->mlp, d_points, ctx->d_perm, ctx->d_meta, d_sdf, ctx->num_sms, st));
+  else if (ctx->cfg.prec == SAND_FP32 && !simt_supported_H(ctx->cfg.H))
     CU(launch_query_fp32(ctx->mlp, ctx->d_wt_f32, d_points, ctx->d_perm, ctx->d_meta, d_sdf, ctx->num_sms, st));
   else if (ctx->cfg.prec == SAND_FP32)
     CU(launch_tmlp_simt(ctx->mlp, d_points, ctx->d_perm, ctx->d_meta, d_sdf, ctx->num_sms, st));
@@ -783,8 +816,11 @@ extern "C" int sand_required_depth(sand_ctx* ctx, const float* d_points, int64_t
   if (!d_points || !d_out_depth) return fail(ctx, SAND_ERR_ARG, "NULL buffer");
   if (!depthpop_supported(ctx->cfg.H)) return fail(ctx, SAND_ERR_UNSUPPORTED, "H = %d", ctx->cfg.H);
   CU(cudaSetDevice(ctx->cfg.device));
-  CU(launch_required_depth(ctx->mlp, ctx->d_wt_f32, d_points, n, r, near ? 1 : 0, d_out_depth, ctx->num_sms,
-                           ctx->stream));
+  if (use_x3_population(ctx))
+    CU(launch_required_depth_x3(ctx->mlp, d_points, n, r, near ? 1 : 0, d_out_depth, ctx->num_sms, ctx->stream));
+  else
+    CU(launch_required_depth(ctx->mlp, ctx->d_wt_f32, d_points, n, r, near ? 1 : 0, d_out_depth, ctx->num_sms,
+                             ctx->stream));
   return SAND_OK;
 }
 
@@ -829,7 +865,10 @@ extern "C" int sand_populate_leaf_depths(sand_ctx* ctx, const float* d_samples, 
     CU(cudaMalloc(&ctx->d_dp_tmp, (size_t)ns));
     ctx->cap_dp = ns;
   }
-  CU(launch_required_depth(ctx->mlp, ctx->d_wt_f32, d_samples, ns, r, 1, ctx->d_dp_tmp, ctx->num_sms, ctx->stream));
+  if (use_x3_population(ctx))
+    CU(launch_required_depth_x3(ctx->mlp, d_samples, ns, r, 1, ctx->d_dp_tmp, ctx->num_sms, ctx->stream));
+  else
+    CU(launch_required_depth(ctx->mlp, ctx->d_wt_f32, d_samples, ns, r, 1, ctx->d_dp_tmp, ctx->num_sms, ctx->stream));
   CU(launch_leaf_max(ctx->d_dp_tmp, n_leaves, samples_per_leaf, d_leaf_depth, ctx->stream));
   return SAND_OK;
 }

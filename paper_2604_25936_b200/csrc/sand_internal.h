@@ -77,6 +77,12 @@ struct MlpDev {
   const void* w1_image;      // layer-1 split-BF16 B operand, [2 halves][H/2 rows][16 bf16] (l1_off layout)
   long long pt_floats, pt_off_l1, pt_off_bias, pt_off_a, pt_off_a1, pt_off_c, pt_off_c1, pt_off_csum;
   int kprof;                 // diagnostic (SAND_OPT_KPROF): per-role clock counters, synchronous dump
+  // split-FP16 x3 kernel (tmlp_x3.cu, FP32-accurate on tensor cores): per (layer, CTA) image
+  // [split bias][KC W_hi chunks][KC W_lo chunks] and FP32 tables: w1 float4 [H] (w0 W1, w0 b1), a [L][H],
+  // a1 [L-1][H] (MULT), c [L], c1 [L]
+  const void* x3_image;
+  const float* x3_tables;
+  long long x3_floats, x3_off_w1, x3_off_a, x3_off_a1, x3_off_c, x3_off_c1;
 };
 
 
@@ -134,5 +140,15 @@ void tc3_build_host(int L, int H, float w0, const float* const* W, const float* 
 cudaError_t launch_tmlp_tc3(const MlpDev& m, const float* pts, const uint32_t* perm, const QueryMeta* meta,
                             float* out, int num_sms, cudaStream_t st);
 cudaError_t prepare_tc3();
+// FP32-accurate CTA-pair kernel on split-FP16 operands (tmlp_x3.cu): query and Eq. 5 population modes
+bool x3_available(int H);
+bool x3_usable(int L, int H, int tail, int pop);
+void x3_build_host(int L, int H, int tail, float w0, const float* const* W, const float* const* b,
+                   const float* const* a, const float* const* a1, const float* c, const float* c1, MlpDev* m,
+                   std::vector<float>* tables, std::vector<uint8_t>* img);
+cudaError_t launch_tmlp_x3(const MlpDev& m, const float* pts, const uint32_t* perm, const QueryMeta* meta, float* out,
+                           int num_sms, cudaStream_t st);
+cudaError_t launch_required_depth_x3(const MlpDev& m, const float* pts, long long n, float r, int near, uint8_t* out,
+                                     int num_sms, cudaStream_t st);
 
 }  // namespace sand

@@ -319,6 +319,7 @@ static cudaError_t prep_tc_t() {
 
 
 int tmlp_tile_rows(int H, int prec, bool use_pair) {
+  if (prec == SAND_F16X3) return 256;
   return (prec == SAND_BF16 && use_pair && (tc2_available(H) || tc3_available(H, SAND_TAIL_LINEAR))) ? 256 : kTileM;
 }
 

@@ -14,9 +14,9 @@ from .build import LIB as _LIB_PATH
 SAND_OK = 0
 SAND_ERR_ARG, SAND_ERR_STATE, SAND_ERR_SIZE, SAND_ERR_DEPTHMAP = -1, -2, -3, -4
 SAND_ERR_CUDA, SAND_ERR_OOM, SAND_ERR_UNSUPPORTED = -5, -6, -7
-SAND_FP32, SAND_TF32X3, SAND_BF16 = 0, 1, 2
+SAND_FP32, SAND_TF32X3, SAND_BF16, SAND_F16X3 = 0, 1, 2, 3
 SAND_TAIL_LINEAR, SAND_TAIL_MULT = 0, 1
-SAND_OPT_PAIR_KERNEL, SAND_OPT_DYN_SCHEDULE, SAND_OPT_KPROF = 1, 2, 3
+SAND_OPT_PAIR_KERNEL, SAND_OPT_DYN_SCHEDULE, SAND_OPT_KPROF, SAND_OPT_FP32_TENSOR = 1, 2, 3, 4
 SAND_MAX_L = 32
 SAND_DEPTH_NONFINITE = 255
 

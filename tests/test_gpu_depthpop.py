@@ -45,32 +45,36 @@ def _run_required(ctx, pts, r, near):
     return out.cpu().numpy().astype(np.int64)
 
 
+@pytest.mark.parametrize("tensor", [1, 0])
 @pytest.mark.parametrize("H,L,tail,prec", [(16, 4, 0, 0), (64, 6, 1, 0), (256, 8, 0, 2), (256, 8, 1, 2),
-                                           (336, 8, 0, 2), (128, 5, 0, 2)])
+                                           (336, 8, 0, 2), (128, 5, 0, 2), (64, 1, 0, 2)])
 @pytest.mark.parametrize("near", [True, False])
-def test_required_depth_matches_oracle(H, L, tail, prec, near):
-    from paper_2604_25936_b200 import SandContext
+def test_required_depth_matches_oracle(H, L, tail, prec, near, tensor):
+    """tensor = 1: H in {64, 128, 256} on the split-FP16 tensor-core kernel (tmlp_x3.cu); 0: FP32 SIMT."""
+    from paper_2604_25936_b200 import SAND_OPT_FP32_TENSOR, SandContext
     spec = g.TMlpSpec(L=L, H=H, omega0=30.0, tail=tail, seed=41)
     p = g.make_weights(spec)
     pts = np.random.default_rng(42).uniform(-1, 1, (20011, 3)).astype(np.float32)
     _, _, ys = oracle.tmlp_trace(p, pts)
-    r = float(np.quantile(np.abs(ys[-1] - ys[L // 2]), 0.5))   # spreads the decisions over 1..L
+    r = float(np.quantile(np.abs(ys[-1] - ys[L // 2]), 0.5)) if L > 1 else 1e-3   # spreads the decisions over 1..L
     d_or = oracle.required_depth(p, pts, r, near=near)
     with SandContext(L, H, 30.0, prec, tail, 0) as ctx:
+        ctx.sand_set_option(SAND_OPT_FP32_TENSOR, tensor)
         ctx.sand_load_weights(g.pack_blob(p))
         d = _run_required(ctx, pts, r, near)
     assert d.min() >= 1 and d.max() <= L
     mism = d != d_or
     assert mism.mean() < 0.01, f"{mism.mean():.4f} of points differ"
     assert np.all(_valid(ys[:, mism], d[mism], r, near)), "GPU depth invalid under Eq. 5 at differing points"
-    if near:
+    if near and L > 1:
         assert len(np.unique(d_or)) > 1   # the threshold really decides something
 
 
-def test_populate_leaf_depths_c2_octree_leaves():
+@pytest.mark.parametrize("tensor", [1, 0])
+def test_populate_leaf_depths_c2_octree_leaves(tensor):
     """Eq. 6 on the C2 octree's finest leaves with the paper's r = 1.5e-4 and a loose r."""
     import torch
-    from paper_2604_25936_b200 import SandContext
+    from paper_2604_25936_b200 import SAND_OPT_FP32_TENSOR, SandContext
     c = g.make_config("C2")
     p = c.params()
     oc = c.depthmap
@@ -78,6 +82,7 @@ def test_populate_leaf_depths_c2_octree_leaves():
     samples = g.leaf_samples(oc.leaf_level[sel], oc.leaf_ijk[sel], 16, seed=5)   # 25 per leaf
     n, spl = samples.shape[0], samples.shape[1]
     with SandContext(c.spec.L, c.spec.H, 30.0, 2, 0, 0) as ctx:
+        ctx.sand_set_option(SAND_OPT_FP32_TENSOR, tensor)
         ctx.sand_load_weights(g.pack_blob(p))
         ts = torch.from_numpy(np.ascontiguousarray(samples.reshape(-1, 3))).cuda()
         for r in (1.5e-4, 0.05):

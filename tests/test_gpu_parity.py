@@ -355,3 +355,42 @@ def test_full_sdf_all_points(name):
         idx = np.arange(q0, min(q0 + step, pts.shape[0]))
         sdf_or, dep_or = oracle_query(p, c.depthmap, pts[idx])
         assert_parity(sdf, dep, sdf_or, dep_or, TOL_BF16, idx=idx)
+
+
+@pytest.mark.parametrize("H", [64, 128, 256])
+@pytest.mark.parametrize("tail", [0, 1])
+def test_f16x3_random_depths(H, tail):
+    """SAND_F16X3 (split-FP16 three-product MMAs, FP32 accuracy): mixed depths 1..L with ragged tiles at the
+    FP32 tolerance 1e-4 against the FP32 C oracle."""
+    from paper_2604_25936_b200 import SAND_F16X3
+    L = 6
+    spec = g.TMlpSpec(L=L, H=H, omega0=30.0, tail=tail, seed=70 + H)
+    p = g.make_weights(spec)
+    dm = _random_voxel_map(3, L, 71)
+    pts = _pts(30011, 72)
+    pts[17] = [np.nan, 0, 0]
+    with make_ctx(spec, SAND_F16X3) as ctx:
+        sdf, dep = run_engine(ctx, p, dm, pts)
+    sdf_or, dep_or = oracle_query(p, dm, pts)
+    assert_parity(sdf, dep, sdf_or, dep_or, TOL_FP32)
+
+
+def test_f16x3_c0_full_and_c2_sample():
+    """BASELINE.json configs[0] (the FP32 config) on the split-FP16 tensor path, every point; and C2's 8 x 256 net
+    on a stratified sample of its grid, both at the FP32 tolerance."""
+    from paper_2604_25936_b200 import SAND_F16X3
+    c = g.make_config("C0")
+    p = c.params()
+    pts = c.points_fn()
+    with make_ctx(c.spec, SAND_F16X3) as ctx:
+        sdf, dep = run_engine(ctx, p, c.depthmap, pts)
+    sdf_or, dep_or = oracle_query(p, c.depthmap, pts)
+    assert_parity(sdf, dep, sdf_or, dep_or, TOL_FP32)
+    c = g.make_config("C2")
+    p = c.params()
+    pts = g.grid_points_slab(512, 240, 272)
+    with make_ctx(c.spec, SAND_F16X3) as ctx:
+        sdf, dep = run_engine(ctx, p, c.depthmap, pts)
+    idx = stratified_sample(dep, 4096, 1 << 15, seed=3)
+    sdf_or, dep_or = oracle_query(p, c.depthmap, pts[idx])
+    assert_parity(sdf, dep, sdf_or, dep_or, TOL_FP32, idx=idx)
