@@ -19,7 +19,7 @@ __device__ __forceinline__ uint32_t cell_of(float x, float scale, float maxc) {
   float u = __fadd_rn(x, 1.0f);
   float v = __fmul_rn(u, scale);
   v = fminf(fmaxf(v, 0.0f), maxc);
-  return (uint32_t)v;  // v >= 0 : truncation == floor
+  return (uint32_t)v;  // v >= 0 : truncation == floor (an FADD.RZ + 2^23 variant measured 4% slower)
 }
 
 struct LookupResult {
@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(kLookupThreads) k_lookup(const float* __restri
                                                             LookupParams lp, uint8_t* __restrict__ out_depth,
                                                             float* __restrict__ out_sdf,
                                                             uint32_t* __restrict__ hist, long long nblk,
-                                                            int vec_in, int vec_out) {
+                                                            int vec_in, int vec_out, int vec_sdf) {
   __shared__ uint32_t sh[kMaxBins];
   const int nb = lp.L + 2;
   for (int i = threadIdx.x; i < nb; i += blockDim.x) sh[i] = 0;
@@ -108,12 +108,26 @@ __global__ void __launch_bounds__(kLookupThreads) k_lookup(const float* __restri
     }
     uint32_t dw = 0;
     int bins[4];
+    float far[4];
+    int nfar = 0;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const LookupResult r = lookup_one(px[j], py[j], pz[j], lp, scale, maxc);
       dw |= (r.d & 0xFFu) << (8 * j);
       bins[j] = (j < cnt) ? (r.d == SAND_DEPTH_NONFINITE ? lp.L + 1 : (int)r.d) : -1;
-      if (j < cnt && (r.d == 0 || r.d == SAND_DEPTH_NONFINITE)) out_sdf[p0 + j] = r.far;
+      far[j] = r.far;
+      nfar += (j < cnt && (r.d == 0 || r.d == SAND_DEPTH_NONFINITE)) ? 1 : 0;
+    }
+    // cached / NaN sdf of far and non-finite points (Eq. 7): one 16-byte store when all four need it (the
+    // far-field regime), else per point
+    if (nfar == 4 && vec_sdf) {
+      __stcs(reinterpret_cast<float4*>(out_sdf + p0), make_float4(far[0], far[1], far[2], far[3]));
+    } else if (nfar) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t dj = (dw >> (8 * j)) & 0xFFu;
+        if (j < cnt && (dj == 0 || dj == SAND_DEPTH_NONFINITE)) out_sdf[p0 + j] = far[j];
+      }
     }
     if (cnt == 4 && vec_out) {
       *reinterpret_cast<uint32_t*>(out_depth + p0) = dw;
@@ -229,79 +243,51 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_offs(const uint32_t* __re
   }
 }
 
+// K2b: stable scatter.  Warp w of a block owns the contiguous points [512 w, 512 w + 512) of the block's 4096
+// and walks them in 16 rounds of 32 (lane i <-> point 32 r + i), so the stable order is round-major, lane
+// order within a round.  Per round one __match_any_sync groups the lanes of equal depth; a point's rank is
+// its warp's running count of that depth (shared memory, updated by the group's first lane) plus the
+// number of equal lanes below it.  After all rounds one block-wide prefix over the warps' counts gives every
+// warp its base per depth, and the 16 (depth, rank) pairs kept in registers are written out.
 __global__ void __launch_bounds__(kLookupThreads) k_scatter(const uint8_t* __restrict__ depth, long long n,
                                                              int L, const uint32_t* __restrict__ offs,
-                                                             uint32_t* __restrict__ perm, long long nblk,
-                                                             int vec) {
+                                                             uint32_t* __restrict__ perm, long long nblk) {
   constexpr int kWarps = kLookupThreads / 32;
-  __shared__ uint32_t run[kMaxBins];
-  __shared__ uint32_t wtot[kWarps][kMaxBins];
-  __shared__ uint32_t btot[kMaxBins];
+  constexpr int kRounds = kLookupChunk / kLookupThreads;   // 16
+  __shared__ uint32_t wcnt[kWarps][kMaxBins];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned lt = (1u << lane) - 1u;
-  for (int d = tid; d < kMaxBins; d += blockDim.x) {
-    run[d] = (d >= 1 && d <= L) ? offs[(long long)d * nblk + blockIdx.x] : 0u;
-    for (int w = 0; w < kWarps; ++w) wtot[w][d] = 0;
+  for (int d = lane; d < kMaxBins; d += 32) wcnt[warp][d] = 0;
+  __syncwarp();
+  const long long p0 = (long long)blockIdx.x * kLookupChunk + (long long)warp * (32 * kRounds) + lane;
+  uint32_t key[kRounds];   // (depth << 16) | rank within the warp, depth 0 = not binned
+#pragma unroll
+  for (int r = 0; r < kRounds; ++r) {   // all loads first (independent of the ranking chain)
+    const long long pt = p0 + 32 * r;
+    key[r] = pt < n ? __ldcs(depth + pt) : 0u;
+  }
+#pragma unroll
+  for (int r = 0; r < kRounds; ++r) {
+    uint32_t d = key[r];
+    if (d < 1 || d > (uint32_t)L) d = 0;   // far, non-finite or padding: not binned
+    const unsigned m = __match_any_sync(0xffffffffu, d);
+    const uint32_t before = wcnt[warp][d];
+    __syncwarp();
+    if (lane == __ffs(m) - 1) wcnt[warp][d] = before + (uint32_t)__popc(m);
+    __syncwarp();
+    key[r] = (d << 16) | (before + (uint32_t)__popc(m & lt));
   }
   __syncthreads();
-  const long long base = (long long)blockIdx.x * kLookupChunk;
-#pragma unroll 1
-  for (int it = 0; it < kLookupChunk / (4 * kLookupThreads); ++it) {
-    const long long p0 = base + (long long)it * 4 * kLookupThreads + 4 * tid;
-    const long long rem = n - p0;
-    const int cnt = rem >= 4 ? 4 : (rem > 0 ? (int)rem : 0);
-    int dj[4];
-    if (cnt == 4 && vec) {
-      const uint32_t w4 = *reinterpret_cast<const uint32_t*>(depth + p0);
+  // warp bases: base[w][d] = offs[d][block] + sum of warps < w (in place over wcnt)
+  if (tid >= 1 && tid <= L) {
+    uint32_t acc = offs[(long long)tid * nblk + blockIdx.x];
+    for (int w = 0; w < kWarps; ++w) { const uint32_t t = wcnt[w][tid]; wcnt[w][tid] = acc; acc += t; }
+  }
+  __syncthreads();
 #pragma unroll
-      for (int j = 0; j < 4; ++j) dj[j] = (w4 >> (8 * j)) & 0xFF;
-    } else {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) dj[j] = (j < cnt) ? depth[p0 + j] : 0;
-    }
-    unsigned mine = 0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (dj[j] < 1 || dj[j] > L) dj[j] = 0;  // not binned: far, non-finite or padding
-      if (dj[j]) mine |= 1u << (dj[j] - 1);
-    }
-    unsigned present = __reduce_or_sync(0xffffffffu, mine);
-    int rank[4] = {0, 0, 0, 0};
-    while (present) {
-      const int v = __ffs(present);  // depth value v (bit v-1)
-      present &= present - 1;
-      unsigned tot = 0, before = 0;
-      unsigned m[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        m[j] = __ballot_sync(0xffffffffu, dj[j] == v);
-        tot += __popc(m[j]);
-        before += __popc(m[j] & lt);
-      }
-      int local = 0;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if (dj[j] == v) { rank[j] = (int)before + local; ++local; }
-      }
-      if (lane == 0) wtot[warp][v] = tot;
-    }
-    __syncthreads();
-    if (tid >= 1 && tid <= L) {
-      uint32_t acc = 0;
-      for (int w = 0; w < kWarps; ++w) { const uint32_t t = wtot[w][tid]; wtot[w][tid] = acc; acc += t; }
-      btot[tid] = acc;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (dj[j]) perm[run[dj[j]] + wtot[warp][dj[j]] + rank[j]] = (uint32_t)(p0 + j);
-    }
-    __syncthreads();
-    if (tid >= 1 && tid <= L) {
-      run[tid] += btot[tid];
-      for (int w = 0; w < kWarps; ++w) wtot[w][tid] = 0;
-    }
-    __syncthreads();
+  for (int r = 0; r < kRounds; ++r) {
+    const uint32_t d = key[r] >> 16;
+    if (d) perm[wcnt[warp][d] + (key[r] & 0xFFFFu)] = (uint32_t)(p0 + 32 * r);
   }
 }
 
@@ -353,8 +339,9 @@ cudaError_t launch_lookup(const float* pts, long long n, const LookupParams& lp,
                           float* out_sdf, uint32_t* hist, long long nblk, cudaStream_t st) {
   const int vec_in = ((reinterpret_cast<uintptr_t>(pts) & 15) == 0) ? 1 : 0;
   const int vec_out = ((reinterpret_cast<uintptr_t>(out_depth) & 3) == 0) ? 1 : 0;
+  const int vec_sdf = ((reinterpret_cast<uintptr_t>(out_sdf) & 15) == 0) ? 1 : 0;
   k_lookup<<<(unsigned)nblk, kLookupThreads, 0, st>>>(pts, n, lp, out_depth, out_sdf, hist, nblk, vec_in,
-                                                      vec_out);
+                                                      vec_out, vec_sdf);
   return cudaGetLastError();
 }
 
@@ -376,8 +363,7 @@ cudaError_t launch_scan(const uint32_t* hist, long long nblk, int L, int tile_ro
 
 cudaError_t launch_scatter(const uint8_t* depth, long long n, int L, const uint32_t* offs, uint32_t* perm,
                            long long nblk, cudaStream_t st) {
-  const int vec = ((reinterpret_cast<uintptr_t>(depth) & 3) == 0) ? 1 : 0;
-  k_scatter<<<(unsigned)nblk, kLookupThreads, 0, st>>>(depth, n, L, offs, perm, nblk, vec);
+  k_scatter<<<(unsigned)nblk, kLookupThreads, 0, st>>>(depth, n, L, offs, perm, nblk);
   return cudaGetLastError();
 }
 
