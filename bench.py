@@ -443,6 +443,18 @@ def run_dynamic(args):
             return e0.elapsed_time(e1) / k
 
         ms_oct = timed(lambda: ctx.sand_query(pts.data_ptr(), n, sdf.data_ptr(), dep.data_ptr()), 5)
+        # the octree path in the dynamic path's own arithmetic (FP32 SIMT) and on the FP32-accurate tensor
+        # path, so that the ratio below compares the methods, not SIMT against tensor cores
+        oct_same = {}
+        from paper_2604_25936_b200 import SAND_F16X3, SAND_FP32
+        for pname, pcode in (("fp32_simt", SAND_FP32), ("f16x3_tensor", SAND_F16X3)):
+            with SandContext(c.spec.L, c.spec.H, c.spec.omega0, pcode, c.spec.tail, 0) as cx:
+                cx.sand_load_weights(g.pack_blob(p))
+                cx.sand_load_depthmap(c.depthmap)
+                cx.sand_reserve(n)
+                cx.sand_set_stream(st.cuda_stream)
+                ms_p = timed(lambda: cx.sand_query(pts.data_ptr(), n, sdf.data_ptr(), dep.data_ptr()), steps)
+                oct_same[pname] = {"value": n / (ms_p / 1e3), "unit": UNIT, "ms_per_step": ms_p}
         for mode in ("tile", "pool"):   # tile-level early exit / pools re-compacted after every layer
             ctx.sand_set_option(SAND_OPT_DYN_SCHEDULE, 1 if mode == "pool" else 0)
             for name, r in (("paper r = 1.5e-4", 1.5e-4), (f"r = 30% quantile of |t_i| ({r30:.3e})", r30)):
@@ -469,6 +481,11 @@ def run_dynamic(args):
             "config": {"workload": f"C2 512^3 grid ({n} points), 8x256 SIREN T-MLP (seeded init)"},
             "octree_path": {"value": n / (ms_oct / 1e3), "unit": UNIT, "ms_per_step": ms_oct,
                             "dtype": "bf16", "note": "sand_query with C2's level-7 octree, same points"},
+            "octree_path_fp32": oct_same,
+            "method_gap": {e["threshold"] + " / " + e["mode"]: e["ms_per_step"] / oct_same["fp32_simt"]["ms_per_step"]
+                           for e in entries},
+            "method_gap_note": "dynamic-exit time / octree-path time, both FP32 SIMT (the paper: 13.67 s / 0.378 s = 36x, "
+                               "P:761-762, on its trained nets where most of the grid is far field)",
             "entries": entries, "cpu_baseline": cpu}
     print(json.dumps(line), flush=True)
     return 0

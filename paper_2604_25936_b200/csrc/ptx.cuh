@@ -74,7 +74,10 @@ __device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-__device__ __forceinline__ void mbar_wait_lazy(uint32_t bar, uint32_t parity, uint32_t ns = 256) {
+#ifndef SAND_LAZY_NS
+#define SAND_LAZY_NS 256
+#endif
+__device__ __forceinline__ void mbar_wait_lazy(uint32_t bar, uint32_t parity, uint32_t ns = SAND_LAZY_NS) {
   while (!mbar_test(bar, parity)) __nanosleep(ns);
 }
 

@@ -83,6 +83,9 @@ static_assert(!SAND_SMR || 4 * (SAND_SMR_EPI - 96) <= 96 - SAND_SMR_CTL, "setmax
 #ifndef SAND_BW
 #define SAND_BW 16   // accumulator columns per TMEM load batch (8, 16 or 32)
 #endif
+#ifndef SAND_EPI_BARWAIT
+#define SAND_EPI_BARWAIT 1   // accumulator waits: one polling warp per column group + a named barrier
+#endif
 #ifndef SAND_PDEG
 #define SAND_PDEG 7
 #endif
@@ -643,7 +646,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
         constexpr bool ST = SAND_SPLIT_STORE ? decltype(st_c)::value : true;
         {
           const long long w0_ = (SAND_DIAG && p.prof) ? clock64() : 0;
-          mbar_wait(b_accfull + 16 * s + 8 * decltype(pass_c)::value, e.pe);
+          if (SAND_EPI_BARWAIT) {
+            // one warp of the column group polls the mbarrier, the other three sleep in a named barrier
+            // (16 spinning warps per CTA would flood the MIO queue the sines use with barrier polls)
+            if ((ew & 3) == 0) mbar_wait(b_accfull + 16 * s + 8 * decltype(pass_c)::value, e.pe);
+            named_bar_sync(5 + cq, 128);
+          } else {
+            mbar_wait(b_accfull + 16 * s + 8 * decltype(pass_c)::value, e.pe);
+          }
           if (SAND_DIAG && p.prof) wt += clock64() - w0_;
           tc_fence_after();
         }

@@ -6,7 +6,7 @@ mkdir -p abl/obj
 C=paper_2604_25936_b200/csrc
 F="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr -I include"
 objs=""
-for src in sand_api lookup tmlp_simt tmlp_tc tmlp_tc3 depthpop mesh; do
+for src in sand_api lookup tmlp_simt tmlp_tc tmlp_tc3 tmlp_x3 depthpop mesh; do
   nvcc $F ${ALLDEFS} -c $C/$src.cu -o abl/obj/$src.o & objs="$objs abl/obj/$src.o"
 done
 for spec in "$@"; do
