@@ -855,7 +855,7 @@ def main():
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                     help="strong: the config's fixed grid cut into work-balanced z-slabs; weak: the grid refined "
                          "along z to R x R x RN so every rank holds ~R^3 points")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--e2e-chunk", type=int, default=0, help="points per host-pipeline chunk (0: library default)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")

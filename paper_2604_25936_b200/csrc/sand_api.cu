@@ -19,8 +19,15 @@
 
 #include "../../include/sand.h"
 #include "sand_internal.h"
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: ranges for nsys / ncu timelines, inert without a tool
 
 using namespace sand;
+
+// Host-side NVTX range (enqueue of a library stage) -- SURVEY 5's profiling aux.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 struct sand_ctx {
   sand_config cfg{};
@@ -589,13 +596,21 @@ extern "C" int sand_query(sand_ctx* ctx, const float* d_points, int64_t n, float
   }
   const size_t qi = ctx->nq++;
   cudaEvent_t* ev = ctx->evq[qi].data();
+  NvtxRange nq("sand_query");
   CU(cudaEventRecord(ev[0], st));
-  CU(launch_lookup(d_points, n, lp, d_depth, d_sdf, ctx->d_hist, nblk, st));
+  {
+    NvtxRange r("K1 depth-map lookup");
+    CU(launch_lookup(d_points, n, lp, d_depth, d_sdf, ctx->d_hist, nblk, st));
+  }
   CU(cudaEventRecord(ev[1], st));
-  CU(launch_scan(ctx->d_hist, nblk, ctx->cfg.L, tmlp_tile_rows(ctx->cfg.H, ctx->cfg.prec, ctx->use_pair), ctx->d_offs,
-                 ctx->d_meta, ctx->d_scan, st));
-  CU(launch_scatter(d_depth, n, ctx->cfg.L, ctx->d_offs, ctx->d_perm, nblk, st));
+  {
+    NvtxRange r("K2 binning (scan + scatter)");
+    CU(launch_scan(ctx->d_hist, nblk, ctx->cfg.L, tmlp_tile_rows(ctx->cfg.H, ctx->cfg.prec, ctx->use_pair), ctx->d_offs,
+                   ctx->d_meta, ctx->d_scan, st));
+    CU(launch_scatter(d_depth, n, ctx->cfg.L, ctx->d_offs, ctx->d_perm, nblk, st));
+  }
   CU(cudaEventRecord(ev[2], st));
+  NvtxRange r3("K3 T-MLP");
   if (ctx->cfg.prec == SAND_F16X3)
     CU(launch_tmlp_x3(ctx->mlp, d_points, ctx->d_perm, ctx->d_meta, d_sdf, ctx->num_sms, st));
   else if (ctx->cfg.prec == SAND_FP32 && !simt_supported_H(ctx->cfg.H))
@@ -631,6 +646,7 @@ static int ensure_hostpipe(sand_ctx* ctx, long long chunk) {
 
 extern "C" int sand_query_host(sand_ctx* ctx, const float* h_points, int64_t n, float* h_sdf, uint8_t* h_depth,
                                int64_t chunk_points) {
+  NvtxRange nvtx_("sand_query_host (pipelined H2D / query / D2H)");
   if (!ctx) return fail(ctx, SAND_ERR_ARG, "NULL ctx");
   if (n < 0 || chunk_points < 0) return fail(ctx, SAND_ERR_ARG, "negative size");
   if (!ctx->have_w || !ctx->have_dm) return fail(ctx, SAND_ERR_STATE, "load weights and depth map first");
@@ -770,6 +786,7 @@ extern "C" int sand_marching_cubes(sand_ctx* ctx, const float* d_sdf, int R, flo
 }
 
 extern "C" int sand_mesh_grid(sand_ctx* ctx, int R, int slab, float* d_tris, int64_t cap, int64_t* n_tris) {
+  NvtxRange nvtx_("sand_mesh_grid");
   if (!ctx) return fail(ctx, SAND_ERR_ARG, "NULL ctx");
   if (R < 2 || slab < 0 || cap < 0 || !n_tris || (cap > 0 && !d_tris))
     return fail(ctx, SAND_ERR_ARG, "sand_mesh_grid: R < 2, slab < 0, cap < 0 or NULL argument");
@@ -809,6 +826,7 @@ extern "C" int sand_mesh_grid(sand_ctx* ctx, int R, int slab, float* d_tris, int
 // ------------------------------------------------------------------------------- depth-map population
 extern "C" int sand_required_depth(sand_ctx* ctx, const float* d_points, int64_t n, float r, int near,
                                    uint8_t* d_out_depth) {
+  NvtxRange nvtx_("sand_required_depth (Eq. 5)");
   if (!ctx) return fail(ctx, SAND_ERR_ARG, "NULL ctx");
   if (n < 0 || !(r >= 0.0f)) return fail(ctx, SAND_ERR_ARG, "sand_required_depth: n < 0 or r < 0");
   if (!ctx->have_w) return fail(ctx, SAND_ERR_STATE, "load weights before sand_required_depth");
@@ -826,6 +844,7 @@ extern "C" int sand_required_depth(sand_ctx* ctx, const float* d_points, int64_t
 
 extern "C" int sand_query_dynamic(sand_ctx* ctx, const float* d_points, int64_t n, float r, float* d_out_sdf,
                                   uint8_t* d_out_exit_depth) {
+  NvtxRange nvtx_("sand_query_dynamic");
   if (!ctx) return fail(ctx, SAND_ERR_ARG, "NULL ctx");
   if (n < 0 || !(r >= 0.0f)) return fail(ctx, SAND_ERR_ARG, "sand_query_dynamic: n < 0 or r < 0");
   if (!ctx->have_w) return fail(ctx, SAND_ERR_STATE, "load weights before sand_query_dynamic");
@@ -850,6 +869,7 @@ extern "C" int sand_query_dynamic(sand_ctx* ctx, const float* d_points, int64_t 
 
 extern "C" int sand_populate_leaf_depths(sand_ctx* ctx, const float* d_samples, int64_t n_leaves,
                                          int samples_per_leaf, float r, uint8_t* d_leaf_depth) {
+  NvtxRange nvtx_("sand_populate_leaf_depths (Eq. 5/6)");
   if (!ctx) return fail(ctx, SAND_ERR_ARG, "NULL ctx");
   if (n_leaves < 0 || samples_per_leaf < 1 || !(r >= 0.0f))
     return fail(ctx, SAND_ERR_ARG, "sand_populate_leaf_depths: bad size or r");

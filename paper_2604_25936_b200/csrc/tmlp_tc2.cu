@@ -86,6 +86,12 @@ static_assert(!SAND_SMR || 4 * (SAND_SMR_EPI - 96) <= 96 - SAND_SMR_CTL, "setmax
 #ifndef SAND_EPI_BARWAIT
 #define SAND_EPI_BARWAIT 1   // accumulator waits: one polling warp per column group + a named barrier
 #endif
+#ifndef SAND_EARLY_LO
+#define SAND_EARLY_LO 0   // 1: publish the first K-half of the next A as soon as it is stored (pass-1 start)
+#endif
+#ifndef SAND_DEFER_PUB
+#define SAND_DEFER_PUB 0   // 1: publish a step's A after the first batch of the other slot's next step; 2: after its pass 0
+#endif
 #ifndef SAND_PDEG
 #define SAND_PDEG 7
 #endif
@@ -252,13 +258,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
   const uint32_t b_wfull = smem_u32(bars);
   const uint32_t b_wempty = b_wfull + 8 * nst;
   const uint32_t b_wpeer = b_wempty + 8 * nst;
-  const uint32_t b_afull = b_wpeer + 8 * nst;           // [slot]  epilogue step done (A written / acc read)
-  const uint32_t b_accfull = b_afull + 8 * NSLOT;       // [slot][pass]  accumulator half ready
+  const uint32_t b_afull = b_wpeer + 8 * nst;           // [slot][K-half] epilogue step: A K-chunks [0, KC/2) written +
+                                                        // accumulator pass 0 read (lo); all A written + all read (hi)
+  const uint32_t b_accfull = b_afull + 16 * NSLOT;      // [slot][pass]  accumulator half ready
   const uint32_t b_a1full = b_accfull + 16 * NSLOT;     // [slot]  layer-1 A written (leader: 2 arrivals)
   const uint32_t b_a1free = b_a1full + 8 * NSLOT;       // [slot]  layer-1 MMA done with the A1 buffer
   const uint32_t b_iodone = b_a1free + 8 * NSLOT;       // [slot]  all epilogue warps wrote their partials
   const uint32_t b_partfree = b_iodone + 8 * NSLOT;     // [slot]  IO warp has read the partials
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * nst + 8 * NSLOT);   // (3 nst + 8 NSLOT) barriers
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * nst + 9 * NSLOT);   // (3 nst + 9 NSLOT) barriers
 #ifdef SAND_HANG_DEBUG
   if (blockIdx.x == 0 && threadIdx.x == 0)
     printf("[bars] wfull 0x%x wempty 0x%x wpeer 0x%x afull 0x%x accfull 0x%x a1full 0x%x a1free 0x%x iodone 0x%x\n",
@@ -299,7 +306,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
     }
     // a_full: one arrive per epilogue warp of both CTAs
     for (int s = 0; s < NSLOT; ++s) {
-      mbar_init(b_afull + 8 * s, 2 * kEpiWarps);
+      mbar_init(b_afull + 16 * s, 2 * kEpiWarps);
+      mbar_init(b_afull + 16 * s + 8, 2 * kEpiWarps);
       mbar_init(b_accfull + 16 * s, 1);
       mbar_init(b_accfull + 16 * s + 8, 1);
     }
@@ -333,7 +341,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
       const uint8_t* img = reinterpret_cast<const uint8_t*>(p.m.w_image_pair) + (size_t)rank * 2 * C::STAGE;
       const uint32_t peer_wpeer = mapa_shared(b_wpeer, 0);
       constexpr uint32_t ID = idesc_bf16(256, C::HN);
-      uint32_t pa0 = 0, pa1 = 0;
+      uint32_t pa[2][2] = {{0, 0}, {0, 0}};   // [slot][lo, hi] a_full parities
       int st = 0;
       uint32_t ph = 0;
       unsigned long long pc[6] = {0, 0, 0, 0, 0, 0};
@@ -341,14 +349,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
       // a_full[s] completes once per epilogue step of slot s (all epilogue warps of both CTAs arrived:
       // A written for the next layer and accumulator read).  Every MMA job but the first of a slot waits
       // for the previous step of its slot, so the accumulator is never overwritten while read.
-      auto wait_prev_step = [&](const SlotWalk& w, int s) {
+      auto wait_prev_half = [&](const SlotWalk& w, int s, int hi) {
         if (w.ti == 0 && w.l == 1) return;
-        uint32_t& pa = s ? pa1 : pa0;
         const long long c0_ = (SAND_DIAG && p.prof) ? clock64() : 0;
-        mbar_wait_cluster(b_afull + 8 * s, pa);
-        if (SAND_DIAG && p.prof) { pc[0] += clock64() - c0_; pc[3] += 1; }
-        pa ^= 1u;
+        mbar_wait_cluster(b_afull + 16 * s + 8 * hi, pa[s][hi]);
+        if (SAND_DIAG && p.prof) { pc[0] += clock64() - c0_; pc[3] += hi; }
+        pa[s][hi] ^= 1u;
       };
+      auto wait_prev_step = [&](const SlotWalk& w, int s) { wait_prev_half(w, s, 0); wait_prev_half(w, s, 1); };
       auto job = [&](const SlotWalk& w, int s) {
         const int l = w.l;
         const int nsj = l == 1 ? 0 : 2;   // ring stages of this job (one per pass)
@@ -362,7 +370,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
             if (++st == nst) { st = 0; ph ^= 1u; }
           }
         } else if (rank == 0) {
-          wait_prev_step(w, s);
+          const bool early = SAND_EARLY_LO && l >= 2 && C::KC >= 2;
+          if (early) wait_prev_half(w, s, 0);   // K-chunks [0, KC/2) of A and the pass-0 accumulator are free
+          else wait_prev_step(w, s);
           const uint32_t acc = tmem_base + (uint32_t)(s * H);
           if (l == 1) {
             // ---- layer 1: per pass one K = 16 MMA on the split-BF16 operands (A written by the IO warps)
@@ -399,8 +409,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
             mma_bf16_cg2_w(d, ones_d, desc_nosw(slot, 128, 256), ID, 0u);
             const uint64_t w_d = desc_sw128(slot + C::QSMALL);
 #pragma unroll 1
-            for (int kc = 0; kc < C::KC; ++kc)
+            for (int kc = 0; kc < C::KC; ++kc) {
+              if (early && j == 0 && kc == C::KC / 2) { wait_prev_half(w, s, 1); tc_fence_after(); }
               mma4_bf16_cg2_w(d, a_d + (uint64_t)(kc * (C::A_CHUNK >> 4)), w_d + (uint64_t)(kc * (C::QCHUNK >> 4)), ID, 1u);
+            }
             mma_commit_cg2_mc_w(b_wempty + 8 * st, 0x3);
             mma_commit_cg2_mc_w(b_accfull + 16 * s + 8 * j, 0x3);
             if (++st == nst) { st = 0; ph ^= 1u; }
@@ -569,14 +581,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
     const uint32_t afull_dst0 = rank == 0 ? b_afull : mapa_shared(b_afull, 0);
     unsigned long long ep_wait = 0, ep_busy = 0, ep_steps = 0, ep_pub = 0, ep_tend = 0;
 
-    auto publish = [&](int s, bool wrote_a) {
+    auto publish_half = [&](int s, bool wrote_a, int hi) {
       if (wrote_a) fence_proxy_async_smem();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        if (rank == 0) mbar_arrive(afull_dst0 + 8 * s);
-        else mbar_arrive_remote(afull_dst0 + 8 * s);
+        if (rank == 0) mbar_arrive(afull_dst0 + 16 * s + 8 * hi);
+        else mbar_arrive_remote(afull_dst0 + 16 * s + 8 * hi);
       }
+    };
+    // the lo half is published early (SAND_EARLY_LO, at the start of pass 1) or together with the hi half
+    auto publish = [&](int s, bool wrote_a) {
+      if (!SAND_EARLY_LO) publish_half(s, wrote_a, 0);
+      publish_half(s, wrote_a, 1);
     };
     auto quad_sum = [](float v) {
       v += __shfl_xor_sync(0xffffffffu, v, 1);
@@ -585,7 +602,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
     };
 
     // one epilogue step (layer l of the current tile) of slot s
-    auto step = [&](EpiSlot& e, const int s) {
+    int pend = -1;          // slot whose publish is deferred into the other slot's step (SAND_DEFER_PUB)
+    bool pend_store = false;
+    auto flush_pend = [&]() {
+      if (pend >= 0) { publish(pend, pend_store); pend = -1; }
+    };
+    auto step = [&](EpiSlot& e, const int s, const bool defer_ok) {
       const int d = e.w.d, l = e.w.l;
       const uint32_t aSt = a_st + s * C::A_BYTES;
       float2 yv[4], yv1[4];
@@ -661,6 +683,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
 #pragma unroll
           for (int i = 0; i < NCHP; ++i) st_chunk(8 * i, stash[i]);
         }
+        // K-chunks [0, KC/2) of the next A (pass-0 columns) are in place and the pass-0 accumulator has been
+        // read: the next layer's MMA may start on them
+        if (SAND_EARLY_LO && decltype(pass_c)::value == 1) publish_half(s, ST && (SAND_SPLIT_STORE || store), 0);
 #pragma unroll
         for (int bb = 0; bb < NCHP / CB; ++bb) {
           uint32_t r0[4 * CB], r1[4 * CB];   // lane block 0 (rows R0, R1) and block 1 (rows R2, R3)
@@ -673,6 +698,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
           tmem_wait_ld_dep(r0);
           tmem_wait_ld_dep(r1);
 #endif
+          if (SAND_DEFER_PUB == 1 && decltype(pass_c)::value == 0 && bb == 0) flush_pend();
 #pragma unroll
           for (int i = 0; i < CB; ++i) {
             uint32_t pk[4];
@@ -691,12 +717,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
       using P0 = std::integral_constant<int, 0>;
       using P1 = std::integral_constant<int, 1>;
       if (!(SAND_DIAG && p.prof >= 2)) {   // diagnostic 2/3 (SAND_DIAG builds): no epilogue math
-        if (SAND_SPLIT_STORE && store) { math(std::true_type{}, P0{}); math(std::true_type{}, P1{}); }
-        else { math(std::false_type{}, P0{}); math(std::false_type{}, P1{}); }
+        if (SAND_SPLIT_STORE && store) {
+          math(std::true_type{}, P0{});
+          if (SAND_DEFER_PUB == 2) flush_pend();
+          math(std::true_type{}, P1{});
+        } else {
+          math(std::false_type{}, P0{});
+          if (SAND_DEFER_PUB == 2) flush_pend();
+          math(std::false_type{}, P1{});
+        }
       } else {
         mbar_wait(b_accfull + 16 * s, e.pe);
         mbar_wait(b_accfull + 16 * s + 8, e.pe);
         tc_fence_after();
+        if (SAND_EARLY_LO) publish_half(s, false, 0);
       }
       e.pe ^= 1u;
       if (prod) {
@@ -722,7 +756,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
         for (int k = 0; k < 4; ++k) e.ylin[k] += yv[k].x + yv[k].y;
       }
       const long long cp_ = (SAND_DIAG && p.prof) ? clock64() : 0;
-      publish(s, store);
+      flush_pend();   // (already done inside math when deferral is on; a no-op then)
+      if (SAND_DEFER_PUB && defer_ok) { pend = s; pend_store = store; }
+      else publish(s, store);
       if (SAND_DIAG && p.prof) ep_pub += clock64() - cp_;
       const long long ct_ = (SAND_DIAG && p.prof) ? clock64() : 0;
       if (l == d) {
@@ -757,9 +793,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
     const long long t_start = (SAND_DIAG && p.prof) ? clock64() : 0;
 #pragma unroll 1
     while (!(e0.w.done && e1.w.done)) {
-      if (!e0.w.done) step(e0, 0);
-      if (!e1.w.done) step(e1, 1);
+      // a step may defer its publish into the other slot's next step only if that step exists
+      if (!e0.w.done) step(e0, 0, !e1.w.done);
+      if (!e1.w.done) {
+        bool nxt0 = !e0.w.done;
+        step(e1, 1, nxt0);
+      }
     }
+    flush_pend();
     if (SAND_DIAG && p.prof && warp == 3 && lane == 0) {
       g_kprof[blockIdx.x][6] = ep_wait;
       g_kprof[blockIdx.x][7] = ep_busy;
@@ -784,7 +825,7 @@ static size_t smem_for2(long long pt_floats, int L, int tail, int nst) {
   const size_t io_bytes = (size_t)C::NSLOT * (tail == SAND_TAIL_MULT ? C::NGRP + 1 : C::NGRP) * 128 * 4;
   const size_t red_bytes = tail == SAND_TAIL_MULT ? (size_t)C::NSLOT * 2 * C::NGRP * 128 * 8 : 0;
   return (size_t)C::NSLOT * C::A_BYTES + (size_t)nst * C::STAGE + C::ONES_BYTES + C::W1_BYTES + (size_t)C::NSLOT * C::A1_BYTES +
-         tab_bytes + io_bytes + red_bytes + 4 * (size_t)(L + 2) * sizeof(long long) + (3 * nst + 8 * C::NSLOT) * 8 +
+         tab_bytes + io_bytes + red_bytes + 4 * (size_t)(L + 2) * sizeof(long long) + (3 * nst + 9 * C::NSLOT) * 8 +
          16;
 }
 
