@@ -44,8 +44,8 @@ typedef enum {
 } sand_status;
 
 /* Arithmetic of the H x H layers.
- *   SAND_FP32  : FP32 SIMT kernels (FFMA; sine to ~5e-7: libm sinf for H <= 64, Cody-Waite reduction +
- *                MUFU.SIN for wider nets); supported H in {16, 32, 64} (one thread per
+ *   SAND_FP32  : FP32 SIMT kernels (FFMA; sine to ~5e-7: Cody-Waite reduction to [-pi, pi] +
+ *                MUFU.SIN); supported H in {16, 32, 64} (one thread per
  *                point) and {128, 256, 336} (register-blocked GEMM over 64-point sub-tiles, L <= 32).
  *                Tolerance vs the oracle: 1e-4 max-abs (BASELINE.json north_star).
  *   SAND_BF16  : tcgen05 tensor cores, BF16 operands, FP32 accumulate in TMEM; layer 1 (K = 3) as a

@@ -3,8 +3,10 @@
 // Evaluates Eq. 2 with Eq. 3 tails for binned tiles of 128 points of
 // one uniform exit depth d: h_1 = sin(w0 (W_1 x + b_1)), h_i = sin(w0 (W_i h_{i-1} + b_i)),
 // y_d = sum_{i<=d} t_i.  One thread = one point; the hidden vector lives in registers (H <= 64); the
-// hidden weights live in shared memory and are read as warp-uniform broadcasts.  Accurate sinf keeps
-// the result within the 1e-4 FP32 tolerance of the north star.  Small-H configs (C0 is 4 x 64) are
+// hidden weights live in shared memory and are read as warp-uniform broadcasts.  The sine is a
+// two-constant Cody-Waite reduction to [-pi, pi] followed by MUFU.SIN (~4e-7 absolute, FP32-grade for a
+// SIREN layer's |z| <~ 100; libm sinf cost ~5x the instructions: C0 0.265 ms before), well inside the
+// north star's 1e-4 FP32 tolerance.  Small-H configs (C0 is 4 x 64) are
 // FMA/launch bound, not tensor bound: at H = 64 an H x H layer is 4096 FMAs per point.
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -12,6 +14,13 @@
 #include "sand_internal.h"
 
 namespace sand {
+
+__device__ __forceinline__ float simt_sin(float x) {
+  const float k = rintf(x * 0.159154943091895f);
+  float r = fmaf(-k, 6.28318548202514648f, x);
+  r = fmaf(-k, -1.7484555314695172e-7f, r);
+  return __sinf(r);
+}
 
 template <int H, int TAIL>
 __global__ void __launch_bounds__(kTileM) k_tmlp_simt(MlpDev m, const float* __restrict__ pts,
@@ -51,7 +60,7 @@ __global__ void __launch_bounds__(kTileM) k_tmlp_simt(MlpDev m, const float* __r
 #pragma unroll
       for (int j = 0; j < H; ++j) {
         const float4 w = w1[j];
-        h[j] = sinf(fmaf(w.z, pz, fmaf(w.y, py, fmaf(w.x, px, w.w))));
+        h[j] = simt_sin(fmaf(w.z, pz, fmaf(w.y, py, fmaf(w.x, px, w.w))));
         y = fmaf(a[j], h[j], y);
       }
     }
@@ -72,7 +81,7 @@ __global__ void __launch_bounds__(kTileM) k_tmlp_simt(MlpDev m, const float* __r
           z = fmaf(w.z, h[4 * k + 2], z);
           z = fmaf(w.w, h[4 * k + 3], z);
         }
-        hn[j] = sinf(fmaf(z, w0, bias[j]));
+        hn[j] = simt_sin(fmaf(z, w0, bias[j]));
       }
       float s0 = st[m.off_c + (l - 1)], s1 = 0.0f;
       if (TAIL == SAND_TAIL_MULT) s1 = st[m.off_c1 + (l - 2)];
