@@ -455,8 +455,10 @@ def run_dynamic(args):
                 cx.sand_set_stream(st.cuda_stream)
                 ms_p = timed(lambda: cx.sand_query(pts.data_ptr(), n, sdf.data_ptr(), dep.data_ptr()), steps)
                 oct_same[pname] = {"value": n / (ms_p / 1e3), "unit": UNIT, "ms_per_step": ms_p}
-        for mode in ("tile", "pool"):   # tile-level early exit / pools re-compacted after every layer
-            ctx.sand_set_option(SAND_OPT_DYN_SCHEDULE, 1 if mode == "pool" else 0)
+        # tile-level early exit / pools re-compacted after every layer (FP32 SIMT) / every layer on the split-FP16
+        # tensor kernel with the exit selected afterwards
+        for mode in ("tile", "pool", "tensor"):
+            ctx.sand_set_option(SAND_OPT_DYN_SCHEDULE, {"tile": 0, "pool": 1, "tensor": 2}[mode])
             for name, r in (("paper r = 1.5e-4", 1.5e-4), (f"r = 30% quantile of |t_i| ({r30:.3e})", r30)):
                 ms = timed(lambda: ctx.sand_query_dynamic(pts.data_ptr(), n, r, sdf.data_ptr(), dep.data_ptr()), steps)
                 hist = np.bincount(dep.cpu().numpy(), minlength=c.spec.L + 1)[:c.spec.L + 1].tolist()
@@ -482,10 +484,11 @@ def run_dynamic(args):
             "octree_path": {"value": n / (ms_oct / 1e3), "unit": UNIT, "ms_per_step": ms_oct,
                             "dtype": "bf16", "note": "sand_query with C2's level-7 octree, same points"},
             "octree_path_fp32": oct_same,
-            "method_gap": {e["threshold"] + " / " + e["mode"]: e["ms_per_step"] / oct_same["fp32_simt"]["ms_per_step"]
-                           for e in entries},
-            "method_gap_note": "dynamic-exit time / octree-path time, both FP32 SIMT (the paper: 13.67 s / 0.378 s = 36x, "
-                               "P:761-762, on its trained nets where most of the grid is far field)",
+            "method_gap": {e["threshold"] + " / " + e["mode"]: e["ms_per_step"] / oct_same[
+                "f16x3_tensor" if e["mode"] == "tensor" else "fp32_simt"]["ms_per_step"] for e in entries},
+            "method_gap_note": "dynamic-exit time / octree-path time in the same arithmetic (SIMT schedules vs the FP32 "
+                               "SIMT octree path, the tensor schedule vs the F16X3 octree path); the paper: 13.67 s / "
+                               "0.378 s = 36x, P:761-762, on its trained nets where most of the grid is far field",
             "entries": entries, "cpu_baseline": cpu}
     print(json.dumps(line), flush=True)
     return 0

@@ -125,7 +125,10 @@ int sand_set_stream(sand_ctx* ctx, void* cuda_stream);
  *                         configuration fits them, 0 = the 1-CTA kernel.  1 on a configuration without a
  *                         pair kernel -> SAND_ERR_UNSUPPORTED.
  *   SAND_OPT_DYN_SCHEDULE [0] sand_query_dynamic: 0 = a 64-point tile stops when all its points have
- *                         stopped; 1 = pools of 512 points re-compacted after every layer.
+ *                         stopped; 1 = pools of 512 points re-compacted after every layer (both FP32 SIMT);
+ *                         2 = every layer on the split-FP16 tensor-core kernel (SAND_F16X3 arithmetic),
+ *                         the exit layer selected per point afterwards (H in {64, 128, 256}, else
+ *                         SAND_ERR_UNSUPPORTED at the call).
  *   SAND_OPT_KPROF        [0] diagnostic, -DSAND_DIAG=1 builds only (ignored otherwise): 1 = per-role
  *                         clock64 wait / busy counters of the CTA-pair kernels printed to stderr after every
  *                         launch (adds a stream synchronisation); 2, 3 = timing-only modes that skip epilogue
@@ -215,9 +218,9 @@ int sand_populate_leaf_depths(sand_ctx* ctx, const float* d_samples, int64_t n_l
  * layer i >= 2 whose residual |t_i| < r (reading R23: t_1 = y_1 is the first prediction, not
  * a residual), else at L:
  *   d_out_exit_depth[p] = that layer (255 for a non-finite point),  d_out_sdf[p] = y_d (NaN if 255).
- * FP32 (sine to ~5e-7) like the population calls above.  Schedule: SAND_OPT_DYN_SCHEDULE (a 64-point
- * tile stops as soon as all of its points have stopped, or pools of 512 points are re-compacted after
- * every layer).  Only the weights must be loaded; the depth map
+ * FP32 accuracy (sine to ~5e-7) like the population calls above.  Schedule: SAND_OPT_DYN_SCHEDULE (a 64-point
+ * tile stops as soon as all of its points have stopped; pools of 512 points re-compacted after every
+ * layer; or all layers on the tensor cores with the exit selected afterwards).  Only the weights must be loaded; the depth map
  * and LOD cap are ignored.  Asynchronous on ctx's stream.  Errors: SAND_ERR_ARG (n < 0, r < 0 or NaN,
  * NULL buffer), SAND_ERR_STATE, SAND_ERR_UNSUPPORTED (H as above), SAND_ERR_CUDA. */
 int sand_query_dynamic(sand_ctx* ctx, const float* d_points, int64_t n, float r, float* d_out_sdf,

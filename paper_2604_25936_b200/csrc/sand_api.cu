@@ -516,7 +516,7 @@ extern "C" int sand_set_option(sand_ctx* ctx, int option, int64_t value) {
       ctx->use_pair = value == 1;
       return SAND_OK;
     case SAND_OPT_DYN_SCHEDULE:
-      if (value != 0 && value != 1) return fail(ctx, SAND_ERR_ARG, "SAND_OPT_DYN_SCHEDULE takes 0 or 1");
+      if (value < 0 || value > 2) return fail(ctx, SAND_ERR_ARG, "SAND_OPT_DYN_SCHEDULE takes 0, 1 or 2");
       ctx->dyn_schedule = (int)value;
       return SAND_OK;
     case SAND_OPT_FP32_TENSOR:
@@ -852,8 +852,14 @@ extern "C" int sand_query_dynamic(sand_ctx* ctx, const float* d_points, int64_t 
   if (!d_points || !d_out_sdf || !d_out_exit_depth) return fail(ctx, SAND_ERR_ARG, "NULL buffer");
   if (!depthpop_supported(ctx->cfg.H)) return fail(ctx, SAND_ERR_UNSUPPORTED, "H = %d", ctx->cfg.H);
   CU(cudaSetDevice(ctx->cfg.device));
-  // default: tile-level early exit (measured faster on the synthetic workloads);
-  // SAND_OPT_DYN_SCHEDULE = 1: pools re-compacted after every layer
+  // SAND_OPT_DYN_SCHEDULE: 0 = tile-level early exit, 1 = pools re-compacted after every layer (FP32 SIMT),
+  // 2 = full-depth split-FP16 tensor evaluation with the exit layer selected per point (H in {64, 128, 256})
+  if (ctx->dyn_schedule == 2) {
+    if (!(ctx->have_x3 && x3_usable(ctx->cfg.L, ctx->cfg.H, ctx->cfg.tail, 2)))
+      return fail(ctx, SAND_ERR_UNSUPPORTED, "SAND_OPT_DYN_SCHEDULE = 2 needs H in {64, 128, 256}");
+    CU(launch_query_dynamic_x3(ctx->mlp, d_points, n, r, d_out_sdf, d_out_exit_depth, ctx->num_sms, ctx->stream));
+    return SAND_OK;
+  }
   const bool pool = ctx->dyn_schedule == 1;
   float* hbuf = nullptr;
   if (pool) {

@@ -150,5 +150,7 @@ cudaError_t launch_tmlp_x3(const MlpDev& m, const float* pts, const uint32_t* pe
                            int num_sms, cudaStream_t st);
 cudaError_t launch_required_depth_x3(const MlpDev& m, const float* pts, long long n, float r, int near, uint8_t* out,
                                      int num_sms, cudaStream_t st);
+cudaError_t launch_query_dynamic_x3(const MlpDev& m, const float* pts, long long n, float r, float* out_sdf,
+                                    uint8_t* out_depth, int num_sms, cudaStream_t st);
 
 }  // namespace sand

@@ -10,10 +10,13 @@
 // FP16 keeps the split operands at 2 bytes (TF32 operands would need 4), so A_hi + A_lo of a 256-row tile
 // fit in shared memory like the BF16 kernel's two tile slots.  One tile is in flight per CTA pair.
 //
-// Two modes on the same machinery:
-//   query (Sec. 3.4): binned 256-row tiles of uniform exit depth d, y_d -> sdf[perm[row]];
-//   population (Eq. 5): 256 consecutive samples per tile, all L layers, every y_i kept, and the
-//     required depth d(x) = min{ i : sign(y_i) = sign(y_L) [and |y_L - y_i| < r] } -> depth[sample].
+// Three modes on the same machinery:
+//   query (POP = 0; Sec. 3.4): binned 256-row tiles of uniform exit depth d, y_d -> sdf[perm[row]];
+//   population (POP = 1; Eq. 5): 256 consecutive samples per tile, all L layers, every y_i kept, and
+//     the required depth d(x) = min{ i : sign(y_i) = sign(y_L) [and |y_L - y_i| < r] } -> depth[sample];
+//   dynamic exit (POP = 2; "SAND w/o Octree", R23): as population, every t_i kept, and
+//     the exit layer d = min{ i >= 2 : |t_i| < r } (else L), y_d -> sdf, d -> depth (255 / NaN for
+//     non-finite points).  All L layers are evaluated (no tile-level early stop), the selection is exact.
 //
 // Warp roles per CTA ("leader" = even CTA):
 //   warp 0   producer (lane 0): this CTA's half of a hidden layer's operands through an NST-stage ring:
@@ -121,7 +124,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(X3Shape<H>::THREADS,
   constexpr int NPL = TAIL == SAND_TAIL_MULT ? 8 : 4;             // partial planes per layer
   float* part = tab + ((ntab + 3) & ~3ll);                        // [2 parities][NPL][128]
   float* ybuf = part + 2 * NPL * 128;                             // population: [L][128] cumulative y_i
-  const int ybuf_floats = POP ? L * 128 : 0;
+  const int ybuf_floats = POP == 2 ? 2 * L * 128 : POP ? L * 128 : 0;   // y_i (and t_i for POP = 2)
   const int nb = L + 2;
   long long* meta_s = reinterpret_cast<long long*>(ybuf + ybuf_floats);
   long long* s_tile_end = meta_s;
@@ -338,12 +341,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(X3Shape<H>::THREADS,
         }
         y[k] += t;
         if (POP) ybuf[(l - 1) * 128 + rr] = y[k];
+        if (POP == 2) ybuf[(L + l - 1) * 128 + rr] = t;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(b_pfree + 8 * par);
       par ^= 1u;
       if (l == w.d) {
-        if (POP) {
+        if (POP == 2) {
+          // R23: exit at the first layer i >= 2 whose residual |t_i| < r, else at L
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if (cur[k] == 0xFFFFFFFFu) continue;
+            const int rr = lane + 32 * k;
+            const size_t gi = cur[k];
+            const bool fin = isfinite(__ldg(p.pts + 3 * gi)) && isfinite(__ldg(p.pts + 3 * gi + 1)) &&
+                             isfinite(__ldg(p.pts + 3 * gi + 2));
+            int dd = L;
+            for (int i = 2; i < L; ++i)
+              if (fabsf(ybuf[(L + i - 1) * 128 + rr]) < p.r) { dd = i; break; }
+            p.out_sdf[gi] = fin ? ybuf[(dd - 1) * 128 + rr] : __int_as_float(0x7fc00000);
+            p.out_depth[gi] = fin ? (uint8_t)dd : (uint8_t)SAND_DEPTH_NONFINITE;
+          }
+        } else if (POP) {
           // Eq. 5: d(x) = min{ i : sign(y_i) = sign(y_L) [and |y_L - y_i| < r] }; i = L always qualifies
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
@@ -511,7 +530,7 @@ static size_t smem_x3(long long tab_floats, int L, int tail, int pop, int nst) {
   using C = X3Shape<H>;
   const size_t npl = tail == SAND_TAIL_MULT ? 8 : 4;
   return 2 * (size_t)C::A_BYTES + (size_t)nst * C::STAGE + C::ONES_BYTES + 2 * (size_t)C::XB +
-         (size_t)((tab_floats + 3) & ~3ll) * 4 + 2 * npl * 128 * 4 + (pop ? (size_t)L * 128 * 4 : 0) +
+         (size_t)((tab_floats + 3) & ~3ll) * 4 + 2 * npl * 128 * 4 + (size_t)(pop == 2 ? 2 : pop ? 1 : 0) * L * 128 * 4 +
          4 * (size_t)(L + 2) * 8 + (3 * (size_t)nst + 10) * 8 + 16;
 }
 
@@ -673,6 +692,13 @@ cudaError_t launch_required_depth_x3(const MlpDev& m, const float* pts, long lon
   X3Params p{};
   p.m = m; p.pts = pts; p.n = n; p.r = r; p.near = near; p.out_depth = out;
   return launch_x3_any<1>(p, num_sms, st);
+}
+
+cudaError_t launch_query_dynamic_x3(const MlpDev& m, const float* pts, long long n, float r, float* out_sdf,
+                                    uint8_t* out_depth, int num_sms, cudaStream_t st) {
+  X3Params p{};
+  p.m = m; p.pts = pts; p.n = n; p.r = r; p.out_sdf = out_sdf; p.out_depth = out_depth;
+  return launch_x3_any<2>(p, num_sms, st);
 }
 
 }  // namespace sand

@@ -52,9 +52,11 @@ def _check(p, pts, r, sdf, dep):
     return same.mean(), np.bincount(d, minlength=L + 1)
 
 
-@pytest.mark.parametrize("pool", [0, 1])
-@pytest.mark.parametrize("H,L,tail", [(64, 6, 0), (256, 8, 0), (128, 5, 1), (336, 8, 0), (32, 1, 0)])
+@pytest.mark.parametrize("pool", [0, 1, 2])
+@pytest.mark.parametrize("H,L,tail", [(64, 6, 0), (256, 8, 0), (128, 5, 1), (336, 8, 0), (32, 1, 0), (64, 1, 0)])
 def test_dynamic_exit_matches_oracle(H, L, tail, pool):
+    """Schedules 0 / 1: FP32 SIMT tile exit / re-compaction; 2: all layers on the split-FP16 tensor kernel with
+    the exit selected afterwards (H in {64, 128, 256}; other widths must be refused)."""
     spec = g.TMlpSpec(L=L, H=H, omega0=30.0, tail=tail, seed=21 + H)
     p = g.make_weights(spec)
     pts = np.random.default_rng(H).uniform(-1, 1, (5003, 3)).astype(np.float32)
@@ -66,15 +68,21 @@ def test_dynamic_exit_matches_oracle(H, L, tail, pool):
     else:
         r = 1.0
     with make_ctx(spec, BF16 if H >= 64 else FP32) as ctx:   # the dynamic path is FP32 in either context
-        ctx.sand_set_option(SAND_OPT_DYN_SCHEDULE, pool)   # tile-level exit / per-layer re-compaction
+        ctx.sand_set_option(SAND_OPT_DYN_SCHEDULE, pool)   # tile-level exit / re-compaction / tensor select
         ctx.sand_load_weights(g.pack_blob(p))
+        if pool == 2 and H not in (64, 128, 256):
+            from paper_2604_25936_b200 import SandError
+            with pytest.raises(SandError) as e:
+                _run(ctx, pts, r)
+            assert e.value.code == -7
+            return
         sdf, dep = _run(ctx, pts, r)
     frac, hist = _check(p, pts, r, sdf, dep)
     if L > 2:
         assert hist[2] > 0 and hist[L] > 0, hist   # some points stop early, some run to L
 
 
-@pytest.mark.parametrize("pool", [0, 1])
+@pytest.mark.parametrize("pool", [0, 1, 2])
 def test_dynamic_special_cases_and_sizes(pool):
     """r = 0 -> full depth (= query_full); huge r -> everyone stops at layer 2; n in {0, 1, 65} and a
     ragged last tile."""
