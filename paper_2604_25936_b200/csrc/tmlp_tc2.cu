@@ -460,13 +460,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
         ix[k] = r < rend ? __ldg(p.perm + r) : 0xFFFFFFFFu;
       }
     };
-    auto fill = [&](int s, const uint32_t (&ix)[4]) {
-      float x[4], y[4], z[4];
+    // point gather of a tile's rows (issued a slot-step before the layer-1 operand is built from them, so the
+    // DRAM latency of the 12-byte gathers is off the layer-1 critical path)
+    auto gather = [&](const uint32_t (&ix)[4], float (&x)[4], float (&y)[4], float (&z)[4]) {
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const size_t i = ix[k] == 0xFFFFFFFFu ? 0 : ix[k];
         x[k] = __ldg(p.pts + 3 * i); y[k] = __ldg(p.pts + 3 * i + 1); z[k] = __ldg(p.pts + 3 * i + 2);
       }
+    };
+    auto fill = [&](int s, const float (&x)[4], const float (&y)[4], const float (&z)[4]) {
       const uint32_t a1 = sA1 + s * C::A1_BYTES;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -495,7 +498,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
         else mbar_arrive_remote(a1full_dst + 8 * s);
       }
     };
-    struct IoSlot { uint32_t cur[4], nxt[4], pre[4]; };
+    struct IoSlot { uint32_t cur[4], nxt[4], pre[4]; float nx[4], ny[4], nz[4]; };
     SlotWalk w0, w1;
     w0.start(pair, T, s_tile_end, L);
     w1.start(pair + npairs, T, s_tile_end, L);
@@ -506,8 +509,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
       const long long t0 = pair + (long long)npairs * s;
 #pragma unroll
       for (int k = 0; k < 4; ++k) q.cur[k] = q.nxt[k] = q.pre[k] = 0xFFFFFFFFu;
-      if (t0 < T) { load_perm(t0, q.cur); fill(s, q.cur); }
-      if (t0 + tstride < T) load_perm(t0 + tstride, q.nxt);
+      if (t0 < T) {
+        load_perm(t0, q.cur);
+        gather(q.cur, q.nx, q.ny, q.nz);
+        fill(s, q.nx, q.ny, q.nz);
+      }
+      if (t0 + tstride < T) { load_perm(t0 + tstride, q.nxt); gather(q.nxt, q.nx, q.ny, q.nz); }
     }
     auto io_step = [&](const SlotWalk& w, int s, IoSlot& q) {
       const long long c0_ = (SAND_DIAG && p.prof) ? clock64() : 0;
@@ -517,7 +524,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
         if (t1 < T) {
           mbar_wait_lazy(b_a1free + 8 * s, (uint32_t)(w.ti & 1));   // this tile's layer-1 MMA read A1
           if (SAND_DIAG && p.prof) waited += clock64() - c0_;
-          fill(s, q.nxt);
+          fill(s, q.nx, q.ny, q.nz);
           if (t1 + tstride < T) load_perm(t1 + tstride, q.pre);
         }
       }
@@ -544,6 +551,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
         __syncwarp();
 #pragma unroll
         for (int k = 0; k < 4; ++k) { q.cur[k] = q.nxt[k]; q.nxt[k] = q.pre[k]; }
+        if (w.t + 2 * tstride < T) gather(q.nxt, q.nx, q.ny, q.nz);   // the tile after next: its layer-1 operand
       }
       if (SAND_DIAG && p.prof) { io_wait += waited; io_busy += clock64() - c0_ - waited; }
     };
