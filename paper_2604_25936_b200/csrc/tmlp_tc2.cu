@@ -86,6 +86,9 @@ static_assert(!SAND_SMR || 4 * (SAND_SMR_EPI - 96) <= 96 - SAND_SMR_CTL, "setmax
 #ifndef SAND_EPI_BARWAIT
 #define SAND_EPI_BARWAIT 1   // accumulator waits: one polling warp per column group + a named barrier
 #endif
+#ifndef SAND_HALFSTAGE
+#define SAND_HALFSTAGE 0   // 1: ring stages of half a pass (KC/2 K-chunks; the first carries the bias), twice as many
+#endif
 #ifndef SAND_EARLY_LO
 #define SAND_EARLY_LO 0   // 1: publish the first K-half of the next A as soon as it is stored (pass-1 start)
 #endif
@@ -119,7 +122,10 @@ struct Tc2Shape {
   static constexpr int QCHUNK = QR * 128;          // one K-chunk of a CTA's pass rows (SW128, bytes)
   static constexpr int QSMALL = QR * 32 < 1024 ? 1024 : QR * 32;   // K = 16 bias operand of a pass (padded so
                                                    // the SW128 chunks that follow stay 1024-aligned)
-  static constexpr int STAGE = QSMALL + KC * QCHUNK;   // ring slot = one pass: [bias operand][KC K-chunks]
+  static constexpr int PASS_BYTES = QSMALL + KC * QCHUNK;   // one pass in the image: [bias operand][KC K-chunks]
+  static constexpr int SPP = (SAND_HALFSTAGE && KC >= 2) ? 2 : 1;   // ring stages per pass
+  static constexpr int CPS = KC / SPP;                      // K-chunks per stage
+  static constexpr int STAGE = QSMALL + CPS * QCHUNK;       // ring slot: [bias operand (first stage of a pass)][CPS chunks]
   static constexpr int A1_BYTES = 128 * 32;        // layer-1 A operand: 128 rows x 16 bf16
   static constexpr int W1_BYTES = 2 * QR * 32;     // resident layer-1 B operand: this CTA's 2 x QR rows
   static constexpr int ONES_BYTES = SAND_ONES_A1 ? 0 : 128 * 32;   // bias MMA A operand: 128 rows of (1, 1, 0, ...)
@@ -338,7 +344,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
       w0.start(pair, T, s_tile_end, L);
       w1.start(pair + npairs, T, s_tile_end, L);
       // hidden-layer image: [L-1][CTA][pass][STAGE]: one bulk copy per pass
-      const uint8_t* img = reinterpret_cast<const uint8_t*>(p.m.w_image_pair) + (size_t)rank * 2 * C::STAGE;
+      const uint8_t* img = reinterpret_cast<const uint8_t*>(p.m.w_image_pair) + (size_t)rank * 2 * C::PASS_BYTES;
       const uint32_t peer_wpeer = mapa_shared(b_wpeer, 0);
       constexpr uint32_t ID = idesc_bf16(256, C::HN);
       uint32_t pa[2][2] = {{0, 0}, {0, 0}};   // [slot][lo, hi] a_full parities
@@ -359,14 +365,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
       auto wait_prev_step = [&](const SlotWalk& w, int s) { wait_prev_half(w, s, 0); wait_prev_half(w, s, 1); };
       auto job = [&](const SlotWalk& w, int s) {
         const int l = w.l;
-        const int nsj = l == 1 ? 0 : 2;   // ring stages of this job (one per pass)
+        const int nsj = l == 1 ? 0 : 2 * C::SPP;   // ring stages of this job
         if (warp == 0) {
           for (int j = 0; j < nsj && !(SAND_DIAG && p.prof == 3); ++j) {
             const long long c0_ = (SAND_DIAG && p.prof) ? clock64() : 0;
             mbar_wait_lazy(b_wempty + 8 * st, ph ^ 1u);
             if (SAND_DIAG && p.prof) { pc[4] += clock64() - c0_; pc[5] += 1; }
-            mbar_arrive_expect_tx(b_wfull + 8 * st, C::STAGE);
-            bulk_g2s(sW + st * C::STAGE, img + ((size_t)(l - 2) * 4 + j) * C::STAGE, C::STAGE, b_wfull + 8 * st);
+            // stage j = pass j / SPP, part j % SPP: part 0 = [bias | CPS chunks], part 1 = the other CPS chunks
+            const uint8_t* pb = img + ((size_t)(l - 2) * 4 + j / C::SPP) * C::PASS_BYTES;
+            const bool first = (j % C::SPP) == 0;
+            const uint32_t bytes = first ? C::STAGE : C::CPS * C::QCHUNK;
+            mbar_arrive_expect_tx(b_wfull + 8 * st, bytes);
+            bulk_g2s(first ? sW + st * C::STAGE : sW + st * C::STAGE + C::QSMALL,
+                     first ? pb : pb + C::QSMALL + (size_t)C::CPS * C::QCHUNK, bytes, b_wfull + 8 * st);
             if (++st == nst) { st = 0; ph ^= 1u; }
           }
         } else if (rank == 0) {
@@ -398,7 +409,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
           // so the product is b_hi + b_lo whichever version the tensor core reads)
           const uint64_t ones_d = desc_nosw(SAND_ONES_A1 ? sA1 + s * C::A1_BYTES : sOnes, 128, 256);
 #pragma unroll 1
-          for (int j = 0; j < 2; ++j) {
+          for (int jj = 0; jj < 2 * C::SPP; ++jj) {
+            const int j = jj / C::SPP, part = jj % C::SPP;   // pass, stage within the pass
             const long long c0_ = (SAND_DIAG && p.prof) ? clock64() : 0;
             if (!(SAND_DIAG && p.prof == 3)) { mbar_wait(b_wfull + 8 * st, ph);
             mbar_wait_cluster(b_wpeer + 8 * st, ph); }   // diagnostic 3: no weight streaming
@@ -406,15 +418,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc2Shape<H>::THREADS
             tc_fence_after();
             const uint32_t slot = sW + st * C::STAGE;
             const uint32_t d = acc + (uint32_t)(j * C::HN);
-            mma_bf16_cg2_w(d, ones_d, desc_nosw(slot, 128, 256), ID, 0u);
+            if (part == 0) mma_bf16_cg2_w(d, ones_d, desc_nosw(slot, 128, 256), ID, 0u);
             const uint64_t w_d = desc_sw128(slot + C::QSMALL);
 #pragma unroll 1
-            for (int kc = 0; kc < C::KC; ++kc) {
+            for (int c = 0; c < C::CPS; ++c) {
+              const int kc = part * C::CPS + c;
               if (early && j == 0 && kc == C::KC / 2) { wait_prev_half(w, s, 1); tc_fence_after(); }
-              mma4_bf16_cg2_w(d, a_d + (uint64_t)(kc * (C::A_CHUNK >> 4)), w_d + (uint64_t)(kc * (C::QCHUNK >> 4)), ID, 1u);
+              mma4_bf16_cg2_w(d, a_d + (uint64_t)(kc * (C::A_CHUNK >> 4)), w_d + (uint64_t)(c * (C::QCHUNK >> 4)), ID, 1u);
             }
             mma_commit_cg2_mc_w(b_wempty + 8 * st, 0x3);
-            mma_commit_cg2_mc_w(b_accfull + 16 * s + 8 * j, 0x3);
+            if (part == C::SPP - 1) mma_commit_cg2_mc_w(b_accfull + 16 * s + 8 * j, 0x3);
             if (++st == nst) { st = 0; ph ^= 1u; }
           }
         } else {
