@@ -659,6 +659,10 @@ def run_query(args):
     if args.kprof:
         from paper_2604_25936_b200 import SAND_OPT_KPROF
         ctx.sand_set_option(SAND_OPT_KPROF, args.kprof)
+    from paper_2604_25936_b200 import SAND_OPT_PAIR_KERNEL
+    if args.pair_kernel is not None:
+        ctx.sand_set_option(SAND_OPT_PAIR_KERNEL, args.pair_kernel)
+    pair_mode = ctx.sand_get_option(SAND_OPT_PAIR_KERNEL)
     ctx.sand_load_weights(g.pack_blob(p))
     ctx.sand_load_depthmap(dm)
     ctx.sand_reserve(n)
@@ -799,7 +803,9 @@ def run_query(args):
                  "k_query_simt (FP32, one thread per point)" if fp32 and H <= 64 else
                  "k_query_fp32 (FP32 register-blocked GEMM)" if fp32 else
                  "k_tmlp_wide (K3 fused T-MLP, CTA pair, N-halves)" if H == 336 else
-                 "k_tmlp_tc2 (K3 fused T-MLP, CTA pair)")
+                 "k_tmlp_tc4 (K3 fused T-MLP, CTA pair, one epilogue team per slot)" if pair_mode == 2 else
+                 "k_tmlp_tc2 (K3 fused T-MLP, CTA pair, two N-half passes)" if pair_mode == 1 else
+                 "k_tmlp_tc (K3 fused T-MLP, 1 CTA)")
         full = None
         if summ["ms_full_max"] > 0:
             ms_fd = summ["ms_full_max"] / args.steps
@@ -866,6 +872,8 @@ def main():
     ap.add_argument("--no-full-depth", action="store_true", help="skip the all-L (non-adaptive) comparison run")
     ap.add_argument("--ref-sample", type=int, default=1 << 15)
     ap.add_argument("--full-depth", action="store_true", help="all-L depth map (non-adaptive GPU baseline)")
+    ap.add_argument("--pair-kernel", type=int, default=None, choices=[0, 1, 2],
+                    help="SAND_OPT_PAIR_KERNEL (default: the library's choice, 2 = slot-team CTA-pair kernel)")
     ap.add_argument("--kprof", type=int, default=0, help="diagnostic SAND_OPT_KPROF (per-role counters, stderr)")
     ap.add_argument("--prec", default=None, choices=["bf16", "fp32", "f16x3"],
                     help="default: the config's precision (C0 FP32, others BF16); fp32: the accurate FP32 path "

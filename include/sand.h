@@ -121,9 +121,12 @@ int sand_set_stream(sand_ctx* ctx, void* cuda_stream);
 
 /* Explicit execution options.  libsand reads no environment variable; every choice of kernel or
  * schedule is made here (defaults in brackets).
- *   SAND_OPT_PAIR_KERNEL  [1] SAND_BF16: 1 = CTA-pair (cta_group::2) tcgen05 kernels where the
- *                         configuration fits them, 0 = the 1-CTA kernel.  1 on a configuration without a
- *                         pair kernel -> SAND_ERR_UNSUPPORTED.
+ *   SAND_OPT_PAIR_KERNEL  [2] SAND_BF16: 2 = the slot-team CTA-pair (cta_group::2) kernel (one N = H MMA
+ *                         chain per layer, one epilogue team per tile slot; H in {64, 128, 256}, its tables
+ *                         must fit shared memory), 1 = the two-pass CTA-pair kernels (H in {64, 128, 256,
+ *                         336}), 0 = the 1-CTA kernel.  The default is 2 where usable, else 1, else 0; a value
+ *                         without a kernel for the configuration -> SAND_ERR_UNSUPPORTED.  All compute the
+ *                         same Eq. 2 / 3 arithmetic (BF16 operands, FP32 accumulation, sines and tails).
  *   SAND_OPT_DYN_SCHEDULE [0] sand_query_dynamic: 0 = a 64-point tile stops when all its points have
  *                         stopped; 1 = pools of 512 points re-compacted after every layer (both FP32 SIMT);
  *                         2 = every layer on the split-FP16 tensor-core kernel (SAND_F16X3 arithmetic),

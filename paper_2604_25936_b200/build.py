@@ -7,7 +7,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libsand.so")
-SOURCES = ["sand_api.cu", "lookup.cu", "tmlp_simt.cu", "tmlp_tc.cu", "tmlp_tc2.cu", "tmlp_tc3.cu", "tmlp_x3.cu", "depthpop.cu", "mesh.cu"]
+SOURCES = ["sand_api.cu", "lookup.cu", "tmlp_simt.cu", "tmlp_tc.cu", "tmlp_tc2.cu", "tmlp_tc3.cu", "tmlp_tc4.cu", "tmlp_x3.cu", "depthpop.cu", "mesh.cu"]
 HEADERS = ["ptx.cuh", "sand_internal.h", "tmlp_common.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 # extra defines for diagnostic builds, e.g. SAND_BUILD_DEFS="-DSAND_HANG_DEBUG" (bounded mbarrier waits)

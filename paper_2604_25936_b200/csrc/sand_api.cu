@@ -34,8 +34,9 @@ struct sand_ctx {
   int num_sms = 0;
   cudaStream_t stream = nullptr;
   int lod_cap = 0;
-  bool use_pair = true;   // CTA-pair tcgen05 kernel where available (SAND_OPT_PAIR_KERNEL)
-  bool pair_ok = true;    // the CTA-pair kernel supports (L, H, tail) at all
+  int use_pair = 2;       // SAND_OPT_PAIR_KERNEL: 0 = 1-CTA, 1 = two-pass CTA-pair, 2 = slot-team CTA-pair kernel
+  bool pair_ok = true;    // a CTA-pair kernel supports (L, H, tail) at all
+  bool team_ok = false;   // the slot-team CTA-pair kernel does
   int dyn_schedule = 0;   // sand_query_dynamic schedule (SAND_OPT_DYN_SCHEDULE)
   int kprof = 0;          // diagnostic per-role counters (SAND_OPT_KPROF)
   std::string err;
@@ -46,6 +47,8 @@ struct sand_ctx {
   void* d_w1_image = nullptr;
   void* d_wimage = nullptr;
   void* d_wimage_pair = nullptr;
+  void* d_tc4_w1 = nullptr;       // slot-team kernel images (tmlp_tc4.cu)
+  void* d_tc4_image = nullptr;
   float* d_whidden = nullptr;
   float* d_wt_f32 = nullptr;      // FP32 hidden weights transposed [L-1][k][j] (depth-map population)
   void* d_x3_image = nullptr;     // split-FP16 hidden-layer image (tmlp_x3.cu)
@@ -170,8 +173,11 @@ extern "C" int sand_create(const sand_config* cfg, sand_ctx** out) {
   ctx->num_sms = prop.multiProcessorCount;
   // the CTA-pair kernel keeps its per-column tables in shared memory: large L falls back to the 1-CTA kernel
   if (cfg->prec == SAND_BF16)
+  {
     ctx->pair_ok = tc2_usable(cfg->L, cfg->H, cfg->tail) || tc3_usable(cfg->L, cfg->H, cfg->tail);
-  ctx->use_pair = ctx->pair_ok;
+    ctx->team_ok = tc4_usable(cfg->L, cfg->H, cfg->tail);
+  }
+  ctx->use_pair = ctx->team_ok ? 2 : (ctx->pair_ok ? 1 : 0);
   cudaError_t e = prepare_tmlp_kernels(cfg->L, cfg->H, cfg->tail, cfg->prec);
   if (e != cudaSuccess) { fail(ctx, SAND_ERR_CUDA, "kernel attribute setup: %s", cudaGetErrorString(e)); return bail(SAND_ERR_CUDA); }
   *out = ctx;
@@ -187,7 +193,7 @@ static void free_depthmap(sand_ctx* c) {
   c->have_dm = false;
 }
 static void free_weights(sand_ctx* c) {
-  dfree(c->d_tables); dfree(c->d_pair_tables); dfree(c->d_w1_image); dfree(c->d_wimage); dfree(c->d_wimage_pair); dfree(c->d_whidden); dfree(c->d_wt_f32);
+  dfree(c->d_tables); dfree(c->d_pair_tables); dfree(c->d_w1_image); dfree(c->d_wimage); dfree(c->d_wimage_pair); dfree(c->d_tc4_w1); dfree(c->d_tc4_image); dfree(c->d_whidden); dfree(c->d_wt_f32);
   dfree(c->d_x3_image); dfree(c->d_x3_tables); c->have_x3 = false;
   c->have_w = false;
 }
@@ -308,6 +314,22 @@ extern "C" int sand_load_weights(sand_ctx* ctx, const float* blob, size_t n_floa
     CU(cudaMalloc(&ctx->d_pair_tables, sizeof(float) * pt.size()));
     CU(cudaMemcpy(ctx->d_pair_tables, pt.data(), sizeof(float) * pt.size(), cudaMemcpyHostToDevice));
     m.pair_tables = ctx->d_pair_tables;
+  }
+  if (ctx->cfg.prec == SAND_BF16 && tc4_available(H, tail)) {
+    // slot-team CTA-pair kernel: its own layer-1 and hidden-layer images (tables shared with tmlp_tc2.cu)
+    std::vector<uint16_t> w1img;
+    std::vector<uint8_t> img;
+    tc4_build_host(L, H, w0, W.data(), b.data(), &w1img, &img);
+    dfree(ctx->d_tc4_w1);
+    dfree(ctx->d_tc4_image);
+    CU(cudaMalloc(&ctx->d_tc4_w1, w1img.size() * 2));
+    CU(cudaMemcpy(ctx->d_tc4_w1, w1img.data(), w1img.size() * 2, cudaMemcpyHostToDevice));
+    m.tc4_w1 = ctx->d_tc4_w1;
+    if (!img.empty()) {
+      CU(cudaMalloc(&ctx->d_tc4_image, img.size()));
+      CU(cudaMemcpy(ctx->d_tc4_image, img.data(), img.size(), cudaMemcpyHostToDevice));
+    }
+    m.tc4_image = ctx->d_tc4_image;
   }
   if (ctx->cfg.prec == SAND_BF16 && tc3_available(H, tail)) {
     // wide CTA-pair kernel: padded-width tables, layer-1 and hidden-layer images (tmlp_tc3.cu)
@@ -511,9 +533,10 @@ extern "C" int sand_set_option(sand_ctx* ctx, int option, int64_t value) {
   if (!ctx) return fail(ctx, SAND_ERR_ARG, "NULL ctx");
   switch (option) {
     case SAND_OPT_PAIR_KERNEL:
-      if (value != 0 && value != 1) return fail(ctx, SAND_ERR_ARG, "SAND_OPT_PAIR_KERNEL takes 0 or 1");
-      if (value == 1 && !ctx->pair_ok) return fail(ctx, SAND_ERR_UNSUPPORTED, "no CTA-pair kernel for this (prec, L, H, tail)");
-      ctx->use_pair = value == 1;
+      if (value < 0 || value > 2) return fail(ctx, SAND_ERR_ARG, "SAND_OPT_PAIR_KERNEL takes 0, 1 or 2");
+      if (value >= 1 && !ctx->pair_ok) return fail(ctx, SAND_ERR_UNSUPPORTED, "no CTA-pair kernel for this (prec, L, H, tail)");
+      if (value == 2 && !ctx->team_ok) return fail(ctx, SAND_ERR_UNSUPPORTED, "no slot-team CTA-pair kernel for this (prec, L, H, tail)");
+      ctx->use_pair = (int)value;
       return SAND_OK;
     case SAND_OPT_DYN_SCHEDULE:
       if (value < 0 || value > 2) return fail(ctx, SAND_ERR_ARG, "SAND_OPT_DYN_SCHEDULE takes 0, 1 or 2");
@@ -536,7 +559,7 @@ extern "C" int sand_set_option(sand_ctx* ctx, int option, int64_t value) {
 extern "C" int sand_get_option(const sand_ctx* ctx, int option, int64_t* value) {
   if (!ctx || !value) return SAND_ERR_ARG;
   switch (option) {
-    case SAND_OPT_PAIR_KERNEL: *value = ctx->use_pair ? 1 : 0; return SAND_OK;
+    case SAND_OPT_PAIR_KERNEL: *value = ctx->use_pair; return SAND_OK;
     case SAND_OPT_DYN_SCHEDULE: *value = ctx->dyn_schedule; return SAND_OK;
     case SAND_OPT_KPROF: *value = ctx->kprof; return SAND_OK;
     case SAND_OPT_FP32_TENSOR: *value = ctx->fp32_tensor; return SAND_OK;

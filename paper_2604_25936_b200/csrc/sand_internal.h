@@ -82,18 +82,23 @@ struct MlpDev {
   // a1 [L-1][H] (MULT), c [L], c1 [L]
   const void* x3_image;
   const float* x3_tables;
+  // slot-team CTA-pair kernel (tmlp_tc4.cu): layer-1 split-BF16 operand [2 CTAs][H/2 rows][16 bf16] and
+  // per (layer, CTA) runs [bias operand][KC SW128 K-chunks] of this CTA's H/2 output features; tables = pair_tables
+  const void* tc4_w1;
+  const void* tc4_image;
   long long x3_floats, x3_off_w1, x3_off_a, x3_off_a1, x3_off_c, x3_off_c1;
 };
 
 
 cudaError_t launch_tmlp_simt(const MlpDev& m, const float* pts, const uint32_t* perm, const QueryMeta* meta,
                              float* out_sdf, int num_sms, cudaStream_t st);
-// use_pair: CTA-pair (cta_group::2, 256-row tiles) kernel where available (H in {128, 256})
+// pair_mode (SAND_OPT_PAIR_KERNEL): 0 = 1-CTA kernel; 1 = two-pass CTA-pair kernel (tc2 / tc3);
+// 2 = slot-team CTA-pair kernel (tc4) where usable, else as 1.  Pair kernels consume 256-row tiles.
 cudaError_t launch_tmlp_tc(const MlpDev& m, const float* pts, const uint32_t* perm, const QueryMeta* meta,
-                           float* out_sdf, int num_sms, cudaStream_t st, bool use_pair);
+                           float* out_sdf, int num_sms, cudaStream_t st, int pair_mode);
 // configuration query: dynamic smem bytes for the tc kernel, 0 if unsupported
 size_t tc_smem_bytes(int L, int H, int tail);
-int tmlp_tile_rows(int H, int prec, bool use_pair);   // tile size the selected T-MLP kernel consumes
+int tmlp_tile_rows(int H, int prec, int pair_mode);   // tile size the selected T-MLP kernel consumes
 bool tc_supported_H(int H);
 bool simt_supported_H(int H);
 size_t simt_smem_bytes(int L, int H, int tail);
@@ -129,6 +134,14 @@ void tc2_build_host(int L, int H, int tail, float w0, const float* const* W, con
 cudaError_t launch_tmlp_tc2(const MlpDev& m, const float* pts, const uint32_t* perm, const QueryMeta* meta,
                             float* out, int num_sms, cudaStream_t st);
 cudaError_t prepare_tc2(int H, int tail);
+// Slot-team CTA-pair kernel (tmlp_tc4.cu): one N = H MMA chain per layer, one epilogue team per tile slot
+bool tc4_available(int H, int tail);
+bool tc4_usable(int L, int H, int tail);
+void tc4_build_host(int L, int H, float w0, const float* const* W, const float* const* b, std::vector<uint16_t>* w1img,
+                    std::vector<uint8_t>* img);
+cudaError_t launch_tmlp_tc4(const MlpDev& m, const float* pts, const uint32_t* perm, const QueryMeta* meta,
+                            float* out, int num_sms, cudaStream_t st);
+cudaError_t prepare_tc4(int H, int tail);
 size_t tc2_w1_offset(int H, int n, int k);   // byte offset of (unit n, column k) in MlpDev::w1_image
 // Wide CTA-pair kernel (tmlp_tc3.cu): H = 336, LINEAR; one 256-row tile split into two N-halves.  It reuses
 // MlpDev::pair_tables / w1_image / w_image_pair with its own (padded-width) layouts, built by tc3_build_host.

@@ -318,15 +318,17 @@ static cudaError_t prep_tc_t() {
 
 
 
-int tmlp_tile_rows(int H, int prec, bool use_pair) {
+int tmlp_tile_rows(int H, int prec, int pair_mode) {
   if (prec == SAND_F16X3) return 256;
-  return (prec == SAND_BF16 && use_pair && (tc2_available(H) || tc3_available(H, SAND_TAIL_LINEAR))) ? 256 : kTileM;
+  return (prec == SAND_BF16 && pair_mode && (tc2_available(H) || tc3_available(H, SAND_TAIL_LINEAR))) ? 256 : kTileM;
 }
 
 cudaError_t launch_tmlp_tc(const MlpDev& m, const float* pts, const uint32_t* perm, const QueryMeta* meta,
-                           float* out, int num_sms, cudaStream_t st, bool use_pair) {
-  if (use_pair && tc2_available(m.H)) return launch_tmlp_tc2(m, pts, perm, meta, out, num_sms, st);
-  if (use_pair && tc3_available(m.H, m.tail)) return launch_tmlp_tc3(m, pts, perm, meta, out, num_sms, st);
+                           float* out, int num_sms, cudaStream_t st, int pair_mode) {
+  if (pair_mode == 2 && m.tc4_w1 && tc4_usable(m.L, m.H, m.tail))
+    return launch_tmlp_tc4(m, pts, perm, meta, out, num_sms, st);
+  if (pair_mode && tc2_available(m.H)) return launch_tmlp_tc2(m, pts, perm, meta, out, num_sms, st);
+  if (pair_mode && tc3_available(m.H, m.tail)) return launch_tmlp_tc3(m, pts, perm, meta, out, num_sms, st);
   const bool mult = m.tail == SAND_TAIL_MULT;
 #define SAND_TC_CASE(HH)                                                                     \
   case HH:                                                                                   \
@@ -349,6 +351,10 @@ cudaError_t prepare_tmlp_kernels(int L, int H, int tail, int prec) {
   const bool mult = tail == SAND_TAIL_MULT;
   if (tc2_available(H)) {
     const cudaError_t e = prepare_tc2(H, tail);
+    if (e != cudaSuccess) return e;
+  }
+  if (tc4_available(H, tail)) {
+    const cudaError_t e = prepare_tc4(H, tail);
     if (e != cudaSuccess) return e;
   }
   if (tc3_available(H, tail)) {

@@ -310,9 +310,9 @@ def test_deep_nets_pair_kernel_limits(L, tail):
 
 
 def test_options_explicit_and_pair_kernel_switch():
-    """sand_set_option (no environment variables): defaults, bad keys / values, and the 1-CTA kernel
-    selected at run time through SAND_OPT_PAIR_KERNEL gives the same exit depths and SDF within the
-    BF16 tolerance as the CTA-pair kernel on the same context."""
+    """sand_set_option (no environment variables): defaults, bad keys / values, and every kernel selectable
+    through SAND_OPT_PAIR_KERNEL (2 = slot-team CTA-pair, 1 = two-pass CTA-pair, 0 = 1-CTA) gives the same
+    exit depths and SDF within the BF16 tolerance on the same context."""
     from paper_2604_25936_b200 import SAND_OPT_DYN_SCHEDULE, SAND_OPT_KPROF, SAND_OPT_PAIR_KERNEL, SandError
     spec = g.TMlpSpec(L=5, H=256, omega0=30.0, seed=77)
     p = g.make_weights(spec)
@@ -321,18 +321,42 @@ def test_options_explicit_and_pair_kernel_switch():
     pts = rng.uniform(-1, 1, (70001, 3)).astype(np.float32)
     sdf_or, dep_or = oracle_query(p, dm, pts)
     with make_ctx(spec, BF16) as ctx:
-        assert ctx.sand_get_option(SAND_OPT_PAIR_KERNEL) == 1
+        assert ctx.sand_get_option(SAND_OPT_PAIR_KERNEL) == 2
         assert ctx.sand_get_option(SAND_OPT_DYN_SCHEDULE) == 0
         assert ctx.sand_get_option(SAND_OPT_KPROF) == 0
-        for bad in ((99, 0), (SAND_OPT_PAIR_KERNEL, 2), (SAND_OPT_DYN_SCHEDULE, -1), (SAND_OPT_KPROF, 7)):
+        for bad in ((99, 0), (SAND_OPT_PAIR_KERNEL, 3), (SAND_OPT_PAIR_KERNEL, -1), (SAND_OPT_DYN_SCHEDULE, -1),
+                    (SAND_OPT_KPROF, 7)):
             with pytest.raises(SandError):
                 ctx.sand_set_option(*bad)
-        sdf2, dep2 = run_engine(ctx, p, dm, pts)
-        ctx.sand_set_option(SAND_OPT_PAIR_KERNEL, 0)
-        assert ctx.sand_get_option(SAND_OPT_PAIR_KERNEL) == 0
-        sdf1, dep1 = run_engine(ctx, p, dm, pts)
-    assert_parity(sdf2, dep2, sdf_or, dep_or, TOL_BF16)
-    assert_parity(sdf1, dep1, sdf_or, dep_or, TOL_BF16)
+        res = {}
+        for mode in (2, 1, 0):
+            ctx.sand_set_option(SAND_OPT_PAIR_KERNEL, mode)
+            assert ctx.sand_get_option(SAND_OPT_PAIR_KERNEL) == mode
+            res[mode] = run_engine(ctx, p, dm, pts)
+    for mode in (2, 1, 0):
+        assert_parity(*res[mode], sdf_or, dep_or, TOL_BF16)
+
+
+@pytest.mark.parametrize("H", [64, 128, 256])
+@pytest.mark.parametrize("tail", [0, 1])
+@pytest.mark.parametrize("mode", [1, 2])
+def test_bf16_pair_kernels_both(H, tail, mode):
+    """Both CTA-pair kernels (SAND_OPT_PAIR_KERNEL 1: two N-half passes per layer, 16 lock-step epilogue warps;
+    2: one N = H chain per layer, one epilogue team per tile slot, weight stages shared by the slots) on every
+    depth 1..L, many 256-row tiles per depth with ragged tails, and a second query on the same context (the
+    persistent kernels' barrier phases restart per launch)."""
+    from paper_2604_25936_b200 import SAND_OPT_PAIR_KERNEL
+    L = 8
+    spec = g.TMlpSpec(L=L, H=H, omega0=30.0, tail=tail, seed=90 + H + tail)
+    p = g.make_weights(spec)
+    dm = _random_voxel_map(4, L, 91)
+    pts = _pts(150001, 92)
+    sdf_or, dep_or = oracle_query(p, dm, pts)
+    with make_ctx(spec, BF16) as ctx:
+        ctx.sand_set_option(SAND_OPT_PAIR_KERNEL, mode)
+        for _ in range(2):
+            sdf, dep = run_engine(ctx, p, dm, pts)
+            assert_parity(sdf, dep, sdf_or, dep_or, TOL_BF16)
 
 
 @pytest.mark.parametrize("name", [
