@@ -25,11 +25,11 @@
 //   warp 0   weight producer (lane 0): bias operand + K-chunks of this CTA's N/2 B rows, bulk async copies
 //   warp 1   TMEM allocator; leader: tcgen05.mma.cta_group::2 issuer (converged warp, elected lane);
 //            odd CTA: relays "my half landed" to the leader (w_peer / b_peer)
-//   warp 2   IO: perm rows, point gathers, the split-BF16 layer-1 operand, sdf[perm[row]] stores
-//   warp 3   idle (the teams start at a warpgroup boundary: warp % 4 = TMEM lane quadrant)
+//   warps 2, 3  IO of slot 0 / slot 1: perm rows, point gathers, the split-BF16 layer-1 operand, sdf[perm[row]]
+//            stores
 //   warps 4.. epilogue teams: team s = warps 4 + 4 NCG s .. ; thread = row 32 (warp % 4) + lane
-// The producer, MMA issuer, relay and IO warps walk one job order (slot 0, slot 1 alternating; a slot's jobs
-// are its tiles' layers); each team walks its own slot's jobs.
+// The producer, MMA issuer and relay walk one job order (slot 0, slot 1 alternating; a slot's jobs are its tiles'
+// layers); each IO warp and each team walks its own slot's jobs.
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -44,34 +44,45 @@
 #ifndef SAND_T4_NCG
 #define SAND_T4_NCG 1     // column groups per team (1: a thread owns all H columns of its row)
 #endif
+#ifndef SAND_T4_PP
+#define SAND_T4_PP 1      // LINEAR tails: all epilogue warps serve both slots step by step (ping-pong)
+#endif
 #ifndef SAND_T4_SHARE
 #define SAND_T4_SHARE 1   // slot 1 reuses slot 0's weight stages when it runs the same layer right after it
 #endif
+#ifndef SAND_T4_PROF
+#define SAND_T4_PROF 0    // 1: per-role clock64 wait / busy counters, dumped to stderr after every launch (synchronous)
+#endif
+#ifndef SAND_T4_TRACE
+#define SAND_T4_TRACE 0   // 1: per-job clock64 timeline of CTA 0 (MMA issuer + epilogue warp 4), dumped by the host
+#endif
 #ifndef SAND_T4_ABL
-#define SAND_T4_ABL 0     // ablation builds, timing only: 1 no sine, 2 no A stores, 3 no TMEM loads, 4 no tail
+#define SAND_T4_ABL 0     // ablation bitmask, timing only (wrong results): 1 no sine, 2 no A stores, 4 no TMEM loads, 8 no tail
 #endif
 
 namespace sand {
 
-template <int H>
+template <int H, bool PP>
 struct Tc4Shape {
   static constexpr int KC = H / 64;                 // 64-wide K-chunks (128-byte swizzle atoms)
   static constexpr int NR = H / 2;                  // B rows (output features) per CTA (cta_group::2: half each)
   static constexpr int CHUNK = NR * 128;            // one K-chunk of this CTA's B rows (SW128)
   static constexpr int A_CHUNK = 128 * 128;         // one K-chunk of this CTA's 128 A rows
   static constexpr int A_BYTES = KC * A_CHUNK;
-  static constexpr int BIAS_BYTES = NR * 32;        // K = 16 bias operand (l1_off layout)
+  static constexpr int BIAS_BYTES = NR * 32;        // K = 16 bias operand (l1_off layout, (b_hi, b_lo) at k = 9, 10)
   static constexpr int LAYER_BYTES = BIAS_BYTES + KC * CHUNK;   // one (layer, CTA) run of the image
   static constexpr int A1_BYTES = 128 * 32;
   static constexpr int W1_BYTES = NR * 32;
-  static constexpr int ONES_BYTES = 128 * 32;
-  static constexpr int NCG = SAND_T4_NCG;
+  // PP (ping-pong): all 16 epilogue warps serve both slots step by step (4 column groups); else two teams of
+  // 4 NCG warps, one per slot
+  static constexpr int NCG = PP ? 4 : SAND_T4_NCG;
   static constexpr int CW = H / NCG;                // columns per epilogue thread
   static constexpr int NB = CW / 32;                // 32-column TMEM load batches per thread
   static constexpr int TMEM_COLS = 2 * H <= 128 ? 128 : (2 * H <= 256 ? 256 : 512);
   static constexpr int NCTL = 4;
-  static constexpr int TEAM_WARPS = 4 * NCG;
-  static constexpr int THREADS = 32 * (NCTL + 2 * TEAM_WARPS);
+  static constexpr int TEAM_WARPS = 4 * NCG;        // epilogue warps serving one slot
+  static constexpr int EPI_WARPS = PP ? TEAM_WARPS : 2 * TEAM_WARPS;
+  static constexpr int THREADS = 32 * (NCTL + EPI_WARPS);
   static_assert(H % 64 == 0 && H <= 256, "team kernel: H in {64, 128, 192, 256}");
   static_assert(CW % 32 == 0, "whole 32-column batches per thread");
 };
@@ -84,6 +95,22 @@ struct Tc4Params {
   float* out;
   int nst;
 };
+
+// Diagnostic counters (SAND_T4_PROF builds), per CTA: 0-3 team 0 wait_acc / busy / tile_end / steps, 4-7 team 1,
+// 8 MMA wait a_full, 9 MMA wait a1_full, 10 MMA wait weights, 11 MMA loop, 12 producer wait empty,
+// 13 IO0 wait a1_free, 14 IO0 wait io_done, 15 team 0 loop
+constexpr int kT4Prof = 16;
+__device__ unsigned long long g_t4prof[160][kT4Prof];
+#define T4CLK() (SAND_T4_PROF ? clock64() : 0ll)
+// Trace (SAND_T4_TRACE builds), CTA 0 only, per job j in MMA order: 0 MMA wait start, 1 a_full passed, 2 weights
+// passed, 3 issue done (acc commit), 4 epilogue wait start, 5 accumulator ready, 6 published, 7 step end
+constexpr int kT4Trace = 8192;
+__device__ long long g_t4trace[kT4Trace][8];
+// IO trace (slot 0 IO warp of CTA 0), per tile: 0 a1free wait start, 1 a1free ok, 2 fill+gather+perm done,
+// 3 iodone wait start, 4 iodone ok, 5 partfree arrived, 6 end; team tile end: 7 partfree ok (epilogue warp 4)
+__device__ long long g_t4iotr[kT4Trace][8];
+#define T4IO(j, f) do { if (SAND_T4_TRACE && blockIdx.x == 0 && (j) < kT4Trace) g_t4iotr[(j)][(f)] = clock64(); } while (0)
+#define T4TR(j, f) do { if (SAND_T4_TRACE && blockIdx.x == 0 && (j) < kT4Trace) g_t4trace[(j)][(f)] = clock64(); } while (0)
 
 __device__ __forceinline__ int tile_depth4(long long t, const long long* te, int L) {
   for (int d = L; d >= 1; --d)
@@ -101,10 +128,13 @@ struct Walk4 {
     t = t_;
     done = t >= T;
     l = 1;
-    d = done ? 0 : tile_depth4(t, te, L);
+    // tiles are ordered deepest depth first and a walk only moves forward: step the depth down from the last one
+    if (!done)
+      while (d > 1 && t >= te[d]) --d;
   }
   __device__ __forceinline__ void start(long long t0, long long T, const long long* te, int L) {
     ti = 0;
+    d = L;
     set(t0, T, te, L);
   }
   __device__ __forceinline__ void advance(long long stride, long long T, const long long* te, int L) {
@@ -121,18 +151,60 @@ __device__ __forceinline__ float4 lds128f(uint32_t addr) {
   asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
   return v;
 }
+// bf16x2 pack without F2FP: F2FP.BF16.F32.PACK_AB issues to the same pipe as MUFU.SIN on sm_100a
+// (scripts/micro/epi4.cu: sine + F2FP pack + store 10.4 clk per element-warp per SMSP, integer pack 9.0, MUFU
+// floor 8).  Round to nearest, ties away from zero on the magnitude: bits + 0x8000, then the high halves of two
+// words by one PRMT (IADD + PRMT on the ALU pipe).  h = sin(.) is finite, |h| <= 1, so no carry reaches the sign.
+__device__ __forceinline__ uint32_t pack_bf16x2_int(float lo, float hi) {
+  return __byte_perm(__float_as_uint(lo) + 0x8000u, __float_as_uint(hi) + 0x8000u, 0x7632);
+}
+#ifndef SAND_T4_NPOLY
+#define SAND_T4_NPOLY 2   // sine pairs per 16 (per 32-column batch) evaluated by the FMA-pipe polynomial instead of MUFU
+#endif
+#ifndef SAND_T4_F2FP
+#define SAND_T4_F2FP 0    // 1: pack with cvt.rn.bf16x2.f32 (F2FP) instead
+#endif
+__device__ __forceinline__ uint32_t pack_h(float lo, float hi) {
+  return SAND_T4_F2FP ? pack_bf16x2(lo, hi) : pack_bf16x2_int(lo, hi);
+}
+// Odd polynomial sine on the FMA pipe for two lanes at a time (shares the sine work with MUFU.SIN, which is the
+// epilogue's binding pipe): k = rint(z / 2 pi) by the 1.5 2^23 magic add fused into the scaling FMA, r = z - 2 pi k
+// in [-pi, pi], sin r = r P(r^2), degree-7 minimax fit on [-pi, pi] (|err| < 2.6e-4 -- below the 2^-9 relative
+// rounding of h to bf16 for the next layer; in the FP32 tail a few 1e-5 at most).
+__device__ __forceinline__ float2 sin_poly2(float2 z) {
+#if SAND_T4_ABL & 1
+  return z;
+#else
+  const float2 t = __ffma2_rn(z, make_float2(0.15915494309189535f, 0.15915494309189535f),
+                              make_float2(12582912.0f, 12582912.0f));
+  const float2 k = __fadd2_rn(t, make_float2(-12582912.0f, -12582912.0f));
+  const float2 r = __ffma2_rn(k, make_float2(-6.283185307179586f, -6.283185307179586f), z);
+  const float2 r2 = __fmul2_rn(r, r);
+  float2 q = __ffma2_rn(r2, make_float2(-0.0001450767886126414f, -0.0001450767886126414f),
+                        make_float2(0.007958059199154377f, 0.007958059199154377f));
+  q = __ffma2_rn(q, r2, make_float2(-0.16566696763038635f, -0.16566696763038635f));
+  q = __ffma2_rn(q, r2, make_float2(0.9992758631706238f, 0.9992758631706238f));
+  return __fmul2_rn(q, r);
+#endif
+}
 __device__ __forceinline__ float sin_mufu(float z) {
-#if SAND_T4_ABL == 1
+#if SAND_T4_ABL & 1
   return z;
 #else
   return __sinf(z);
 #endif
 }
 
+// ping-pong for LINEAR tails at H >= 128 (4 column groups of >= 32 columns); teams otherwise (Eq. 3 products need a
+// row's two full dot products in one thread)
 template <int H, int TAIL>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc4Shape<H>::THREADS, 1)
+constexpr bool tc4_pp() { return SAND_T4_PP && TAIL == SAND_TAIL_LINEAR && H >= 128; }
+
+template <int H, int TAIL>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc4Shape<H, tc4_pp<H, TAIL>()>::THREADS, 1)
     k_tmlp_tc4(const Tc4Params p) {
-  using C = Tc4Shape<H>;
+  constexpr bool PP = tc4_pp<H, TAIL>();
+  using C = Tc4Shape<H, PP>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base = smem_u32(smem_raw);
   if (base & 1023u) __trap();
@@ -144,8 +216,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc4Shape<H>::THREADS
   const uint32_t sA = base;                                  // [slot] KC x 16 KB, SW128 K-major
   const uint32_t sW = sA + 2 * C::A_BYTES;                   // chunk ring, nst x CHUNK
   const uint32_t sB = sW + nst * C::CHUNK;                   // bias ring, 2 x BIAS_BYTES
-  const uint32_t sOnes = sB + 2 * C::BIAS_BYTES;             // (1, 1, 0, ...) rows: bias MMA A operand
-  const uint32_t sW1 = sOnes + C::ONES_BYTES;                // resident layer-1 B operand
+  // The bias MMA's A operand is the slot's layer-1 operand A1: its k = 9, 10 are 1 in every row and the bias
+  // operand is zero outside k = 9, 10, so the product is b_hi + b_lo whichever tile's rows the IO warp is
+  // writing into A1's other columns meanwhile (all finite).
+  const uint32_t sW1 = sB + 2 * C::BIAS_BYTES;               // resident layer-1 B operand
   const uint32_t sA1 = sW1 + C::W1_BYTES;                    // [slot] layer-1 A operand
   const uint32_t sTab = sA1 + 2 * C::A1_BYTES;
   const long long ntab = (p.m.pt_floats + 3) & ~3ll;
@@ -177,10 +251,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc4Shape<H>::THREADS
     const float4* src = reinterpret_cast<const float4*>(p.m.pair_tables);
     float4* dst = reinterpret_cast<float4*>(tab);
     for (long long i = tid; i < ntab / 4; i += blockDim.x) dst[i] = src[i];
-    uint32_t* ones = reinterpret_cast<uint32_t*>(smem_raw + (sOnes - base));
-    for (int i = tid; i < C::ONES_BYTES / 4; i += blockDim.x) ones[i] = 0u;
-    __syncthreads();
-    for (int r = tid; r < 128; r += blockDim.x) ones[l1_off((uint32_t)r, 0) / 4] = 0x3F803F80u;
     const uint4* w1s = reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(p.m.tc4_w1) + rank * C::W1_BYTES);
     uint4* w1d = reinterpret_cast<uint4*>(smem_raw + (sW1 - base));
     for (int i = tid; i < C::W1_BYTES / 16; i += blockDim.x) w1d[i] = w1s[i];
@@ -190,7 +260,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc4Shape<H>::THREADS
       s_start[tid] = p.meta->start[tid];
       s_count[tid] = p.meta->count[tid];
     }
-    fence_proxy_async_smem();   // ones / W1 (generic stores) -> tensor core (async proxy)
+    fence_proxy_async_smem();   // W1 (generic stores) -> tensor core (async proxy)
   }
   if (tid == 0) {
     for (int i = 0; i < nst; ++i) {
@@ -237,49 +307,73 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc4Shape<H>::THREADS
     int st = 0, bst = 0;          // next free chunk / bias stage (owner jobs)
     uint32_t ph = 0, bph = 0;
     int own_st = 0, own_bst = 0;  // stages of the last owner job (sharers reuse them)
+    unsigned long long pc[5] = {0, 0, 0, 0, 0};   // SAND_T4_PROF: wait a_full, a1_full, weights, loop, empty
+    const long long tl0 = T4CLK();
+    int jc = 0;   // job counter (trace)
     auto job = [&](const Walk4& w, int s, bool share, bool next_shares) {
       const int l = w.l;
+      const bool tr = SAND_T4_TRACE && warp == 1 && rank == 0 && lane == 0;
+      if (tr) T4TR(jc, 0);
       if (l == 1) {
         if (warp == 1 && rank == 0) {
+          long long c0 = T4CLK();
           if (w.ti != 0) { mbar_wait_cluster(b_afull + 8 * s, pa[s]); pa[s] ^= 1u; }
+          long long c1 = T4CLK();
+          if (tr) T4TR(jc, 1);
           mbar_wait_cluster(b_a1full + 8 * s, (uint32_t)(w.ti & 1));
+          if (tr) T4TR(jc, 2);
+          if (SAND_T4_PROF) { pc[0] += c1 - c0; pc[1] += T4CLK() - c1; }
           tc_fence_after();
           const uint32_t acc = tmem_base + (uint32_t)(s * H);
           mma_bf16_cg2_w(acc, desc_nosw(sA1 + s * C::A1_BYTES, 128, 256), desc_nosw(sW1, 128, 256), ID, 0u);
           mma_commit_cg2_mc_w(b_a1free + 8 * s, 0x3);
           mma_commit_cg2_mc_w(b_accfull + 8 * s, 0x3);
+          if (tr) T4TR(jc, 3);
         }
+        ++jc;
         return;
       }
       if (warp == 0) {
         if (share) return;
         const uint8_t* lb = img + (size_t)(l - 2) * 2 * C::LAYER_BYTES;
-        mbar_wait_lazy(b_bempty + 8 * bst, bph ^ 1u);
+        long long c0 = T4CLK();
+        mbar_wait(b_bempty + 8 * bst, bph ^ 1u);
+        if (SAND_T4_PROF) pc[4] += T4CLK() - c0;
         mbar_arrive_expect_tx(b_bfull + 8 * bst, C::BIAS_BYTES);
         bulk_g2s(sB + bst * C::BIAS_BYTES, lb, C::BIAS_BYTES, b_bfull + 8 * bst);
         if (++bst == 2) { bst = 0; bph ^= 1u; }
         for (int kc = 0; kc < C::KC; ++kc) {
-          mbar_wait_lazy(b_wempty + 8 * st, ph ^ 1u);
+          c0 = T4CLK();
+          mbar_wait(b_wempty + 8 * st, ph ^ 1u);
+          if (SAND_T4_PROF) pc[4] += T4CLK() - c0;
           mbar_arrive_expect_tx(b_wfull + 8 * st, C::CHUNK);
           bulk_g2s(sW + st * C::CHUNK, lb + C::BIAS_BYTES + (size_t)kc * C::CHUNK, C::CHUNK, b_wfull + 8 * st);
           if (++st == nst) { st = 0; ph ^= 1u; }
         }
       } else if (rank == 0) {
+        long long c0 = T4CLK();
         mbar_wait_cluster(b_afull + 8 * s, pa[s]);   // the slot's previous step (l - 1) is done
         pa[s] ^= 1u;
+        if (SAND_T4_PROF) pc[0] += T4CLK() - c0;
+        if (tr) T4TR(jc, 1);
         const uint32_t acc = tmem_base + (uint32_t)(s * H);
         const uint64_t a_d = desc_sw128(sA + s * C::A_BYTES);
         if (!share) {
           own_bst = bst;
           own_st = st;
+          c0 = T4CLK();
           mbar_wait(b_bfull + 8 * bst, bph);
           mbar_wait_cluster(b_bpeer + 8 * bst, bph);
+          if (SAND_T4_PROF) pc[2] += T4CLK() - c0;
+          if (tr) T4TR(jc, 2);
           tc_fence_after();
-          mma_bf16_cg2_w(acc, desc_nosw(sOnes, 128, 256), desc_nosw(sB + bst * C::BIAS_BYTES, 128, 256), ID, 0u);
+          mma_bf16_cg2_w(acc, desc_nosw(sA1 + s * C::A1_BYTES, 128, 256), desc_nosw(sB + bst * C::BIAS_BYTES, 128, 256), ID, 0u);
 #pragma unroll 1
           for (int kc = 0; kc < C::KC; ++kc) {
+            c0 = T4CLK();
             mbar_wait(b_wfull + 8 * st, ph);
             mbar_wait_cluster(b_wpeer + 8 * st, ph);
+            if (SAND_T4_PROF) pc[2] += T4CLK() - c0;
             tc_fence_after();
             mma4_bf16_cg2_w(acc, a_d + (uint64_t)(kc * (C::A_CHUNK >> 4)), desc_sw128(sW + st * C::CHUNK), ID, 1u);
             if (!next_shares) mma_commit_cg2_mc_w(b_wempty + 8 * st, 0x3);
@@ -288,8 +382,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc4Shape<H>::THREADS
           if (!next_shares) mma_commit_cg2_mc_w(b_bempty + 8 * bst, 0x3);
           if (++bst == 2) { bst = 0; bph ^= 1u; }
         } else {
+          if (tr) T4TR(jc, 2);
           tc_fence_after();
-          mma_bf16_cg2_w(acc, desc_nosw(sOnes, 128, 256), desc_nosw(sB + own_bst * C::BIAS_BYTES, 128, 256), ID, 0u);
+          mma_bf16_cg2_w(acc, desc_nosw(sA1 + s * C::A1_BYTES, 128, 256), desc_nosw(sB + own_bst * C::BIAS_BYTES, 128, 256),
+                         ID, 0u);
           int cs = own_st;
 #pragma unroll 1
           for (int kc = 0; kc < C::KC; ++kc) {
@@ -300,8 +396,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc4Shape<H>::THREADS
           mma_commit_cg2_mc_w(b_bempty + 8 * own_bst, 0x3);
         }
         mma_commit_cg2_mc_w(b_accfull + 8 * s, 0x3);
+        if (tr) T4TR(jc, 3);
       } else {
-        if (share) return;
+        if (share) { ++jc; return; }
         mbar_wait(b_bfull + 8 * bst, bph);
         if (lane == 0) mbar_arrive_remote(peer_bpeer + 8 * bst);
         __syncwarp();
@@ -313,6 +410,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc4Shape<H>::THREADS
           if (++st == nst) { st = 0; ph ^= 1u; }
         }
       }
+      ++jc;
     };
 #pragma unroll 1
     while (!(w0.done && w1.done)) {
@@ -331,11 +429,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc4Shape<H>::THREADS
         w1.advance(tstride, T, s_tile_end, L);
       }
     }
-  } else if (warp == 2) {
-    // =========================== IO warp (same protocol as tmlp_tc2.cu): every global access of the tile rows.
-    // At a tile's layer-1 job it waits until the layer-1 MMA consumed the slot's A1 buffer and refills it with
-    // the slot's next tile (gathered one tile earlier); at a tile's last job it waits for the team's row sums
-    // and stores sdf[perm[row]].
+    if (SAND_T4_PROF) {
+      pc[3] = T4CLK() - tl0;
+      if (warp == 1 && rank == 0 && lane == 0)
+        for (int k = 0; k < 4; ++k) g_t4prof[blockIdx.x][8 + k] = pc[k];
+      if (warp == 0) g_t4prof[blockIdx.x][12] = pc[4];
+    }
+  } else if (warp == 2 || warp == 3) {
+    // =========================== IO warps, one per tile slot (warp 2: slot 0, warp 3: slot 1): every global
+    // access of the slot's tile rows.  At a tile's layer-1 job the warp waits until the layer-1 MMA consumed the
+    // slot's A1 buffer and refills it with the slot's next tile (gathered one tile earlier); at a tile's last
+    // job it waits for the team's row sums and stores sdf[perm[row]].  One warp per slot: a slot's next layer-1
+    // operand never waits behind the other slot's tile end.
+    const int s = warp - 2;
     const uint32_t a1full_dst = rank == 0 ? b_a1full : mapa_shared(b_a1full, 0);
     const float* tcs = tab + p.m.pt_off_csum;
     auto load_perm = [&](long long t, uint32_t (&ix)[4]) {
@@ -378,35 +484,47 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc4Shape<H>::THREADS
         else mbar_arrive_remote(a1full_dst + 8 * s);
       }
     };
-    struct IoSlot { uint32_t cur[4], nxt[4], pre[4]; float nx[4], ny[4], nz[4]; };
-    Walk4 w0, w1;
-    w0.start(pair, T, s_tile_end, L);
-    w1.start(pair + npairs, T, s_tile_end, L);
-    IoSlot q0, q1;
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      IoSlot& q = s ? q1 : q0;
+    // perm rows of tiles t (cur), t+S (p1), t+2S (p2), t+3S (p3; S = this slot's tile stride); the points of the
+    // next tile to fill (px/py/pz) are gathered one whole tile ahead of their use
+    uint32_t cur[4], p1[4], p2[4], p3[4];
+    float px[4], py[4], pz[4];
+    Walk4 w;
+    w.start(pair + (long long)npairs * s, T, s_tile_end, L);
+    {
       const long long t0 = pair + (long long)npairs * s;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) q.cur[k] = q.nxt[k] = q.pre[k] = 0xFFFFFFFFu;
+      for (int k = 0; k < 4; ++k) cur[k] = p1[k] = p2[k] = p3[k] = 0xFFFFFFFFu;
       if (t0 < T) {
-        load_perm(t0, q.cur);
-        gather(q.cur, q.nx, q.ny, q.nz);
-        fill(s, q.nx, q.ny, q.nz);
+        load_perm(t0, cur);
+        gather(cur, px, py, pz);
+        fill(s, px, py, pz);
       }
-      if (t0 + tstride < T) { load_perm(t0 + tstride, q.nxt); gather(q.nxt, q.nx, q.ny, q.nz); }
+      if (t0 + tstride < T) { load_perm(t0 + tstride, p1); gather(p1, px, py, pz); }
+      if (t0 + 2 * tstride < T) load_perm(t0 + 2 * tstride, p2);
     }
-    auto io_step = [&](const Walk4& w, int s, IoSlot& q) {
+    unsigned long long io_w[2] = {0, 0};
+    const bool iotr = SAND_T4_TRACE && s == 0 && lane == 0;
+    auto io_step = [&]() {
       if (w.l == 1) {
         const long long t1 = w.t + tstride;
+        if (iotr) T4IO(w.ti, 0);
         if (t1 < T) {
-          mbar_wait_lazy(b_a1free + 8 * s, (uint32_t)(w.ti & 1));
-          fill(s, q.nx, q.ny, q.nz);
-          if (t1 + tstride < T) load_perm(t1 + tstride, q.pre);
+          const long long c0 = T4CLK();
+          mbar_wait(b_a1free + 8 * s, (uint32_t)(w.ti & 1));   // this tile's layer-1 MMA has read A1
+          if (iotr) T4IO(w.ti, 1);
+          if (SAND_T4_PROF) io_w[0] += T4CLK() - c0;
+          fill(s, px, py, pz);                                  // next tile's points (gathered a tile ago)
+          if (t1 + tstride < T) gather(p2, px, py, pz);         // the tile after: in flight for a whole tile
+          if (t1 + 2 * tstride < T) load_perm(t1 + 2 * tstride, p3);
         }
+        if (iotr) T4IO(w.ti, 2);
       }
       if (w.l == w.d) {
-        mbar_wait_lazy(b_iodone + 8 * s, (uint32_t)(w.ti & 1));
+        const long long c0 = T4CLK();
+        if (iotr) T4IO(w.ti, 3);
+        mbar_wait(b_iodone + 8 * s, (uint32_t)(w.ti & 1));
+        if (iotr) T4IO(w.ti, 4);
+        if (SAND_T4_PROF) io_w[1] += T4CLK() - c0;
         const float* pl = part + s * C::NCG * 128;
         const float cs = tcs[w.d];
         float y[4];
@@ -419,54 +537,67 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc4Shape<H>::THREADS
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(b_partfree + 8 * s);
+        if (iotr) T4IO(w.ti, 5);
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          if (q.cur[k] != 0xFFFFFFFFu) p.out[q.cur[k]] = y[k];
-        __syncwarp();
+          if (cur[k] != 0xFFFFFFFFu) p.out[cur[k]] = y[k];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) { q.cur[k] = q.nxt[k]; q.nxt[k] = q.pre[k]; }
-        if (w.t + 2 * tstride < T) gather(q.nxt, q.nx, q.ny, q.nz);
+        for (int k = 0; k < 4; ++k) { cur[k] = p1[k]; p1[k] = p2[k]; p2[k] = p3[k]; }
+        if (iotr) T4IO(w.ti, 6);
       }
     };
 #pragma unroll 1
-    while (!(w0.done && w1.done)) {
-      if (!w0.done) { io_step(w0, 0, q0); w0.advance(tstride, T, s_tile_end, L); }
-      if (!w1.done) { io_step(w1, 1, q1); w1.advance(tstride, T, s_tile_end, L); }
+    while (!w.done) {
+      io_step();
+      w.advance(tstride, T, s_tile_end, L);
     }
+    if (SAND_T4_PROF && s == 0 && lane == 0) { g_t4prof[blockIdx.x][13] = io_w[0]; g_t4prof[blockIdx.x][14] = io_w[1]; }
   } else if (warp >= C::NCTL) {
-    // =========================== epilogue team s: one thread per row, CW columns per thread
+    // =========================== epilogue: one thread per row (TMEM lane), CW columns per thread.  Ping-pong:
+    // all warps serve slot 0 and slot 1 step by step (the MMA of one slot overlaps the epilogue of the other);
+    // teams: warps [TEAM_WARPS s, TEAM_WARPS (s + 1)) serve slot s only.
     const int ew = warp - C::NCTL;
-    const int s = ew / C::TEAM_WARPS;            // slot served by this team
     const int q = warp & 3;                      // TMEM lane quadrant
-    const int cg = (ew % C::TEAM_WARPS) >> 2;    // column group within the team
+    const int cg = (ew % C::TEAM_WARPS) >> 2;    // column group
     const int row = 32 * q + lane;               // this CTA's tile row
     const int c0 = cg * C::CW;
-    const uint32_t tm = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(s * H + c0);
+    const uint32_t tm0 = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)c0;
     // A operand row segment: element (row, k) of K-chunk kc at kc * 16 KB + (row/8) 1024 + (row%8) 128 +
     // (((k%64)/8) ^ (row%8)) 16 + (k%8) 2
-    const uint32_t a_row = sA + s * C::A_BYTES + (uint32_t)(row >> 3) * 1024 + (uint32_t)(row & 7) * 128;
+    const uint32_t a_row0 = sA + (uint32_t)(row >> 3) * 1024 + (uint32_t)(row & 7) * 128;
     const uint32_t rx = (uint32_t)(row & 7);
     const uint32_t tab_a = sTab + (uint32_t)p.m.pt_off_a * 4 + (uint32_t)c0 * 4;
     const uint32_t tab_a1 = sTab + (uint32_t)p.m.pt_off_a1 * 4 + (uint32_t)c0 * 4;
     const float* tc0 = tab + p.m.pt_off_c;
     const float* tc1 = tab + p.m.pt_off_c1;
     const uint32_t afull_dst = rank == 0 ? b_afull : mapa_shared(b_afull, 0);
-    Walk4 w;
-    w.start(pair + (long long)npairs * s, T, s_tile_end, L);
-    uint32_t pe = 0;
-    float ylin = 0.f, yprod = 0.f;
-    float* my_part = part + (s * C::NCG + cg) * 128 + row;
+    struct EState {
+      Walk4 w;
+      uint32_t pe;
+      float ylin, yprod;
+    };
+    unsigned long long tp[4] = {0, 0, 0, 0};   // SAND_T4_PROF: wait_acc, busy, tile_end, steps
+    const long long tt0 = T4CLK();
 
     // one 32-column batch at column offset cb (relative to c0) of layer l: sines, tail dot products, A stores
-    auto batch = [&](const uint32_t (&r)[32], const int cb, const uint32_t ta, const uint32_t ta1, float2 (&y0)[2],
-                     float2 (&y1)[2], auto st_c) {
+    auto batch = [&](const uint32_t (&r)[32], const int cb, const uint32_t a_row, const uint32_t ta, const uint32_t ta1,
+                     float2 (&y0)[2], float2 (&y1)[2], auto st_c) {
       constexpr bool ST = decltype(st_c)::value;
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
         float hv[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) hv[i] = sin_mufu(__uint_as_float(r[8 * g + i]));
-#if SAND_T4_ABL != 4
+        for (int i = 0; i < 8; i += 2) {
+          if (4 * g + i / 2 < SAND_T4_NPOLY) {
+            const float2 hh = sin_poly2(make_float2(__uint_as_float(r[8 * g + i]), __uint_as_float(r[8 * g + i + 1])));
+            hv[i] = hh.x;
+            hv[i + 1] = hh.y;
+          } else {
+            hv[i] = sin_mufu(__uint_as_float(r[8 * g + i]));
+            hv[i + 1] = sin_mufu(__uint_as_float(r[8 * g + i + 1]));
+          }
+        }
+#if !(SAND_T4_ABL & 8)
         const float4 aa = lds128f(ta + (uint32_t)(cb + 8 * g) * 4);
         const float4 ab = lds128f(ta + (uint32_t)(cb + 8 * g + 4) * 4);
         y0[0] = __ffma2_rn(make_float2(aa.x, aa.y), make_float2(hv[0], hv[1]), y0[0]);
@@ -485,20 +616,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc4Shape<H>::THREADS
         if (ST) {
           const uint32_t k = (uint32_t)(c0 + cb + 8 * g);   // first column of this 8-column unit
           const uint32_t addr = a_row + (k >> 6) * C::A_CHUNK + ((((k & 63) >> 3) ^ rx) << 4);
-#if SAND_T4_ABL == 2
+#if SAND_T4_ABL & 2
           if (hv[0] == 1234.5f)
 #endif
-          sts128(addr, pack_bf16x2(hv[0], hv[1]), pack_bf16x2(hv[2], hv[3]), pack_bf16x2(hv[4], hv[5]),
-                 pack_bf16x2(hv[6], hv[7]));
+          sts128(addr, pack_h(hv[0], hv[1]), pack_h(hv[2], hv[3]), pack_h(hv[4], hv[5]), pack_h(hv[6], hv[7]));
         }
       }
     };
 
-#pragma unroll 1
-    while (!w.done) {
-      const int l = w.l, d = w.d;
-      mbar_wait(b_accfull + 8 * s, pe);
-      pe ^= 1u;
+    // one step (layer l of the slot's current tile)
+    int ec = 0;   // step counter (trace)
+    const bool etr = SAND_T4_TRACE && ew == 0 && lane == 0;
+    auto step = [&](EState& e, const int s) {
+      const int l = e.w.l, d = e.w.d;
+      if (etr) T4TR(ec, 4);
+      const uint32_t tm = tm0 + (uint32_t)(s * H);
+      const uint32_t a_row = a_row0 + (uint32_t)(s * C::A_BYTES);
+      const long long c0 = T4CLK();
+      mbar_wait(b_accfull + 8 * s, e.pe);
+      const long long c1 = T4CLK();
+      if (etr) T4TR(ec, 5);
+      e.pe ^= 1u;
       tc_fence_after();
       const bool prod = TAIL == SAND_TAIL_MULT && l >= 2;
       const uint32_t ta = tab_a + (uint32_t)((l - 1) * H) * 4;
@@ -507,7 +645,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc4Shape<H>::THREADS
       float2 y1[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
       auto run = [&](auto st_c) {
         uint32_t ra[32], rb[32];
-#if SAND_T4_ABL == 3
+#if SAND_T4_ABL & 4
 #pragma unroll
         for (int i = 0; i < 32; ++i) { ra[i] = __float_as_uint(0.01f * (i + lane)); rb[i] = ra[i] ^ 1u; }
 #else
@@ -515,17 +653,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc4Shape<H>::THREADS
 #endif
 #pragma unroll 1
         for (int b = 0; b < C::NB; b += 2) {
-#if SAND_T4_ABL != 3
+#if !(SAND_T4_ABL & 4)
           tmem_wait_ld_dep(ra);
           if (b + 1 < C::NB) tmem_ld32(tm + (uint32_t)(32 * (b + 1)), rb);
 #endif
-          batch(ra, 32 * b, ta, ta1, y0, y1, st_c);
+          batch(ra, 32 * b, a_row, ta, ta1, y0, y1, st_c);
           if (b + 1 < C::NB) {
-#if SAND_T4_ABL != 3
+#if !(SAND_T4_ABL & 4)
             tmem_wait_ld_dep(rb);
             if (b + 2 < C::NB) tmem_ld32(tm + (uint32_t)(32 * (b + 2)), ra);
 #endif
-            batch(rb, 32 * (b + 1), ta, ta1, y0, y1, st_c);
+            batch(rb, 32 * (b + 1), a_row, ta, ta1, y0, y1, st_c);
           }
         }
       };
@@ -541,23 +679,55 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc4Shape<H>::THREADS
         if (rank == 0) mbar_arrive(afull_dst + 8 * s);
         else mbar_arrive_remote(afull_dst + 8 * s);
       }
+      if (etr) T4TR(ec, 6);
       const float dot0 = (y0[0].x + y0[0].y) + (y0[1].x + y0[1].y);
       if (prod) {
         const float dot1 = (y1[0].x + y1[0].y) + (y1[1].x + y1[1].y);
-        if (C::NCG == 1) yprod += (tc0[l - 1] + dot0) * (tc1[l - 1] + dot1);
+        if (C::NCG == 1) e.yprod += (tc0[l - 1] + dot0) * (tc1[l - 1] + dot1);
       } else {
-        ylin += dot0;
+        e.ylin += dot0;
       }
+      const long long c2 = T4CLK();
+      if (SAND_T4_PROF) { tp[0] += c1 - c0; tp[1] += c2 - c1; tp[3] += 1; }
       if (l == d) {
         // tile end: hand this row's sum to the IO warp (which adds the tail-bias prefix sum csum[d])
-        mbar_wait(b_partfree + 8 * s, (uint32_t)((w.ti & 1) ^ 1));
-        *my_part = ylin + yprod;
-        ylin = 0.f;
-        yprod = 0.f;
+        mbar_wait(b_partfree + 8 * s, (uint32_t)((e.w.ti & 1) ^ 1));
+        if (etr && s == 0) T4IO(e.w.ti, 7);
+        part[(s * C::NCG + cg) * 128 + row] = e.ylin + e.yprod;
+        e.ylin = 0.f;
+        e.yprod = 0.f;
         __syncwarp();
         if (lane == 0) mbar_arrive(b_iodone + 8 * s);
+        if (SAND_T4_PROF) tp[2] += T4CLK() - c2;
       }
-      w.advance(tstride, T, s_tile_end, L);
+      e.w.advance(tstride, T, s_tile_end, L);
+      if (etr) T4TR(ec, 7);
+      ++ec;
+    };
+    int s_team = 0;
+    if (PP) {
+      EState e0, e1;
+      e0.w.start(pair, T, s_tile_end, L);
+      e1.w.start(pair + npairs, T, s_tile_end, L);
+      e0.pe = e1.pe = 0;
+      e0.ylin = e0.yprod = e1.ylin = e1.yprod = 0.f;
+#pragma unroll 1
+      while (!(e0.w.done && e1.w.done)) {
+        if (!e0.w.done) step(e0, 0);
+        if (!e1.w.done) step(e1, 1);
+      }
+    } else {
+      s_team = ew / C::TEAM_WARPS;
+      EState e;
+      e.w.start(pair + (long long)npairs * s_team, T, s_tile_end, L);
+      e.pe = 0;
+      e.ylin = e.yprod = 0.f;
+#pragma unroll 1
+      while (!e.w.done) step(e, s_team);
+    }
+    if (SAND_T4_PROF && q == 0 && cg == 0 && lane == 0) {
+      for (int k = 0; k < 4; ++k) g_t4prof[blockIdx.x][4 * s_team + k] = tp[k];
+      if (s_team == 0) g_t4prof[blockIdx.x][15] = T4CLK() - tt0;
     }
   }
   tc_fence_before();
@@ -568,22 +738,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc4Shape<H>::THREADS
 }
 
 // ------------------------------------------------------------------------------------ host side
-template <int H>
+template <int H, int TAIL>
 static size_t smem_for4(long long pt_floats, int L, int nst) {
-  using C = Tc4Shape<H>;
+  using C = Tc4Shape<H, tc4_pp<H, TAIL>()>;
   const size_t tab_bytes = (size_t)((pt_floats + 3) & ~3ll) * 4;
-  return (size_t)2 * C::A_BYTES + (size_t)nst * C::CHUNK + 2 * C::BIAS_BYTES + C::ONES_BYTES + C::W1_BYTES +
+  return (size_t)2 * C::A_BYTES + (size_t)nst * C::CHUNK + 2 * C::BIAS_BYTES + C::W1_BYTES +
          2 * C::A1_BYTES + tab_bytes + (size_t)2 * C::NCG * 128 * 4 + 4 * (size_t)(L + 2) * sizeof(long long) +
          (3 * nst + 6 + 12) * 8 + 16;
 }
 
 static constexpr size_t kSmemMax4 = 232448;
 
-template <int H>
+template <int H, int TAIL>
 static int pick_nst4(long long pt_floats, int L) {
   int best = 0;
   for (int nst = 2; nst <= 8; ++nst)
-    if (smem_for4<H>(pt_floats, L, nst) <= kSmemMax4) best = nst;
+    if (smem_for4<H, TAIL>(pt_floats, L, nst) <= kSmemMax4) best = nst;
   return best;
 }
 
@@ -596,10 +766,11 @@ bool tc4_usable(int L, int H, int tail) {
   if (!tc4_available(H, tail)) return false;
   MlpDev m{};
   tc2_table_layout(L, H, tail, &m, false);
+  const bool mult = tail == SAND_TAIL_MULT;
   switch (H) {
-    case 64: return pick_nst4<64>(m.pt_floats, L) > 0;
-    case 128: return pick_nst4<128>(m.pt_floats, L) > 0;
-    case 256: return pick_nst4<256>(m.pt_floats, L) > 0;
+    case 64: return (mult ? pick_nst4<64, 1>(m.pt_floats, L) : pick_nst4<64, 0>(m.pt_floats, L)) > 0;
+    case 128: return (mult ? pick_nst4<128, 1>(m.pt_floats, L) : pick_nst4<128, 0>(m.pt_floats, L)) > 0;
+    case 256: return (mult ? pick_nst4<256, 1>(m.pt_floats, L) : pick_nst4<256, 0>(m.pt_floats, L)) > 0;
     default: return false;
   }
 }
@@ -623,7 +794,8 @@ static inline void bf16_split4(float v, uint16_t* hi, uint16_t* lo) {
 // n % (H/2) of CTA n / (H/2) (cta_group::2 takes an instruction's first N/2 B rows from the even CTA).
 //   w1img : [2 CTAs][H/2 rows][16 bf16] (l1_off layout): (W_hi x y z | W_lo x y z | W_hi x y z | b_hi b_lo | 0)
 //           of w0 W_1, w0 b_1 against the IO warp's A row (x_hi | x_hi | x_lo | 1 1 | 0)
-//   img   : [L-1 layers][2 CTAs] runs of [bias operand: H/2 rows x 16 bf16, (w0 b_hi, w0 b_lo) at k = 0, 1]
+//   img   : [L-1 layers][2 CTAs] runs of [bias operand: H/2 rows x 16 bf16, (w0 b_hi, w0 b_lo) at k = 9, 10, the
+//           columns where the layer-1 A operand (the bias MMA's A) holds 1, 1]
 //           [KC K-chunks of bf16(w0 W_l): H/2 rows x 128 B, SW128 K-major]
 void tc4_build_host(int L, int H, float w0, const float* const* W, const float* const* b, std::vector<uint16_t>* w1img,
                     std::vector<uint8_t>* img) {
@@ -652,8 +824,8 @@ void tc4_build_host(int L, int H, float w0, const float* const* W, const float* 
       uint8_t* run = img->data() + ((size_t)(i - 1) * 2 + cta) * layer;
       uint16_t bhi, blo;
       bf16_split4(w0 * b[i][n], &bhi, &blo);
-      std::memcpy(run + l1_off((uint32_t)r, 0), &bhi, 2);
-      std::memcpy(run + l1_off((uint32_t)r, 1), &blo, 2);
+      std::memcpy(run + l1_off((uint32_t)r, 9), &bhi, 2);
+      std::memcpy(run + l1_off((uint32_t)r, 10), &blo, 2);
       for (int k = 0; k < H; ++k) {
         const int kc = k / 64, kk = k % 64;
         const size_t byte = bias_bytes + kc * chunk + (size_t)(r / 8) * 1024 + (r % 8) * 128 +
@@ -667,13 +839,44 @@ void tc4_build_host(int L, int H, float w0, const float* const* W, const float* 
 template <int H, int TAIL>
 static cudaError_t launch_tc4_t(const MlpDev& m, const float* pts, const uint32_t* perm, const QueryMeta* meta,
                                 float* out, int num_sms, cudaStream_t st) {
-  const int nst = pick_nst4<H>(m.pt_floats, m.L);
+  const int nst = pick_nst4<H, TAIL>(m.pt_floats, m.L);
   if (!nst) return cudaErrorInvalidConfiguration;
-  const size_t sm = smem_for4<H>(m.pt_floats, m.L, nst);
+  const size_t sm = smem_for4<H, TAIL>(m.pt_floats, m.L, nst);
   Tc4Params p{m, pts, perm, meta, out, nst};
   const int grid = num_sms & ~1;
-  k_tmlp_tc4<H, TAIL><<<grid, Tc4Shape<H>::THREADS, sm, st>>>(p);
-  return cudaGetLastError();
+  k_tmlp_tc4<H, TAIL><<<grid, Tc4Shape<H, tc4_pp<H, TAIL>()>::THREADS, sm, st>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (SAND_T4_TRACE && e == cudaSuccess) {
+    static long long tr[kT4Trace][8];
+    e = cudaStreamSynchronize(st);
+    for (int which = 0; which < 2 && e == cudaSuccess; ++which) {
+      e = which ? cudaMemcpyFromSymbol(tr, g_t4iotr, sizeof tr) : cudaMemcpyFromSymbol(tr, g_t4trace, sizeof tr);
+      FILE* f = e == cudaSuccess ? fopen(which ? "gpurun_out/t4iotrace.txt" : "gpurun_out/t4trace.txt", "w") : nullptr;
+      if (f) {
+        for (int j = 0; j < kT4Trace; ++j)
+          fprintf(f, "%lld %lld %lld %lld %lld %lld %lld %lld\n", tr[j][0], tr[j][1], tr[j][2], tr[j][3], tr[j][4], tr[j][5],
+                  tr[j][6], tr[j][7]);
+        fclose(f);
+      }
+    }
+  }
+  if (SAND_T4_PROF && e == cudaSuccess) {
+    // diagnostic build only: synchronous dump of the per-role counters (CTA averages; MMA over leaders)
+    static unsigned long long h[160][kT4Prof];
+    e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) e = cudaMemcpyFromSymbol(h, g_t4prof, sizeof h);
+    if (e == cudaSuccess) {
+      double a[kT4Prof] = {0};
+      for (int b = 0; b < grid; ++b)
+        for (int k = 0; k < kT4Prof; ++k) a[k] += (double)h[b][k] / ((k >= 8 && k <= 11) ? grid / 2 : grid);
+      fprintf(stderr,
+              "[t4prof] nst %d | team0: loop %.0f wait_acc %.0f busy %.0f tile_end %.0f steps %.0f | team1: wait_acc %.0f "
+              "busy %.0f tile_end %.0f steps %.0f | MMA: loop %.0f wait_afull %.0f wait_a1full %.0f wait_w %.0f | "
+              "producer wait_empty %.0f | IO0: wait_a1free %.0f wait_iodone %.0f\n",
+              nst, a[15], a[0], a[1], a[2], a[3], a[4], a[5], a[6], a[7], a[11], a[8], a[9], a[10], a[12], a[13], a[14]);
+    }
+  }
+  return e;
 }
 
 template <int H, int TAIL>
