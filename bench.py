@@ -197,14 +197,21 @@ def _sine_roofline(per_depth, H, ms_mlp, clocks):
             "peak_source": "derived: 148 SM x 16 MUFU.SIN / clk x median SM clock (DESIGN.md, K3 per-SM budget)"}
 
 
-def _padding_waste(per_depth, H, fp32):
+def _padding_waste(per_depth, H, fp32, even_bins=False):
     """Fraction of the H x H tensor FLOPs K3 executes that pad: ragged last tile per depth bucket (256-row
-    pair tiles, 128-row otherwise) and, for H = 336, the width padded to 352 (zero weights)."""
+    pair tiles, 128-row otherwise), with even_bins (the slot-team kernel) every bucket rounded up to an even
+    tile count, and, for H = 336, the width padded to 352 (zero weights)."""
     T = 128 if fp32 else 256
     HP = (H + 31) // 32 * 32 if H > 256 and not fp32 else H
+
+    def tiles(c):
+        t = -(-c // T)
+        return t + (t & 1) if even_bins else t
+
     alg = sum(c * (d - 1) * 2.0 * H * H for d, c in enumerate(per_depth) if d >= 1)
-    ex = sum(-(-c // T) * T * (d - 1) * 2.0 * HP * HP for d, c in enumerate(per_depth) if d >= 1)
-    return {"tile_rows": T, "padded_width": HP, "executed_flops": ex, "waste_frac": 1.0 - alg / ex if ex else 0.0}
+    ex = sum(tiles(c) * T * (d - 1) * 2.0 * HP * HP for d, c in enumerate(per_depth) if d >= 1)
+    return {"tile_rows": T, "padded_width": HP, "even_bins": bool(even_bins), "executed_flops": ex,
+            "waste_frac": 1.0 - alg / ex if ex else 0.0}
 
 
 def _cores():
@@ -833,7 +840,8 @@ def run_query(args):
             "tensor_frac_step": f_exec / (ms_step / 1e3) / 1e12 / pk["bf16"],
             "tensor_frac_ns_formula": f_ns / (ms_step / 1e3) / 1e12 / pk["bf16"],
             "flops_exec_per_step": f_exec, "flops_ns_per_step": f_ns,
-            "padding_waste": _padding_waste(st["per_depth"], H, fp32),
+            "padding_waste": _padding_waste(st["per_depth"], H, fp32, even_bins=pair_mode == 2 and not fp32 and not x3
+                                            and H in (64, 128, 256)),
             "stage_ms": {"lookup": ms_lookup, "bin": ms_bin, "mlp": ms_mlp},
             "per_depth": per_depth,
             "full_depth_speedup": full,

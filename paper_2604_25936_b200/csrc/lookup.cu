@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_partial(const uint32_t* _
   if (threadIdx.x == 0) part[(long long)bin * nchunk + c] = tot;
 }
 
-__global__ void k_scan_top(const unsigned long long* __restrict__ part, int nchunk, int L, int tile_rows,
+__global__ void k_scan_top(const unsigned long long* __restrict__ part, int nchunk, int L, int tile_rows, int even_bins,
                            unsigned long long* __restrict__ cpre, QueryMeta* __restrict__ meta) {
   if (threadIdx.x != 0) return;
   long long counts[kMaxBins];
@@ -215,7 +215,9 @@ __global__ void k_scan_top(const unsigned long long* __restrict__ part, int nchu
       running += (long long)part[(long long)d * nchunk + c];
     }
     meta->tile_begin[d] = tb;
-    tb += (counts[d] + tile_rows - 1) / tile_rows;
+    long long nt = (counts[d] + tile_rows - 1) / tile_rows;
+    if (even_bins) nt += nt & 1;   // tile pairs never straddle a depth bin (slot-team kernel: tile 2u + s -> slot s)
+    tb += nt;
     meta->tile_end[d] = tb;
   }
   meta->total_tiles = tb;
@@ -350,13 +352,13 @@ long long scan_scratch_words(long long nblk) {
   return 2 * (long long)kMaxBins * (nchunk > 0 ? nchunk : 1);
 }
 
-cudaError_t launch_scan(const uint32_t* hist, long long nblk, int L, int tile_rows, uint32_t* offs,
+cudaError_t launch_scan(const uint32_t* hist, long long nblk, int L, int tile_rows, int even_bins, uint32_t* offs,
                         QueryMeta* meta, unsigned long long* scratch, cudaStream_t st) {
   const int nchunk = (int)((nblk + kScanChunk - 1) / kScanChunk);
   unsigned long long* part = scratch;
   unsigned long long* cpre = scratch + (long long)kMaxBins * nchunk;
   k_scan_partial<<<dim3(nchunk, L + 2), kScanThreads, 0, st>>>(hist, nblk, part, nchunk);
-  k_scan_top<<<1, 32, 0, st>>>(part, nchunk, L, tile_rows, cpre, meta);
+  k_scan_top<<<1, 32, 0, st>>>(part, nchunk, L, tile_rows, even_bins, cpre, meta);
   k_scan_offs<<<dim3(nchunk, L), kScanThreads, 0, st>>>(hist, nblk, cpre, nchunk, offs);
   return cudaGetLastError();
 }

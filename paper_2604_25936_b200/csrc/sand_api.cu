@@ -628,7 +628,8 @@ extern "C" int sand_query(sand_ctx* ctx, const float* d_points, int64_t n, float
   CU(cudaEventRecord(ev[1], st));
   {
     NvtxRange r("K2 binning (scan + scatter)");
-    CU(launch_scan(ctx->d_hist, nblk, ctx->cfg.L, tmlp_tile_rows(ctx->cfg.H, ctx->cfg.prec, ctx->use_pair), ctx->d_offs,
+    CU(launch_scan(ctx->d_hist, nblk, ctx->cfg.L, tmlp_tile_rows(ctx->cfg.H, ctx->cfg.prec, ctx->use_pair),
+                   tc4_runs(ctx->cfg.L, ctx->cfg.H, ctx->cfg.tail, ctx->cfg.prec, ctx->use_pair) ? 1 : 0, ctx->d_offs,
                    ctx->d_meta, ctx->d_scan, st));
     CU(launch_scatter(d_depth, n, ctx->cfg.L, ctx->d_offs, ctx->d_perm, nblk, st));
   }

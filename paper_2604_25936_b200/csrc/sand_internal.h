@@ -42,7 +42,9 @@ struct LookupParams {
 // Host-side launchers (lookup.cu)
 cudaError_t launch_lookup(const float* pts, long long n, const LookupParams& lp, uint8_t* out_depth,
                           float* out_sdf, uint32_t* hist, long long nblk, cudaStream_t st);
-cudaError_t launch_scan(const uint32_t* hist, long long nblk, int L, int tile_rows, uint32_t* offs,
+// even_bins: round every depth bin up to an even number of tiles (empty padding tiles), so consecutive tile pairs
+// (2u, 2u + 1) always share a depth (the slot-team kernel runs them side by side in its two slots)
+cudaError_t launch_scan(const uint32_t* hist, long long nblk, int L, int tile_rows, int even_bins, uint32_t* offs,
                         QueryMeta* meta, unsigned long long* scratch, cudaStream_t st);
 long long scan_scratch_words(long long nblk);   // u64 words of scratch launch_scan needs
 cudaError_t launch_scatter(const uint8_t* depth, long long n, int L, const uint32_t* offs, uint32_t* perm,
@@ -137,6 +139,7 @@ cudaError_t prepare_tc2(int H, int tail);
 // Slot-team CTA-pair kernel (tmlp_tc4.cu): one N = H MMA chain per layer, one epilogue team per tile slot
 bool tc4_available(int H, int tail);
 bool tc4_usable(int L, int H, int tail);
+bool tc4_runs(int L, int H, int tail, int prec, int pair_mode);   // launch_tmlp_tc would pick the slot-team kernel
 void tc4_build_host(int L, int H, float w0, const float* const* W, const float* const* b, std::vector<uint16_t>* w1img,
                     std::vector<uint8_t>* img);
 cudaError_t launch_tmlp_tc4(const MlpDev& m, const float* pts, const uint32_t* perm, const QueryMeta* meta,

@@ -325,7 +325,7 @@ int tmlp_tile_rows(int H, int prec, int pair_mode) {
 
 cudaError_t launch_tmlp_tc(const MlpDev& m, const float* pts, const uint32_t* perm, const QueryMeta* meta,
                            float* out, int num_sms, cudaStream_t st, int pair_mode) {
-  if (pair_mode == 2 && m.tc4_w1 && tc4_usable(m.L, m.H, m.tail))
+  if (pair_mode == 2 && m.tc4_w1 && tc4_runs(m.L, m.H, m.tail, SAND_BF16, pair_mode))
     return launch_tmlp_tc4(m, pts, perm, meta, out, num_sms, st);
   if (pair_mode && tc2_available(m.H)) return launch_tmlp_tc2(m, pts, perm, meta, out, num_sms, st);
   if (pair_mode && tc3_available(m.H, m.tail)) return launch_tmlp_tc3(m, pts, perm, meta, out, num_sms, st);

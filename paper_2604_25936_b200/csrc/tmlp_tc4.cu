@@ -118,8 +118,10 @@ __device__ __forceinline__ int tile_depth4(long long t, const long long* te, int
   return 0;
 }
 
-// Per-slot walk over this pair's tiles: tile i of slot s is pair + npairs (2 i + s); each tile yields jobs
-// l = 1..d.
+// Per-slot walk over this pair's tiles: tile i of slot s is 2 (pair + npairs i) + s -- the pair takes tile pairs
+// (2u, 2u + 1), one tile per slot, and the scan pads every depth bin to an even tile count (launch_scan even_bins),
+// so both slots always run tiles of the same depth in step and the same layer back to back (weight sharing);
+// each tile yields jobs l = 1..d.
 struct Walk4 {
   long long t;
   int d, l, ti;
@@ -297,8 +299,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc4Shape<H, tc4_pp<H
     // "sharer": it loads nothing and runs on the previous ("owner") job's bias + chunk stages, and it is the one
     // that releases them (its commits fire after both jobs' MMAs).  Every role derives the same decision.
     Walk4 w0, w1;
-    w0.start(pair, T, s_tile_end, L);
-    w1.start(pair + npairs, T, s_tile_end, L);
+    w0.start(2ll * pair, T, s_tile_end, L);
+    w1.start(2ll * pair + 1, T, s_tile_end, L);
     const uint8_t* img = reinterpret_cast<const uint8_t*>(p.m.tc4_image) + (size_t)rank * C::LAYER_BYTES;
     const uint32_t peer_wpeer = mapa_shared(b_wpeer, 0);
     const uint32_t peer_bpeer = mapa_shared(b_bpeer, 0);
@@ -489,9 +491,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc4Shape<H, tc4_pp<H
     uint32_t cur[4], p1[4], p2[4], p3[4];
     float px[4], py[4], pz[4];
     Walk4 w;
-    w.start(pair + (long long)npairs * s, T, s_tile_end, L);
+    w.start(2ll * pair + s, T, s_tile_end, L);
     {
-      const long long t0 = pair + (long long)npairs * s;
+      const long long t0 = 2ll * pair + s;
 #pragma unroll
       for (int k = 0; k < 4; ++k) cur[k] = p1[k] = p2[k] = p3[k] = 0xFFFFFFFFu;
       if (t0 < T) {
@@ -707,8 +709,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc4Shape<H, tc4_pp<H
     int s_team = 0;
     if (PP) {
       EState e0, e1;
-      e0.w.start(pair, T, s_tile_end, L);
-      e1.w.start(pair + npairs, T, s_tile_end, L);
+      e0.w.start(2ll * pair, T, s_tile_end, L);
+      e1.w.start(2ll * pair + 1, T, s_tile_end, L);
       e0.pe = e1.pe = 0;
       e0.ylin = e0.yprod = e1.ylin = e1.yprod = 0.f;
 #pragma unroll 1
@@ -719,7 +721,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc4Shape<H, tc4_pp<H
     } else {
       s_team = ew / C::TEAM_WARPS;
       EState e;
-      e.w.start(pair + (long long)npairs * s_team, T, s_tile_end, L);
+      e.w.start(2ll * pair + s_team, T, s_tile_end, L);
       e.pe = 0;
       e.ylin = e.yprod = 0.f;
 #pragma unroll 1
@@ -760,6 +762,10 @@ static int pick_nst4(long long pt_floats, int L) {
 bool tc4_available(int H, int tail) {
   // Eq. 3 products need both full dot products of a row in one thread
   return (H == 64 || H == 128 || H == 256) && (tail == SAND_TAIL_LINEAR || SAND_T4_NCG == 1);
+}
+
+bool tc4_runs(int L, int H, int tail, int prec, int pair_mode) {
+  return prec == SAND_BF16 && pair_mode == 2 && tc4_usable(L, H, tail);
 }
 
 bool tc4_usable(int L, int H, int tail) {

@@ -164,14 +164,13 @@ int main() {
     }
     (void)mode;
   };
-  run(k<1 | 2 | 4 | 8 | 16 | 32>, "full intpack pipelined", 0);
-  run(k<1 | 2 | 4 | 8 | 16 | 32 | (2 << 8)>, "  + poly 2/16", 0);
-  run(k<1 | 2 | 4 | 8 | 16 | 32 | (3 << 8)>, "  + poly 3/16", 0);
-  run(k<1 | 2 | 4 | 8 | 16 | 32 | (4 << 8)>, "  + poly 4/16", 0);
-  run(k<1 | 2 | 4 | 8 | 16 | 32 | (5 << 8)>, "  + poly 5/16", 0);
-  run(k<1 | 2 | 4 | 8 | 16 | 32 | (6 << 8)>, "  + poly 6/16", 0);
-  run(k<1 | 2 | 4 | 8 | 16 | 32 | (4 << 8) | 4096>, "  + poly 4/16 deg9", 0);
-  run(k<1 | 2 | 4 | 8 | 32 | (4 << 8)>, "  + poly 4/16 unpipelined", 0);
-  run(k<1 | 2 | 4 | 8 | 32 | (2 << 8)>, "  + poly 2/16 unpipelined", 0);
+  run(k<1 | 2 | 4 | 8 | 32 | (2 << 8)>, "poly2 int: full", 0);
+  run(k<1 | 2 | 4 | 8 | 32 | (4 << 8)>, "poly4 int: full", 0);
+  run(k<1 | 2 | 4 | 8 | 32 | (6 << 8)>, "poly6 int: full", 0);
+  run(k<1 | 2 | 4 | 8 | (2 << 8)>, "poly2 f2fp: full", 0);
+  run(k<1 | 2 | 4 | 8 | (4 << 8)>, "poly4 f2fp: full", 0);
+  run(k<1 | 2 | 4 | 8 | (6 << 8)>, "poly6 f2fp: full", 0);
+  run(k<1 | 2 | 4 | 8 | (8 << 8)>, "poly8 f2fp: full", 0);
+  run(k<1 | 2 | 4 | 8 | 64 | (4 << 8)>, "poly4 f16pack: full", 0);
   return 0;
 }

@@ -26,6 +26,10 @@ def test_padding_waste_hand_counts():
     w = bench._padding_waste([0, 0, 129], 336, True)
     assert (w["tile_rows"], w["padded_width"]) == (128, 336)
     assert w["waste_frac"] == pytest.approx(1 - 129 / 256)
+    # slot-team kernel: every depth bucket padded to an even number of 256-row tiles (3 tiles -> 4, 2 stay 2)
+    w = bench._padding_waste([0, 0, 3 * 256, 2 * 256], 256, False, even_bins=True)
+    assert w["executed_flops"] == 4 * 256 * 2.0 * 256 * 256 + 2 * 256 * 2 * 2.0 * 256 * 256
+    assert w["waste_frac"] == pytest.approx(1 - (3 * 1 + 2 * 2) / (4 * 1 + 2 * 2))
 
 
 def test_sine_roofline_counts_every_evaluated_layer():
