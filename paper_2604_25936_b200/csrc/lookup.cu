@@ -27,21 +27,21 @@ struct LookupResult {
   float far;
 };
 
+// KIND (compile time): 0 dense map without cached SDF, 1 dense with cached SDF, 2 octree descent.  Branch-free
+// for the common finite case: the clamp in cell_of maps NaN / Inf to a valid boundary cell, and the non-finite
+// decision is a select after the lookup.
+template <int KIND>
 __device__ __forceinline__ LookupResult lookup_one(float x, float y, float z, const LookupParams& lp,
                                                    float scale, float maxc) {
   LookupResult r;
-  if (!(isfinite(x) && isfinite(y) && isfinite(z))) {
-    r.d = SAND_DEPTH_NONFINITE;
-    r.far = __int_as_float(0x7fc00000);
-    return r;
-  }
+  const bool fin = isfinite(x) && isfinite(y) && isfinite(z);
   const uint32_t cx = cell_of(x, scale, maxc), cy = cell_of(y, scale, maxc), cz = cell_of(z, scale, maxc);
   uint32_t d;
   float far = 0.0f;
-  if (lp.dense) {
+  if (KIND < 2) {
     const uint64_t lin = (uint64_t)cx + ((uint64_t)cy << lp.level) + ((uint64_t)cz << (2 * lp.level));
     d = __ldg(lp.grid + lin);
-    if (d == 0 && lp.grid_far) far = __ldg(lp.grid_far + lin);
+    if (KIND == 1 && d == 0) far = __ldg(lp.grid_far + lin);
   } else {
     uint32_t node = 0, v;
     int bit = lp.level - 1;
@@ -66,11 +66,12 @@ __device__ __forceinline__ LookupResult lookup_one(float x, float y, float z, co
     if (d == 0 && lp.leaf_far) far = __ldg(lp.leaf_far + leaf);
   }
   if (d > (uint32_t)lp.cap) d = (uint32_t)lp.cap;  // d >= 1 only: cap >= 1 leaves 0 untouched
-  r.d = d;
-  r.far = far;
+  r.d = fin ? d : (uint32_t)SAND_DEPTH_NONFINITE;
+  r.far = fin ? far : __int_as_float(0x7fc00000);
   return r;
 }
 
+template <int KIND>
 __global__ void __launch_bounds__(kLookupThreads) k_lookup(const float* __restrict__ pts, long long n,
                                                             LookupParams lp, uint8_t* __restrict__ out_depth,
                                                             float* __restrict__ out_sdf,
@@ -112,7 +113,7 @@ __global__ void __launch_bounds__(kLookupThreads) k_lookup(const float* __restri
     int nfar = 0;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const LookupResult r = lookup_one(px[j], py[j], pz[j], lp, scale, maxc);
+      const LookupResult r = lookup_one<KIND>(px[j], py[j], pz[j], lp, scale, maxc);
       dw |= (r.d & 0xFFu) << (8 * j);
       bins[j] = (j < cnt) ? (r.d == SAND_DEPTH_NONFINITE ? lp.L + 1 : (int)r.d) : -1;
       far[j] = r.far;
@@ -134,11 +135,18 @@ __global__ void __launch_bounds__(kLookupThreads) k_lookup(const float* __restri
     } else {
       for (int j = 0; j < cnt; ++j) out_depth[p0 + j] = (uint8_t)(dw >> (8 * j));
     }
-    // warp-aggregated shared-memory histogram
+    // warp-aggregated shared-memory histogram; fast path when each thread's 4 points share one bin (grid-ordered
+    // queries: neighbouring points mostly have one depth)
+    const bool same = bins[1] == bins[0] && bins[2] == bins[0] && bins[3] == bins[0];
+    if (__all_sync(0xffffffffu, same)) {
+      const unsigned m = __match_any_sync(0xffffffffu, bins[0]);
+      if (bins[0] >= 0 && lane == (__ffs(m) - 1)) atomicAdd(&sh[bins[0]], 4u * (uint32_t)__popc(m));
+    } else {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const unsigned m = __match_any_sync(0xffffffffu, bins[j]);
-      if (bins[j] >= 0 && lane == (__ffs(m) - 1)) atomicAdd(&sh[bins[j]], (uint32_t)__popc(m));
+      for (int j = 0; j < 4; ++j) {
+        const unsigned m = __match_any_sync(0xffffffffu, bins[j]);
+        if (bins[j] >= 0 && lane == (__ffs(m) - 1)) atomicAdd(&sh[bins[j]], (uint32_t)__popc(m));
+      }
     }
   }
   __syncthreads();
@@ -268,16 +276,30 @@ __global__ void __launch_bounds__(kLookupThreads) k_scatter(const uint8_t* __res
     const long long pt = p0 + 32 * r;
     key[r] = pt < n ? __ldcs(depth + pt) : 0u;
   }
+  bool one = true;   // all 512 points of this warp at one depth (grid-ordered queries: the common case)
+  uint32_t d0 = key[0];
+  if (d0 < 1 || d0 > (uint32_t)L) d0 = 0;
 #pragma unroll
-  for (int r = 0; r < kRounds; ++r) {
-    uint32_t d = key[r];
-    if (d < 1 || d > (uint32_t)L) d = 0;   // far, non-finite or padding: not binned
-    const unsigned m = __match_any_sync(0xffffffffu, d);
-    const uint32_t before = wcnt[warp][d];
-    __syncwarp();
-    if (lane == __ffs(m) - 1) wcnt[warp][d] = before + (uint32_t)__popc(m);
-    __syncwarp();
-    key[r] = (d << 16) | (before + (uint32_t)__popc(m & lt));
+  for (int r = 1; r < kRounds; ++r) one &= (key[r] == d0) || (d0 == 0 && (key[r] < 1 || key[r] > (uint32_t)L));
+  const uint32_t dl0 = __shfl_sync(0xffffffffu, d0, 0);   // every lane executes the shuffle (no short-circuit)
+  one = __all_sync(0xffffffffu, one && dl0 == d0);
+  if (one) {
+    // rank of point 32 r + lane = 32 r + lane (round-major, lane order: the stable order)
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r) key[r] = (d0 << 16) | (uint32_t)(32 * r + lane);
+    if (lane == 0) wcnt[warp][d0] = 32u * kRounds;
+  } else {
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r) {
+      uint32_t d = key[r];
+      if (d < 1 || d > (uint32_t)L) d = 0;   // far, non-finite or padding: not binned
+      const unsigned m = __match_any_sync(0xffffffffu, d);
+      const uint32_t before = wcnt[warp][d];
+      __syncwarp();
+      if (lane == __ffs(m) - 1) wcnt[warp][d] = before + (uint32_t)__popc(m);
+      __syncwarp();
+      key[r] = (d << 16) | (before + (uint32_t)__popc(m & lt));
+    }
   }
   __syncthreads();
   // warp bases: base[w][d] = offs[d][block] + sum of warps < w (in place over wcnt)
@@ -342,8 +364,15 @@ cudaError_t launch_lookup(const float* pts, long long n, const LookupParams& lp,
   const int vec_in = ((reinterpret_cast<uintptr_t>(pts) & 15) == 0) ? 1 : 0;
   const int vec_out = ((reinterpret_cast<uintptr_t>(out_depth) & 3) == 0) ? 1 : 0;
   const int vec_sdf = ((reinterpret_cast<uintptr_t>(out_sdf) & 15) == 0) ? 1 : 0;
-  k_lookup<<<(unsigned)nblk, kLookupThreads, 0, st>>>(pts, n, lp, out_depth, out_sdf, hist, nblk, vec_in,
-                                                      vec_out, vec_sdf);
+  if (lp.dense && lp.grid_far)
+    k_lookup<1><<<(unsigned)nblk, kLookupThreads, 0, st>>>(pts, n, lp, out_depth, out_sdf, hist, nblk, vec_in, vec_out,
+                                                           vec_sdf);
+  else if (lp.dense)
+    k_lookup<0><<<(unsigned)nblk, kLookupThreads, 0, st>>>(pts, n, lp, out_depth, out_sdf, hist, nblk, vec_in, vec_out,
+                                                           vec_sdf);
+  else
+    k_lookup<2><<<(unsigned)nblk, kLookupThreads, 0, st>>>(pts, n, lp, out_depth, out_sdf, hist, nblk, vec_in, vec_out,
+                                                           vec_sdf);
   return cudaGetLastError();
 }
 
