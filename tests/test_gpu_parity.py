@@ -337,6 +337,24 @@ def test_options_explicit_and_pair_kernel_switch():
         assert_parity(*res[mode], sdf_or, dep_or, TOL_BF16)
 
 
+@pytest.mark.parametrize("L", [1, 2, 3])
+@pytest.mark.parametrize("H", [64, 128, 256])
+def test_bf16_shallow_nets_team_kernel(L, H):
+    """The slot-team kernel (SAND_OPT_PAIR_KERNEL 2) at its protocol edges: L = 1 (no hidden layer: no weight image,
+    every job a layer-1 job), L = 2 (one hidden layer: every owner job followed by a sharer), L = 3; odd tile counts
+    per depth (the scan pads each bin to an even count of 256-row tiles) and a ragged last tile."""
+    from paper_2604_25936_b200 import SAND_OPT_PAIR_KERNEL
+    spec = g.TMlpSpec(L=L, H=H, omega0=30.0, tail=0, seed=120 + 7 * L + H)
+    p = g.make_weights(spec)
+    dm = _random_voxel_map(3, L, 121 + L)
+    pts = _pts(3 * 256 * L + 77, 122 + L)
+    sdf_or, dep_or = oracle_query(p, dm, pts)
+    with make_ctx(spec, BF16) as ctx:
+        assert ctx.sand_get_option(SAND_OPT_PAIR_KERNEL) == 2
+        sdf, dep = run_engine(ctx, p, dm, pts)
+    assert_parity(sdf, dep, sdf_or, dep_or, TOL_BF16)
+
+
 @pytest.mark.parametrize("H", [64, 128, 256])
 @pytest.mark.parametrize("tail", [0, 1])
 @pytest.mark.parametrize("mode", [1, 2])
