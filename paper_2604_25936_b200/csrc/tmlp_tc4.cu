@@ -57,7 +57,8 @@
 #define SAND_T4_TRACE 0   // 1: per-job clock64 timeline of CTA 0 (MMA issuer + epilogue warp 4), dumped by the host
 #endif
 #ifndef SAND_T4_ABL
-#define SAND_T4_ABL 0     // ablation bitmask, timing only (wrong results): 1 no sine, 2 no A stores, 4 no TMEM loads, 8 no tail
+#define SAND_T4_ABL 0     // ablation bitmask, timing only (wrong results): 1 no sine, 2 no A stores, 4 no TMEM loads, 8 no tail,
+                          // 16 no tail-vector loads
 #endif
 
 namespace sand {
@@ -163,11 +164,21 @@ __device__ __forceinline__ uint32_t pack_bf16x2_int(float lo, float hi) {
 #ifndef SAND_T4_NPOLY
 #define SAND_T4_NPOLY 3   // sine pairs per 16 (per 32-column batch) evaluated by the FMA-pipe polynomial instead of MUFU
 #endif
+#ifndef SAND_T4_NPOLY_LAST
+#define SAND_T4_NPOLY_LAST SAND_T4_NPOLY   // the share in a tile's last-layer steps (no A stores); 0-7 measured, 3 best
+#endif
 #ifndef SAND_T4_F2FP
 #define SAND_T4_F2FP 1    // 1: pack with cvt.rn.bf16x2.f32 (F2FP); 0: integer pack
 #endif
 __device__ __forceinline__ uint32_t pack_h(float lo, float hi) {
   return SAND_T4_F2FP ? pack_bf16x2(lo, hi) : pack_bf16x2_int(lo, hi);
+}
+#ifndef SAND_T4_IPACK
+#define SAND_T4_IPACK 0   // pairs (of the 4 in each 16-byte store) packed on the ALU instead of F2FP (1, 2 measured slower)
+#endif
+template <int J>
+__device__ __forceinline__ uint32_t pack_k(float lo, float hi) {
+  return J < SAND_T4_IPACK ? pack_bf16x2_int(lo, hi) : pack_h(lo, hi);
 }
 // Odd polynomial sine on the FMA pipe for two lanes at a time (shares the sine work with MUFU.SIN, which is the
 // epilogue's binding pipe): k = rint(z / 2 pi) by the 1.5 2^23 magic add fused into the scaling FMA, r = z - 2 pi k
@@ -601,7 +612,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc4Shape<H, tc4_pp<H
         float hv[8];
 #pragma unroll
         for (int i = 0; i < 8; i += 2) {
-          if (4 * g + i / 2 < SAND_T4_NPOLY) {
+          if (4 * g + i / 2 < (ST ? SAND_T4_NPOLY : SAND_T4_NPOLY_LAST)) {
             const float2 hh = sin_poly2(make_float2(__uint_as_float(r[8 * g + i]), __uint_as_float(r[8 * g + i + 1])));
             hv[i] = hh.x;
             hv[i + 1] = hh.y;
@@ -611,8 +622,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc4Shape<H, tc4_pp<H
           }
         }
 #if !(SAND_T4_ABL & 8)
+#if SAND_T4_ABL & 16
+        const float av = __uint_as_float((ta & 0xFFFFu) | 0x3c000000u);   // tail vectors not loaded (LDS cost probe)
+        const float4 aa = make_float4(av, av, av, av), ab = aa;
+#else
         const float4 aa = lds128f(ta + (uint32_t)(cb + 8 * g) * 4);
         const float4 ab = lds128f(ta + (uint32_t)(cb + 8 * g + 4) * 4);
+#endif
         y0[0] = __ffma2_rn(make_float2(aa.x, aa.y), make_float2(hv[0], hv[1]), y0[0]);
         y0[1] = __ffma2_rn(make_float2(aa.z, aa.w), make_float2(hv[2], hv[3]), y0[1]);
         y0[0] = __ffma2_rn(make_float2(ab.x, ab.y), make_float2(hv[4], hv[5]), y0[0]);
@@ -632,7 +648,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tc4Shape<H, tc4_pp<H
 #if SAND_T4_ABL & 2
           if (hv[0] == 1234.5f)
 #endif
-          sts128(addr, pack_h(hv[0], hv[1]), pack_h(hv[2], hv[3]), pack_h(hv[4], hv[5]), pack_h(hv[6], hv[7]));
+          sts128(addr, pack_k<0>(hv[0], hv[1]), pack_k<1>(hv[2], hv[3]), pack_k<2>(hv[4], hv[5]), pack_k<3>(hv[6], hv[7]));
         }
       }
     };
