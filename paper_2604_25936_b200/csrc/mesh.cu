@@ -9,9 +9,9 @@
 // segments chain into loops; each loop, started at its smallest edge id, becomes a triangle fan.
 //
 // k_marching_cubes: blocks walk cube rows; one thread per grid vertex column of a row (4 loads, the x + 1
-// corners from the next lane), tables in shared memory, warp scan + one atomicAdd per warp that meets
-// the surface, then the warp's triangles emitted one per lane from the staged cubes (output order is
-// therefore not deterministic; the triangle set is).  Vertices are interpolated from the edge's lower
+// corners from the next lane), tables in shared memory; surface cubes are queued per warp in shared memory
+// and emitted, one triangle per lane, when more than 32 are waiting (scan of the queue's triangle counts + one
+// atomicAdd per flush; output order is therefore not deterministic; the triangle set is).  Vertices are interpolated from the edge's lower
 // corner so both cubes sharing an edge produce the same bits.  Bound: HBM (4 B of sdf per
 // grid vertex + 36 B per triangle).
 #include <algorithm>
@@ -128,14 +128,18 @@ __global__ void k_grid_points(const float* __restrict__ axis, int R, int k0, int
 // A block walks cube rows (j, k) (grid-stride, no per-element index division); a thread is grid vertex
 // column i of the row: it loads the 4 values at x = i of the row's two y rows and two z planes and takes
 // the x = i + 1 values from the next lane (the last lane of a warp loads them itself), ~4 loads a cube.
+constexpr int MC_QC = 64;   // queue capacity per warp (cubes); flushed when a push of 32 might not fit
 __global__ void __launch_bounds__(256) k_marching_cubes(const float* __restrict__ sdf, int R, int kc0, int kc1,
                                                         int kp0, const float* __restrict__ axis,
                                                         float* __restrict__ tris, long long cap,
                                                         unsigned long long* __restrict__ counter) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int R1 = R - 1;
-  __shared__ float s_lo[8][4][32], s_hi[8][4][32];   // per warp: the lanes' cube corners, case, count scan
-  __shared__ int s_c[8][32], s_off[8][32];
+  // per warp: queue of surface cubes waiting for emission (8 corner values, i | j << 16, k | case << 24) and the
+  // inclusive scan of their triangle counts, filled at flush time
+  __shared__ float s_q[8][8][MC_QC];
+  __shared__ unsigned s_m0[8][MC_QC], s_m1[8][MC_QC];
+  __shared__ int s_off[8][MC_QC];
   const long long R2 = (long long)R * R;
   const long long nrows = (long long)R1 * (kc1 - kc0);
   __shared__ uint8_t s_tri[256][15];   // tables in shared memory: per-thread (divergent) indices
@@ -168,6 +172,57 @@ __global__ void __launch_bounds__(256) k_marching_cubes(const float* __restrict_
 #pragma unroll
     for (int u = 0; u < 4; ++u) x[u] = ext ? __ldg(rowp + i + 1 + (u >> 1) * R2 + (u & 1) * R) : 0.f;
   };
+  int qn = 0;   // queued cubes (warp-uniform)
+  auto flush = [&]() {
+    if (qn == 0) return;
+    __syncwarp();
+    // inclusive scan of the queued cubes' triangle counts (two entries per lane)
+    const int e0 = 2 * lane, e1 = 2 * lane + 1;
+    const int n0 = e0 < qn ? s_ntri[s_m1[warp][e0] >> 24] : 0;
+    const int n1 = e1 < qn ? s_ntri[s_m1[warp][e1] >> 24] : 0;
+    int off = n0 + n1;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, off, d);
+      if (lane >= d) off += y;
+    }
+    s_off[warp][e0] = off - n1;
+    s_off[warp][e1] = off;
+    const int T = __shfl_sync(0xffffffffu, off, 31);
+    unsigned long long wbase = 0;
+    if (lane == 31) wbase = atomicAdd(counter, (unsigned long long)T);
+    wbase = __shfl_sync(0xffffffffu, wbase, 31);
+    __syncwarp();
+    for (int idx = lane; idx < T; idx += 32) {
+      if ((long long)wbase + idx >= cap) break;
+      int L = 0;   // owner entry: the first L with inclusive count off[L] > idx
+#pragma unroll
+      for (int st = MC_QC / 2; st; st >>= 1)
+        if (s_off[warp][L + st - 1] <= idx) L += st;
+      const unsigned m0 = s_m0[warp][L], m1 = s_m1[warp][L];
+      const int cL = (int)(m1 >> 24);
+      const int t = idx - (s_off[warp][L] - s_ntri[cL]);
+      const int iL = (int)(m0 & 0xFFFFu), jL = (int)(m0 >> 16), kL = (int)(m1 & 0xFFFFFFu);
+      float plo[4], phi[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { plo[u] = s_q[warp][u][L]; phi[u] = s_q[warp][4 + u][L]; }
+      float* out = tris + 9 * ((long long)wbase + idx);
+#pragma unroll
+      for (int m = 0; m < 3; ++m) {
+        const int e = s_tri[cL][3 * t + m];
+        const int v0 = s_edge[e][0], v1 = s_edge[e][1];
+        const float a0 = corner(plo, phi, v0), a1 = corner(plo, phi, v1);
+        const float tt = a0 / (a0 - a1);
+        const float p0x = axis[iL + (v0 & 1)], p0y = axis[jL + ((v0 >> 1) & 1)], p0z = axis[kL + (v0 >> 2)];
+        const float p1x = axis[iL + (v1 & 1)], p1y = axis[jL + ((v1 >> 1) & 1)], p1z = axis[kL + (v1 >> 2)];
+        out[3 * m] = p0x + tt * (p1x - p0x);
+        out[3 * m + 1] = p0y + tt * (p1y - p0y);
+        out[3 * m + 2] = p0z + tt * (p1z - p0z);
+      }
+    }
+    __syncwarp();
+    qn = 0;
+  };
   float nv[4], nx[4];
   int nj = 0, nk = 0, ni = 0;
   if (blockIdx.x < nsg) load(blockIdx.x, nv, nx, nj, nk, ni);
@@ -195,53 +250,22 @@ __global__ void __launch_bounds__(256) k_marching_cubes(const float* __restrict_
         c |= (hi[u] < 0.f) << (v | 1);
       }
       const int nt = cube ? s_ntri[c] : 0;
-      if (!__any_sync(0xffffffffu, nt)) continue;   // most warps meet no surface
-      int off = nt;   // warp-inclusive scan of the triangle counts
+      const unsigned act = __ballot_sync(0xffffffffu, nt != 0);
+      if (!act) continue;   // most warps meet no surface
+      // queue the surface cubes (emitting per 32-cube segment would run the long emission path with the ~9
+      // triangles such a segment holds on average: ncu, 80 of the kernel's 137 M warp instructions)
+      if (nt) {
+        const int pos = qn + __popc(act & ((1u << lane) - 1u));
 #pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, off, d);
-        if (lane >= d) off += y;
+        for (int u = 0; u < 4; ++u) { s_q[warp][u][pos] = lo[u]; s_q[warp][4 + u][pos] = hi[u]; }
+        s_m0[warp][pos] = (unsigned)i | ((unsigned)j << 16);
+        s_m1[warp][pos] = (unsigned)k | ((unsigned)c << 24);
       }
-      const int T = __shfl_sync(0xffffffffu, off, 31);   // the warp's triangles
-      unsigned long long wbase = 0;
-      if (lane == 31) wbase = atomicAdd(counter, (unsigned long long)T);
-      wbase = __shfl_sync(0xffffffffu, wbase, 31);
-      // emit the warp's T triangles lane-parallel (triangle idx by lane idx % 32), not cube by cube: surface
-      // cubes are sparse along a row, so per-cube emission would run ~1 active lane per warp instruction
-#pragma unroll
-      for (int u = 0; u < 4; ++u) { s_lo[warp][u][lane] = lo[u]; s_hi[warp][u][lane] = hi[u]; }
-      s_c[warp][lane] = c;
-      s_off[warp][lane] = off;
-      __syncwarp();
-      for (int idx = lane; idx < T; idx += 32) {
-        if ((long long)wbase + idx >= cap) break;
-        int L = 0;   // owner lane: the first L with inclusive count off[L] > idx
-#pragma unroll
-        for (int st = 16; st; st >>= 1)
-          if (s_off[warp][L + st - 1] <= idx) L += st;
-        const int cL = s_c[warp][L];
-        const int t = idx - (s_off[warp][L] - s_ntri[cL]);
-        const int iL = i - lane + L;
-        float plo[4], phi[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) { plo[u] = s_lo[warp][u][L]; phi[u] = s_hi[warp][u][L]; }
-        float* out = tris + 9 * ((long long)wbase + idx);
-#pragma unroll
-        for (int m = 0; m < 3; ++m) {
-          const int e = s_tri[cL][3 * t + m];
-          const int v0 = s_edge[e][0], v1 = s_edge[e][1];
-          const float a0 = corner(plo, phi, v0), a1 = corner(plo, phi, v1);
-          const float tt = a0 / (a0 - a1);
-          const float p0x = axis[iL + (v0 & 1)], p0y = axis[j + ((v0 >> 1) & 1)], p0z = axis[k + (v0 >> 2)];
-          const float p1x = axis[iL + (v1 & 1)], p1y = axis[j + ((v1 >> 1) & 1)], p1z = axis[k + (v1 >> 2)];
-          out[3 * m] = p0x + tt * (p1x - p0x);
-          out[3 * m + 1] = p0y + tt * (p1y - p0y);
-          out[3 * m + 2] = p0z + tt * (p1z - p0z);
-        }
-      }
-      __syncwarp();
+      qn += __popc(act);
+      if (qn > MC_QC - 32) flush();
     }
   }
+  flush();
 }
 
 cudaError_t launch_grid_axis(int R, float* axis, cudaStream_t st) {
