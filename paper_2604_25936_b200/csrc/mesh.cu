@@ -160,11 +160,23 @@ __global__ void __launch_bounds__(256) k_marching_cubes(const float* __restrict_
   // current one is processed (its compute, counter atomic and emission hide their latency)
   const unsigned nseg = (unsigned)((R + 255) / 256);
   const unsigned nsg = (unsigned)nrows * nseg;
-  auto load = [&](unsigned sg, float (&v)[4], float (&x)[4], int& j, int& k, int& i) {
-    const unsigned row = sg / nseg;
-    j = (int)(row % (unsigned)R1);
-    k = kc0 + (int)(row / (unsigned)R1);
-    i = (int)(sg - row * nseg) * 256 + (int)threadIdx.x;
+  // position (segment in row, j, k) of the next segment to load, stepped by gridDim.x segments with carries (a
+  // division per segment cost a quarter of the kernel's instructions)
+  const unsigned dseg = gridDim.x % nseg, drow = gridDim.x / nseg;
+  const int dj = (int)(drow % (unsigned)R1), dk = (int)(drow / (unsigned)R1);
+  int pseg = (int)(blockIdx.x % nseg), pj = (int)((blockIdx.x / nseg) % (unsigned)R1),
+      pk = kc0 + (int)((blockIdx.x / nseg) / (unsigned)R1);
+  auto load = [&](float (&v)[4], float (&x)[4], int& j, int& k, int& i) {
+    j = pj;
+    k = pk;
+    i = pseg * 256 + (int)threadIdx.x;
+    pseg += (int)dseg;
+    const int cy = pseg >= (int)nseg;
+    pseg -= cy ? (int)nseg : 0;
+    pj += dj + cy;
+    const int cz = pj >= R1;
+    pj -= cz ? R1 : 0;
+    pk += dk + cz;
     const float* rowp = sdf + (long long)(k - kp0) * R2 + (long long)j * R;
     const bool inr = i < R, ext = inr && i + 1 < R && lane == 31;
 #pragma unroll
@@ -225,14 +237,14 @@ __global__ void __launch_bounds__(256) k_marching_cubes(const float* __restrict_
   };
   float nv[4], nx[4];
   int nj = 0, nk = 0, ni = 0;
-  if (blockIdx.x < nsg) load(blockIdx.x, nv, nx, nj, nk, ni);
+  if (blockIdx.x < nsg) load(nv, nx, nj, nk, ni);
   for (unsigned sg = blockIdx.x; sg < nsg; sg += gridDim.x) {
     {
       float lo[4], xx[4];   // x = i: (y, z) = (0,0) (1,0) (0,1) (1,1); lane 31 also x = i + 1
 #pragma unroll
       for (int u = 0; u < 4; ++u) { lo[u] = nv[u]; xx[u] = nx[u]; }
       const int j = nj, k = nk, i = ni;
-      if (sg + gridDim.x < nsg) load(sg + gridDim.x, nv, nx, nj, nk, ni);
+      if (sg + gridDim.x < nsg) load(nv, nx, nj, nk, ni);
       const bool inr = i < R;
       float hi[4];   // x = i + 1
 #pragma unroll
