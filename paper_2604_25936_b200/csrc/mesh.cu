@@ -8,10 +8,10 @@
 // crossing of the walk (diagonal inside corners of a face stay separated; face-local, so watertight);
 // segments chain into loops; each loop, started at its smallest edge id, becomes a triangle fan.
 //
-// k_marching_cubes: blocks walk cube rows; one thread per grid vertex column of a row (4 loads, the x + 1
-// corners from the next lane), tables in shared memory; surface cubes are queued per warp in shared memory
-// and emitted, one triangle per lane, when more than 32 are waiting (scan of the queue's triangle counts + one
-// atomicAdd per flush; output order is therefore not deterministic; the triangle set is).  Vertices are interpolated from the edge's lower
+// Two kernels (below): k_mc_signs packs the vertex signs into words, k_mc_emit finds the surface cubes with
+// word-wide bit operations, queues them per warp in shared memory and emits a full queue's triangles one per
+// lane (scan of the queue's triangle counts + one atomicAdd per flush; output order is therefore not
+// deterministic; the triangle set is).  Vertices are interpolated from the edge's lower
 // corner so both cubes sharing an edge produce the same bits.  Bound: HBM (4 B of sdf per
 // grid vertex + 36 B per triangle).
 #include <algorithm>
@@ -23,9 +23,10 @@
 
 namespace sand {
 
-__constant__ uint8_t c_mc_ntri[256];
-__constant__ uint8_t c_mc_tri[256][15];   // up to 5 triangles x 3 edge ids
-__constant__ uint8_t c_mc_edge[12][2];    // (lower corner, upper corner)
+// device-global (not __constant__): every block copies them to shared memory with coalesced word loads
+__device__ __align__(16) uint8_t c_mc_ntri[256];
+__device__ __align__(16) uint8_t c_mc_tri[256][15];   // up to 5 triangles x 3 edge ids
+__device__ __align__(16) uint8_t c_mc_edge[12][2];    // (lower corner, upper corner)
 
 static void mc_build_tables(uint8_t ntri[256], uint8_t tri[256][15], uint8_t edge[12][2]) {
   int ne = 0;
@@ -124,85 +125,107 @@ __global__ void k_grid_points(const float* __restrict__ axis, int R, int k0, int
   }
 }
 
-// Cubes (i, j, k), 0 <= i, j < R - 1, kc0 <= k < kc1, over an sdf buffer holding planes from kp0 on.
-// A block walks cube rows (j, k) (grid-stride, no per-element index division); a thread is grid vertex
-// column i of the row: it loads the 4 values at x = i of the row's two y rows and two z planes and takes
-// the x = i + 1 values from the next lane (the last lane of a warp loads them itself), ~4 loads a cube.
-constexpr int MC_QC = 64;   // queue capacity per warp (cubes); flushed when a push of 32 might not fit
-__global__ void __launch_bounds__(256) k_marching_cubes(const float* __restrict__ sdf, int R, int kc0, int kc1,
-                                                        int kp0, const float* __restrict__ axis,
-                                                        float* __restrict__ tris, long long cap,
-                                                        unsigned long long* __restrict__ counter) {
+// ---- marching cubes in two passes over an sdf buffer holding planes from kp0 on.
+//
+// Pass A (k_mc_signs): the sign of every grid vertex as a bit.  Row = (plane, y) line of R vertices; per group
+// of 128 vertices four words m_0..m_3, bit L of m_q = sdf(vertex 128 g + 4 L + q) < 0 -- the layout a lane
+// that loads 4 consecutive vertices (16 bytes) produces with four ballots.  HBM-bound: 4 B read per vertex.
+//
+// Pass B (k_mc_emit): a thread takes (group g, cube row j, plane k) = 128 cubes, finds the cubes that meet
+// the surface with word-wide bit operations on 4 rows' words (x + 1 is the next q, or the next lane bit for
+// q = 3), and queues them per warp in shared memory; a full queue is flushed: corner values gathered from
+// the sdf (2 queue entries per lane), scan of the triangle counts, one atomicAdd, triangles emitted one per
+// lane.  Only ~2.5% of the cubes of the 512^3 grid meet the surface, so pass B touches the sdf only there.
+constexpr int MC_QC = 64;   // queue capacity per warp (cubes)
+
+__global__ void __launch_bounds__(256) k_mc_signs(const float* __restrict__ sdf, int R, long long nrows, int G,
+                                                  uint32_t* __restrict__ signs, unsigned long long* __restrict__ taskctr) {
+  const int lane = threadIdx.x & 31;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *taskctr = 0ull;   // pass B's work queue (same stream, runs after this)
+  const bool al = (R & 3) == 0 && (reinterpret_cast<uintptr_t>(sdf) & 15) == 0;
+  const long long ngr = nrows * G;
+  const long long wstride = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long gi = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; gi < ngr; gi += wstride) {
+    const long long row = gi / G;
+    const int x = (int)(gi - row * G) * 128 + 4 * lane;
+    const float* rp = sdf + row * R + x;
+    float v[4];
+    if (al && x < R) {
+      const float4 t = __ldcs(reinterpret_cast<const float4*>(rp));
+      v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[q] = x + q < R ? __ldcs(rp + q) : 0.f;
+    }
+    uint32_t m[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) m[q] = __ballot_sync(0xffffffffu, v[q] < 0.f);
+    if (lane == 0) *reinterpret_cast<uint4*>(signs + 4 * gi) = make_uint4(m[0], m[1], m[2], m[3]);
+  }
+}
+
+__global__ void __launch_bounds__(256, 4) k_mc_emit(const float* __restrict__ sdf, const uint32_t* __restrict__ signs,
+                                                    int R, int kc0, int kc1, int kp0, const float* __restrict__ axis,
+                                                    float* __restrict__ tris, long long cap,
+                                                    unsigned long long* __restrict__ counter,
+                                                    unsigned long long* __restrict__ taskctr) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int R1 = R - 1;
-  // per warp: queue of surface cubes waiting for emission (8 corner values, i | j << 16, k | case << 24) and the
-  // inclusive scan of their triangle counts, filled at flush time
+  const int G = (R + 127) / 128;
+  const long long R2 = (long long)R * R;
+  // per warp: queue of surface cubes waiting for emission (x | j << 16, k | case << 24), their 8 corner values
+  // and the inclusive scan of their triangle counts, both filled at flush time
   __shared__ float s_q[8][8][MC_QC];
   __shared__ unsigned s_m0[8][MC_QC], s_m1[8][MC_QC];
   __shared__ int s_off[8][MC_QC];
-  const long long R2 = (long long)R * R;
-  const long long nrows = (long long)R1 * (kc1 - kc0);
-  __shared__ uint8_t s_tri[256][15];   // tables in shared memory: per-thread (divergent) indices
-  __shared__ uint8_t s_ntri[256];
-  __shared__ uint8_t s_edge[12][2];
-  for (int t = threadIdx.x; t < 256 * 15; t += blockDim.x) s_tri[t / 15][t % 15] = c_mc_tri[t / 15][t % 15];
-  for (int t = threadIdx.x; t < 256; t += blockDim.x) s_ntri[t] = c_mc_ntri[t];
-  if (threadIdx.x < 24) s_edge[threadIdx.x >> 1][threadIdx.x & 1] = c_mc_edge[threadIdx.x >> 1][threadIdx.x & 1];
+  __shared__ __align__(16) uint8_t s_tri[256][15];   // tables in shared memory: per-thread (divergent) indices
+  __shared__ __align__(16) uint8_t s_ntri[256];
+  __shared__ __align__(16) uint8_t s_edge[12][2];
+  for (int t = threadIdx.x; t < 256 * 15 / 4; t += blockDim.x)
+    reinterpret_cast<uint32_t*>(&s_tri[0][0])[t] = reinterpret_cast<const uint32_t*>(&c_mc_tri[0][0])[t];
+  if (threadIdx.x < 64) reinterpret_cast<uint32_t*>(s_ntri)[threadIdx.x] = reinterpret_cast<const uint32_t*>(c_mc_ntri)[threadIdx.x];
+  if (threadIdx.x < 6) reinterpret_cast<uint32_t*>(&s_edge[0][0])[threadIdx.x] = reinterpret_cast<const uint32_t*>(&c_mc_edge[0][0])[threadIdx.x];
   __syncthreads();
-  // corner value v of the current cube without dynamic register indexing
+  // corner value v of a cube without dynamic register indexing
   auto corner = [](const float (&lo)[4], const float (&hi)[4], int v) {
     const int u = ((v >> 1) & 1) | (((v >> 2) & 1) << 1);
     const float a = u == 0 ? lo[0] : u == 1 ? lo[1] : u == 2 ? lo[2] : lo[3];
     const float b = u == 0 ? hi[0] : u == 1 ? hi[1] : u == 2 ? hi[2] : hi[3];
     return (v & 1) ? b : a;
   };
-  // segments of 256 cube columns of a row, block-strided; the next segment's loads are issued before the
-  // current one is processed (its compute, counter atomic and emission hide their latency)
-  const unsigned nseg = (unsigned)((R + 255) / 256);
-  const unsigned nsg = (unsigned)nrows * nseg;
-  // position (segment in row, j, k) of the next segment to load, stepped by gridDim.x segments with carries (a
-  // division per segment cost a quarter of the kernel's instructions)
-  const unsigned dseg = gridDim.x % nseg, drow = gridDim.x / nseg;
-  const int dj = (int)(drow % (unsigned)R1), dk = (int)(drow / (unsigned)R1);
-  int pseg = (int)(blockIdx.x % nseg), pj = (int)((blockIdx.x / nseg) % (unsigned)R1),
-      pk = kc0 + (int)((blockIdx.x / nseg) / (unsigned)R1);
-  auto load = [&](float (&v)[4], float (&x)[4], int& j, int& k, int& i) {
-    j = pj;
-    k = pk;
-    i = pseg * 256 + (int)threadIdx.x;
-    pseg += (int)dseg;
-    const int cy = pseg >= (int)nseg;
-    pseg -= cy ? (int)nseg : 0;
-    pj += dj + cy;
-    const int cz = pj >= R1;
-    pj -= cz ? R1 : 0;
-    pk += dk + cz;
-    const float* rowp = sdf + (long long)(k - kp0) * R2 + (long long)j * R;
-    const bool inr = i < R, ext = inr && i + 1 < R && lane == 31;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = inr ? __ldg(rowp + i + (u >> 1) * R2 + (u & 1) * R) : 0.f;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) x[u] = ext ? __ldg(rowp + i + 1 + (u >> 1) * R2 + (u & 1) * R) : 0.f;
-  };
   int qn = 0;   // queued cubes (warp-uniform)
   auto flush = [&]() {
     if (qn == 0) return;
     __syncwarp();
-    // inclusive scan of the queued cubes' triangle counts (two entries per lane)
     const int e0 = 2 * lane, e1 = 2 * lane + 1;
-    const int n0 = e0 < qn ? s_ntri[s_m1[warp][e0] >> 24] : 0;
-    const int n1 = e1 < qn ? s_ntri[s_m1[warp][e1] >> 24] : 0;
-    int off = n0 + n1;
+    int n01[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) n01[h] = 2 * lane + h < qn ? s_ntri[s_m1[warp][2 * lane + h] >> 24] : 0;
+    int off = n01[0] + n01[1];
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       const int y = __shfl_up_sync(0xffffffffu, off, d);
       if (lane >= d) off += y;
     }
-    s_off[warp][e0] = off - n1;
+    s_off[warp][e0] = off - n01[1];
     s_off[warp][e1] = off;
     const int T = __shfl_sync(0xffffffffu, off, 31);
     unsigned long long wbase = 0;
-    if (lane == 31) wbase = atomicAdd(counter, (unsigned long long)T);
+    if (lane == 31) wbase = atomicAdd(counter, (unsigned long long)T);   // in flight under the corner gather
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {   // gather the corners of this lane's two entries
+      const int e = 2 * lane + h;
+      if (e < qn) {
+        const unsigned m0 = s_m0[warp][e], m1 = s_m1[warp][e];
+        const float* cp = sdf + (long long)((int)(m1 & 0xFFFFFFu) - kp0) * R2 + (long long)(m0 >> 16) * R + (m0 & 0xFFFFu);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {   // (y, z) = (u & 1, u >> 1)
+          const float* q = cp + (u >> 1) * R2 + (u & 1) * R;
+          s_q[warp][u][e] = __ldg(q);
+          s_q[warp][4 + u][e] = __ldg(q + 1);
+        }
+      }
+    }
     wbase = __shfl_sync(0xffffffffu, wbase, 31);
     __syncwarp();
     for (int idx = lane; idx < T; idx += 32) {
@@ -235,47 +258,75 @@ __global__ void __launch_bounds__(256) k_marching_cubes(const float* __restrict_
     __syncwarp();
     qn = 0;
   };
-  float nv[4], nx[4];
-  int nj = 0, nk = 0, ni = 0;
-  if (blockIdx.x < nsg) load(nv, nx, nj, nk, ni);
-  for (unsigned sg = blockIdx.x; sg < nsg; sg += gridDim.x) {
-    {
-      float lo[4], xx[4];   // x = i: (y, z) = (0,0) (1,0) (0,1) (1,1); lane 31 also x = i + 1
-#pragma unroll
-      for (int u = 0; u < 4; ++u) { lo[u] = nv[u]; xx[u] = nx[u]; }
-      const int j = nj, k = nk, i = ni;
-      if (sg + gridDim.x < nsg) load(nv, nx, nj, nk, ni);
-      const bool inr = i < R;
-      float hi[4];   // x = i + 1
-#pragma unroll
-      for (int u = 0; u < 4; ++u) hi[u] = __shfl_down_sync(0xffffffffu, lo[u], 1);
-      const bool cube = inr && i + 1 < R;
-      if (lane == 31) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) hi[u] = xx[u];
-      }
-      int c = 0;
+  // lane task = one sign word: 32 cubes x = 128 g + 4 L + q (L = bit) of cube row j, plane k; warp tasks of 32
+  // lane tasks are handed out by a global counter (surface-dense tasks run up to 16 flushes, empty ones none)
+  const long long ntask = 4ll * G * R1 * (kc1 - kc0);
+  const long long nwt = (ntask + 31) >> 5;
+  long long wt = 0;
+  if (lane == 0) wt = (long long)atomicAdd(taskctr, 1ull);
+  wt = __shfl_sync(0xffffffffu, wt, 0);
+  while (wt < nwt) {
+    long long nxt = 0;
+    if (lane == 0) nxt = (long long)atomicAdd(taskctr, 1ull);   // next task, fetched under this one
+    const long long t = wt * 32 + lane;
+    const bool valid = t < ntask;
+    const int q = (int)(t & 3);
+    const long long tg = valid ? t >> 2 : 0;
+    const int g = (int)(tg % G);
+    const long long rest = tg / G;
+    const int j = (int)(rest % R1), k = kc0 + (int)(rest / R1);
+    uint32_t a[4] = {}, b[4] = {};   // [row u = (y, z)]: vertices x (a) and x + 1 (b) as bit L
+    if (valid) {
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const int v = ((u & 1) << 1) | ((u >> 1) << 2);   // corner of (y, z) = (u & 1, u >> 1) at x = 0
-        c |= (lo[u] < 0.f) << v;
-        c |= (hi[u] < 0.f) << (v | 1);
+        const long long row = (long long)(k - kp0 + (u >> 1)) * R + (j + (u & 1));
+        const uint32_t* w = signs + 4 * (row * G + g);
+        a[u] = __ldg(w + q);
+        if (q < 3) b[u] = __ldg(w + q + 1);
+        else b[u] = (__ldg(w) >> 1) | ((g + 1 < G ? __ldg(w + 4) : 0u) << 31);
       }
-      const int nt = cube ? s_ntri[c] : 0;
-      const unsigned act = __ballot_sync(0xffffffffu, nt != 0);
-      if (!act) continue;   // most warps meet no surface
-      // queue the surface cubes (emitting per 32-cube segment would run the long emission path with the ~9
-      // triangles such a segment holds on average: ncu, 80 of the kernel's 137 M warp instructions)
-      if (nt) {
-        const int pos = qn + __popc(act & ((1u << lane) - 1u));
-#pragma unroll
-        for (int u = 0; u < 4; ++u) { s_q[warp][u][pos] = lo[u]; s_q[warp][4 + u][pos] = hi[u]; }
-        s_m0[warp][pos] = (unsigned)i | ((unsigned)j << 16);
-        s_m1[warp][pos] = (unsigned)k | ((unsigned)c << 24);
-      }
-      qn += __popc(act);
-      if (qn > MC_QC - 32) flush();
     }
+    uint32_t m = 0;   // cubes with a sign change among their 8 corners
+#pragma unroll
+    for (int u = 0; u < 4; ++u) m |= (a[u] ^ a[0]) | (b[u] ^ a[0]);
+    // cubes need x + 1 <= R - 1: x = 128 g + 4 L + q < R1  <=>  L < (R1 - 128 g - q + 3) / 4
+    const int nl = (R1 - 128 * g - q + 3) >> 2;
+    m &= nl >= 32 ? 0xFFFFFFFFu : (nl <= 0 ? 0u : ((1u << nl) - 1u));
+    if (!valid) m = 0;
+    while (__any_sync(0xffffffffu, m != 0)) {
+      const int cnt = __popc(m);
+      int off = cnt;   // inclusive scan of the lanes' pending cubes
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, off, d);
+        if (lane >= d) off += y;
+      }
+      // lanes whose cubes still fit form a prefix (off is monotone)
+      const bool fits = off <= MC_QC - qn;
+      const unsigned fm = __ballot_sync(0xffffffffu, fits);
+      const int nfit = __popc(fm);
+      const int pushed = nfit ? __shfl_sync(0xffffffffu, off, nfit - 1) : 0;
+      if (fits && m) {
+        int pos = qn + off - cnt;
+        while (m) {
+          const int L = __ffs(m) - 1;
+          m &= m - 1;
+          unsigned c = 0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int v = ((u & 1) << 1) | ((u >> 1) << 2);   // corner (0, y, z)
+            c |= ((a[u] >> L) & 1u) << v;
+            c |= ((b[u] >> L) & 1u) << (v | 1);
+          }
+          s_m0[warp][pos] = (unsigned)(128 * g + 4 * L + q) | ((unsigned)j << 16);
+          s_m1[warp][pos] = (unsigned)k | (c << 24);
+          ++pos;
+        }
+      }
+      qn += pushed;
+      if (__any_sync(0xffffffffu, m != 0)) flush();   // something did not fit
+    }
+    wt = __shfl_sync(0xffffffffu, nxt, 0);
   }
   flush();
 }
@@ -290,12 +341,25 @@ cudaError_t launch_grid_points(const float* axis, int R, int k0, int np, float* 
   return cudaGetLastError();
 }
 
+size_t mc_sign_words(int R, int planes) { return (size_t)4 * ((R + 127) / 128) * (size_t)R * (size_t)planes; }
+
+// signs: scratch of mc_sign_words(R, kc1 - kc0 + 1) uint32 (16-byte aligned)
 cudaError_t launch_marching_cubes(const float* sdf, int R, int kc0, int kc1, int kp0, const float* axis, float* tris,
-                                  long long cap, unsigned long long* counter, int num_sms, cudaStream_t st) {
-  const long long nrows = (long long)(R - 1) * (kc1 - kc0);
-  if (nrows <= 0) return cudaSuccess;
-  const long long blocks = std::min<long long>(nrows, (long long)num_sms * 8);
-  k_marching_cubes<<<(unsigned)blocks, 256, 0, st>>>(sdf, R, kc0, kc1, kp0, axis, tris, cap, counter);
+                                  long long cap, unsigned long long* counter, uint32_t* signs, int num_sms,
+                                  cudaStream_t st) {   // counter: 2 words (triangle count, pass B's task counter)
+  if (R < 2 || kc1 <= kc0) return cudaSuccess;
+  if (R > 65535) return cudaErrorInvalidValue;   // queue entries pack x and j into 16 bits each
+  const int G = (R + 127) / 128;
+  // planes kc0 .. kc1 of the buffer (it starts at plane kp0); their sign words are indexed from plane kp0 too
+  const long long row0 = (long long)(kc0 - kp0) * R, nrows = (long long)(kc1 - kc0 + 1) * R;
+  const long long ngr = nrows * G;
+  const long long ba = std::min<long long>((ngr + 7) / 8, (long long)num_sms * 16);
+  k_mc_signs<<<(unsigned)ba, 256, 0, st>>>(sdf + row0 * R, R, nrows, G, signs + 4 * row0 * G, counter + 1);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const long long nwt = (4ll * G * (R - 1) * (kc1 - kc0) + 31) / 32;
+  const long long bb = std::min<long long>((nwt + 7) / 8, (long long)num_sms * 4);
+  k_mc_emit<<<(unsigned)bb, 256, 0, st>>>(sdf, signs, R, kc0, kc1, kp0, axis, tris, cap, counter, counter + 1);
   return cudaGetLastError();
 }
 

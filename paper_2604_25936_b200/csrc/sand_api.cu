@@ -65,6 +65,8 @@ struct sand_ctx {
   uint8_t* d_mdep = nullptr;
   long long cap_m = 0;
   unsigned long long* d_tricount = nullptr;
+  uint32_t* d_msigns = nullptr;   // vertex sign words of the planes one marching-cubes launch covers
+  size_t cap_msigns = 0;
   float* d_dyn_h = nullptr;       // dynamic-exit activation scratch (per block, kDynPool x HP floats)
   MlpDev mlp{};
   // depth map
@@ -223,7 +225,7 @@ extern "C" int sand_destroy(sand_ctx* ctx) {
   free_hostpipe(ctx);
   dfree(ctx->d_dp_tmp);
   dfree(ctx->d_dyn_h);
-  dfree(ctx->d_axis); dfree(ctx->d_mpts); dfree(ctx->d_msdf); dfree(ctx->d_mdep); dfree(ctx->d_tricount);
+  dfree(ctx->d_axis); dfree(ctx->d_mpts); dfree(ctx->d_msdf); dfree(ctx->d_mdep); dfree(ctx->d_tricount); dfree(ctx->d_msigns);
   for (auto& q : ctx->evq)
     for (auto& v : q)
       if (v) cudaEventDestroy(v);
@@ -774,8 +776,16 @@ extern "C" int sand_debug_perm(sand_ctx* ctx, uint32_t* host_perm, int64_t cap, 
 }
 
 // ------------------------------------------------------------------------------- marching cubes
-static int mesh_prepare(sand_ctx* ctx, int R) {
+static int mesh_prepare(sand_ctx* ctx, int R, int planes) {
   CU(mc_upload_tables());
+  const size_t nw = mc_sign_words(R, planes);
+  if (nw > ctx->cap_msigns) {
+    CU(cudaStreamSynchronize(ctx->stream));
+    dfree(ctx->d_msigns);
+    ctx->cap_msigns = 0;
+    CU(cudaMalloc(&ctx->d_msigns, sizeof(uint32_t) * nw));
+    ctx->cap_msigns = nw;
+  }
   if (ctx->axis_R != R) {
     CU(cudaStreamSynchronize(ctx->stream));
     dfree(ctx->d_axis);
@@ -783,7 +793,7 @@ static int mesh_prepare(sand_ctx* ctx, int R) {
     ctx->axis_R = R;
     CU(launch_grid_axis(R, ctx->d_axis, ctx->stream));
   }
-  if (!ctx->d_tricount) CU(cudaMalloc(&ctx->d_tricount, sizeof(unsigned long long)));
+  if (!ctx->d_tricount) CU(cudaMalloc(&ctx->d_tricount, 2 * sizeof(unsigned long long)));   // + the MC task counter
   CU(cudaMemsetAsync(ctx->d_tricount, 0, sizeof(unsigned long long), ctx->stream));
   return SAND_OK;
 }
@@ -802,10 +812,10 @@ extern "C" int sand_marching_cubes(sand_ctx* ctx, const float* d_sdf, int R, flo
   if (R < 2 || cap < 0 || !n_tris || !d_sdf || (cap > 0 && !d_tris))
     return fail(ctx, SAND_ERR_ARG, "sand_marching_cubes: R < 2, cap < 0 or NULL argument");
   CU(cudaSetDevice(ctx->cfg.device));
-  int rc = mesh_prepare(ctx, R);
+  int rc = mesh_prepare(ctx, R, R);
   if (rc) return rc;
-  CU(launch_marching_cubes(d_sdf, R, 0, R - 1, 0, ctx->d_axis, d_tris, cap, ctx->d_tricount, ctx->num_sms,
-                           ctx->stream));
+  CU(launch_marching_cubes(d_sdf, R, 0, R - 1, 0, ctx->d_axis, d_tris, cap, ctx->d_tricount, ctx->d_msigns,
+                           ctx->num_sms, ctx->stream));
   return mesh_finish(ctx, n_tris);
 }
 
@@ -818,7 +828,7 @@ extern "C" int sand_mesh_grid(sand_ctx* ctx, int R, int slab, float* d_tris, int
   CU(cudaSetDevice(ctx->cfg.device));
   if (slab == 0) slab = 64;
   if (slab > R - 1) slab = R - 1;
-  int rc = mesh_prepare(ctx, R);
+  int rc = mesh_prepare(ctx, R, slab + 1);
   if (rc) return rc;
   const long long np = (long long)R * R * (slab + 1);   // points of the slab's slab + 1 planes
   if (np > ctx->cap_m) {
@@ -842,7 +852,7 @@ extern "C" int sand_mesh_grid(sand_ctx* ctx, int R, int slab, float* d_tris, int
     rc = sand_query(ctx, ctx->d_mpts, n, ctx->d_msdf + q0 * R2, ctx->d_mdep);
     if (rc) return rc;
     CU(launch_marching_cubes(ctx->d_msdf, R, kc0, kc1, kc0, ctx->d_axis, d_tris, cap, ctx->d_tricount,
-                             ctx->num_sms, ctx->stream));
+                             ctx->d_msigns, ctx->num_sms, ctx->stream));
   }
   return mesh_finish(ctx, n_tris);
 }

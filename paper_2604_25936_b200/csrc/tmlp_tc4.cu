@@ -902,6 +902,13 @@ static cudaError_t launch_tc4_t(const MlpDev& m, const float* pts, const uint32_
       double a[kT4Prof] = {0};
       for (int b = 0; b < grid; ++b)
         for (int k = 0; k < kT4Prof; ++k) a[k] += (double)h[b][k] / ((k >= 8 && k <= 11) ? grid / 2 : grid);
+      for (int r = 0; r < 2; ++r) {   // even (leader) and odd CTAs separately: the odd CTA's arrivals are remote
+        double q[kT4Prof] = {0};
+        for (int b = r; b < grid; b += 2)
+          for (int k = 0; k < kT4Prof; ++k) q[k] += (double)h[b][k] / (grid / 2);
+        fprintf(stderr, "[t4prof] rank %d team0: loop %.0f wait_acc %.0f busy %.0f tile_end %.0f | IO0: wait_a1free %.0f wait_iodone %.0f\n",
+                r, q[15], q[0], q[1], q[2], q[13], q[14]);
+      }
       fprintf(stderr,
               "[t4prof] nst %d | team0: loop %.0f wait_acc %.0f busy %.0f tile_end %.0f steps %.0f | team1: wait_acc %.0f "
               "busy %.0f tile_end %.0f steps %.0f | MMA: loop %.0f wait_afull %.0f wait_a1full %.0f wait_w %.0f | "
