@@ -136,7 +136,11 @@ __global__ void k_grid_points(const float* __restrict__ axis, int R, int k0, int
 // q = 3), and queues them per warp in shared memory; a full queue is flushed: corner values gathered from
 // the sdf (2 queue entries per lane), scan of the triangle counts, one atomicAdd, triangles emitted one per
 // lane.  Only ~2.5% of the cubes of the 512^3 grid meet the surface, so pass B touches the sdf only there.
-constexpr int MC_QC = 64;   // queue capacity per warp (cubes)
+#ifndef SAND_MC_QC
+#define SAND_MC_QC 128
+#endif
+constexpr int MC_QC = SAND_MC_QC;   // queue capacity per warp (cubes), a multiple of 32
+constexpr int MC_EPL = MC_QC / 32;  // queue entries per lane at flush time
 
 __global__ void __launch_bounds__(256) k_mc_signs(const float* __restrict__ sdf, int R, long long nrows, int G,
                                                   uint32_t* __restrict__ signs, unsigned long long* __restrict__ taskctr) {
@@ -177,7 +181,7 @@ __global__ void __launch_bounds__(256, 4) k_mc_emit(const float* __restrict__ sd
   // and the inclusive scan of their triangle counts, both filled at flush time
   __shared__ float s_q[8][8][MC_QC];
   __shared__ unsigned s_m0[8][MC_QC], s_m1[8][MC_QC];
-  __shared__ int s_off[8][MC_QC];
+  __shared__ unsigned short s_off[8][MC_QC];   // <= 5 MC_QC triangles
   __shared__ __align__(16) uint8_t s_tri[256][15];   // tables in shared memory: per-thread (divergent) indices
   __shared__ __align__(16) uint8_t s_ntri[256];
   __shared__ __align__(16) uint8_t s_edge[12][2];
@@ -197,24 +201,33 @@ __global__ void __launch_bounds__(256, 4) k_mc_emit(const float* __restrict__ sd
   auto flush = [&]() {
     if (qn == 0) return;
     __syncwarp();
-    const int e0 = 2 * lane, e1 = 2 * lane + 1;
-    int n01[2];
+    int nh[MC_EPL];   // triangle counts of this lane's entries MC_EPL lane + h
+    int off = 0;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) n01[h] = 2 * lane + h < qn ? s_ntri[s_m1[warp][2 * lane + h] >> 24] : 0;
-    int off = n01[0] + n01[1];
+    for (int h = 0; h < MC_EPL; ++h) {
+      nh[h] = MC_EPL * lane + h < qn ? s_ntri[s_m1[warp][MC_EPL * lane + h] >> 24] : 0;
+      off += nh[h];
+    }
+    const int mine = off;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       const int y = __shfl_up_sync(0xffffffffu, off, d);
       if (lane >= d) off += y;
     }
-    s_off[warp][e0] = off - n01[1];
-    s_off[warp][e1] = off;
+    {
+      int run = off - mine;   // inclusive scan over the queue entries
+#pragma unroll
+      for (int h = 0; h < MC_EPL; ++h) {
+        run += nh[h];
+        s_off[warp][MC_EPL * lane + h] = (unsigned short)run;
+      }
+    }
     const int T = __shfl_sync(0xffffffffu, off, 31);
     unsigned long long wbase = 0;
     if (lane == 31) wbase = atomicAdd(counter, (unsigned long long)T);   // in flight under the corner gather
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {   // gather the corners of this lane's two entries
-      const int e = 2 * lane + h;
+    for (int h = 0; h < MC_EPL; ++h) {   // gather the corners of this lane's entries
+      const int e = MC_EPL * lane + h;
       if (e < qn) {
         const unsigned m0 = s_m0[warp][e], m1 = s_m1[warp][e];
         const float* cp = sdf + (long long)((int)(m1 & 0xFFFFFFu) - kp0) * R2 + (long long)(m0 >> 16) * R + (m0 & 0xFFFFu);
