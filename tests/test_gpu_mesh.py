@@ -70,6 +70,23 @@ def test_marching_cubes_matches_oracle(shape, R):
     assert ok and V - E + F == {"sphere": 2, "torus": 0, "two": 4}[shape]
 
 
+@pytest.mark.parametrize("R", [131, 132])
+def test_marching_cubes_across_sign_word_groups(R):
+    """Grids wider than one 128-vertex sign-word group (csrc/mesh.cu): the surface crosses vertex columns 127 /
+    128 (the x + 1 neighbour of a group's last vertex lives in the next group's first word) and leaves the domain
+    through the x = +1 face (cubes end at column R - 2); R = 132 takes the 16-byte row loads, R = 131 the
+    unaligned path.  Triangle set against oracle.marching_cubes, as above."""
+    X, Y, Z = _grid(R)
+    sdf = (np.sqrt((X - 0.6) ** 2 + (Y + 0.1) ** 2 + (Z - 0.05) ** 2) - 0.45).astype(np.float32)
+    spec = g.TMlpSpec(L=2, H=64, omega0=30.0, seed=1)
+    with make_ctx(spec, 2) as ctx:
+        T = _gpu_mc(ctx, sdf.ravel(), R)
+    To = oracle.marching_cubes(sdf.ravel().astype(np.float64), R)
+    assert T.shape == To.shape and T.shape[0] > 10000
+    np.testing.assert_allclose(_canon(T), _canon(To), rtol=0, atol=2e-6)
+    assert T[:, :, 0].max() == 1.0   # the mesh reaches the domain face
+
+
 def test_capacity_and_empty():
     R = 21
     X, Y, Z = _grid(R)
