@@ -5,9 +5,10 @@ One step = one sand_query over the whole workload: K1 depth-map lookup -> K2 sca
 -> K3 fused T-MLP (tcgen05), i.e. every row of SURVEY.md Sec. 8(a), inputs resident in HBM.
 Default workload (N = 1) = BASELINE.json configs[2] ("C2"): 512^3 marching-cubes vertex grid
 (134,217,728 points), 8 x 256 SIREN T-MLP (seeded SIREN init, BF16 MMA),
-level-7 sphere-union octree.  N > 1 (torchrun, NCCL): weak scaling -- the grid is refined along z
-to 512 x 512 x 512N and cut into work-balanced z-slabs, one per rank; NCCL only all-gathers a small
-per-rank record (no data-path collective).
+level-7 sphere-union octree.  N > 1 (one rank per GPU, NCCL; `--gpus N` self-launches under
+torch.distributed.run): BASELINE.json configs[4] ("C4"), the fixed 1024^3 grid with the level-8 octree,
+strong-scaled -- cut into work-balanced z-slabs, one per rank (`--scaling weak` refines the grid along z
+instead); NCCL only all-gathers a small per-rank record after the timed region (no data-path collective).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl sand|reference]
 """
