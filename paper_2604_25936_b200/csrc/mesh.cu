@@ -136,9 +136,13 @@ __global__ void k_grid_points(const float* __restrict__ axis, int R, int k0, int
 // q = 3), and queues them per warp in shared memory; a full queue is flushed: corner values gathered from
 // the sdf (2 queue entries per lane), scan of the triangle counts, one atomicAdd, triangles emitted one per
 // lane.  Only ~2.5% of the cubes of the 512^3 grid meet the surface, so pass B touches the sdf only there.
+#ifndef SAND_MC_UNROLL
+#define SAND_MC_UNROLL 2   // emission iterations interleaved (the loop body is one long dependent chain)
+#endif
 #ifndef SAND_MC_QC
 #define SAND_MC_QC 64    // 128 measured 6-9% slower (47 KB of shared memory per block, 7-step owner search)
 #endif
+constexpr int MC_UNROLL = SAND_MC_UNROLL;
 constexpr int MC_QC = SAND_MC_QC;   // queue capacity per warp (cubes), a multiple of 32
 constexpr int MC_EPL = MC_QC / 32;  // queue entries per lane at flush time
 
@@ -190,13 +194,6 @@ __global__ void __launch_bounds__(256, 4) k_mc_emit(const float* __restrict__ sd
   if (threadIdx.x < 64) reinterpret_cast<uint32_t*>(s_ntri)[threadIdx.x] = reinterpret_cast<const uint32_t*>(c_mc_ntri)[threadIdx.x];
   if (threadIdx.x < 6) reinterpret_cast<uint32_t*>(&s_edge[0][0])[threadIdx.x] = reinterpret_cast<const uint32_t*>(&c_mc_edge[0][0])[threadIdx.x];
   __syncthreads();
-  // corner value v of a cube without dynamic register indexing
-  auto corner = [](const float (&lo)[4], const float (&hi)[4], int v) {
-    const int u = ((v >> 1) & 1) | (((v >> 2) & 1) << 1);
-    const float a = u == 0 ? lo[0] : u == 1 ? lo[1] : u == 2 ? lo[2] : lo[3];
-    const float b = u == 0 ? hi[0] : u == 1 ? hi[1] : u == 2 ? hi[2] : hi[3];
-    return (v & 1) ? b : a;
-  };
   int qn = 0;   // queued cubes (warp-uniform)
   auto flush = [&]() {
     if (qn == 0) return;
@@ -241,6 +238,7 @@ __global__ void __launch_bounds__(256, 4) k_mc_emit(const float* __restrict__ sd
     }
     wbase = __shfl_sync(0xffffffffu, wbase, 31);
     __syncwarp();
+#pragma unroll MC_UNROLL
     for (int idx = lane; idx < T; idx += 32) {
       if ((long long)wbase + idx >= cap) break;
       int L = 0;   // owner entry: the first L with inclusive count off[L] > idx
@@ -251,15 +249,13 @@ __global__ void __launch_bounds__(256, 4) k_mc_emit(const float* __restrict__ sd
       const int cL = (int)(m1 >> 24);
       const int t = idx - (s_off[warp][L] - s_ntri[cL]);
       const int iL = (int)(m0 & 0xFFFFu), jL = (int)(m0 >> 16), kL = (int)(m1 & 0xFFFFFFu);
-      float plo[4], phi[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) { plo[u] = s_q[warp][u][L]; phi[u] = s_q[warp][4 + u][L]; }
       float* out = tris + 9 * ((long long)wbase + idx);
 #pragma unroll
       for (int m = 0; m < 3; ++m) {
         const int e = s_tri[cL][3 * t + m];
         const int v0 = s_edge[e][0], v1 = s_edge[e][1];
-        const float a0 = corner(plo, phi, v0), a1 = corner(plo, phi, v1);
+        // corner v = x + 2 y + 4 z is queue row 4 x + (v >> 1)
+        const float a0 = s_q[warp][4 * (v0 & 1) + (v0 >> 1)][L], a1 = s_q[warp][4 * (v1 & 1) + (v1 >> 1)][L];
         const float tt = a0 / (a0 - a1);
         const float p0x = axis[iL + (v0 & 1)], p0y = axis[jL + ((v0 >> 1) & 1)], p0z = axis[kL + (v0 >> 2)];
         const float p1x = axis[iL + (v1 & 1)], p1y = axis[jL + ((v1 >> 1) & 1)], p1z = axis[kL + (v1 >> 2)];
