@@ -564,7 +564,7 @@ def run_mesh(args):
             "triangles": ntri, "triangles_unfused": n2,
             "unfused": {"ms_query": ms_query, "ms_marching_cubes": ms_mc, "ms_total": ms_query + ms_mc,
                         "sdf_grid_bytes": 4 * n},
-            "roofline": {"bound": "hbm", "kernel": "k_marching_cubes (unfused call)", "achieved": mc_bytes / (ms_mc / 1e3) / 1e9,
+            "roofline": {"bound": "hbm", "kernel": "k_mc_signs + k_mc_emit (unfused sand_marching_cubes call, host sync included)", "achieved": mc_bytes / (ms_mc / 1e3) / 1e9,
                          "peak": pk["hbm"], "unit": "GB/s", "frac": mc_bytes / (ms_mc / 1e3) / 1e9 / pk["hbm"],
                          "bytes_formula": "4 B sdf per grid vertex + 36 B per triangle", "traffic": None}}
     print(json.dumps(line), flush=True)

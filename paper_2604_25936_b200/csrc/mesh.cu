@@ -25,8 +25,8 @@ namespace sand {
 
 // device-global (not __constant__): every block copies them to shared memory with coalesced word loads
 __device__ __align__(16) uint8_t c_mc_ntri[256];
-__device__ __align__(16) uint8_t c_mc_tri[256][15];   // up to 5 triangles x 3 edge ids
-__device__ __align__(16) uint8_t c_mc_edge[12][2];    // (lower corner, upper corner)
+__device__ __align__(16) uint16_t c_mc_tri[256][5];   // up to 5 triangles: edge ids e0 | e1 << 4 | e2 << 8
+__device__ __align__(16) uint8_t c_mc_edge[16];       // per edge: lower corner | axis << 3 (upper corner = lower | 1 << axis)
 
 static void mc_build_tables(uint8_t ntri[256], uint8_t tri[256][15], uint8_t edge[12][2]) {
   int ne = 0;
@@ -101,9 +101,19 @@ cudaError_t mc_upload_tables() {
   if (dev < 64 && ((done >> dev) & 1)) return cudaSuccess;
   uint8_t ntri[256], tri[256][15] = {}, edge[12][2];
   mc_build_tables(ntri, tri, edge);
+  uint16_t tri16[256][5] = {};
+  for (int c = 0; c < 256; ++c)
+    for (int t = 0; t < ntri[c]; ++t)
+      tri16[c][t] = (uint16_t)(tri[c][3 * t] | (tri[c][3 * t + 1] << 4) | (tri[c][3 * t + 2] << 8));
+  uint8_t edge8[16] = {};
+  for (int k = 0; k < 12; ++k) {
+    int a = 0;
+    while ((edge[k][0] | (1 << a)) != edge[k][1]) ++a;   // mc_build_tables: upper = lower | 1 << axis
+    edge8[k] = (uint8_t)(edge[k][0] | (a << 3));
+  }
   e = cudaMemcpyToSymbol(c_mc_ntri, ntri, sizeof ntri);
-  if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_mc_tri, tri, sizeof tri);
-  if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_mc_edge, edge, sizeof edge);
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_mc_tri, tri16, sizeof tri16);
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_mc_edge, edge8, sizeof edge8);
   if (e == cudaSuccess && dev < 64) done |= 1ull << dev;
   return e;
 }
@@ -143,13 +153,17 @@ __global__ void k_grid_points(const float* __restrict__ axis, int R, int k0, int
 #define SAND_MC_QC 64    // 128 measured 6-9% slower (47 KB of shared memory per block, 7-step owner search)
 #endif
 constexpr int MC_UNROLL = SAND_MC_UNROLL;
+// Pass B's work queue: MC_NRANGE task ranges, each with its own counter on its own 128-byte line (a single
+// counter next to the triangle counter serialised ~200 K same-sector atomics: 340 us of pass B on the 512^3 grid)
+constexpr int MC_NRANGE = 64;
+constexpr int MC_CTR_STRIDE = 16;   // uint64 words between counters
 constexpr int MC_QC = SAND_MC_QC;   // queue capacity per warp (cubes), a multiple of 32
 constexpr int MC_EPL = MC_QC / 32;  // queue entries per lane at flush time
 
 __global__ void __launch_bounds__(256) k_mc_signs(const float* __restrict__ sdf, int R, long long nrows, int G,
                                                   uint32_t* __restrict__ signs, unsigned long long* __restrict__ taskctr) {
   const int lane = threadIdx.x & 31;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *taskctr = 0ull;   // pass B's work queue (same stream, runs after this)
+  if (blockIdx.x == 0 && threadIdx.x < MC_NRANGE) taskctr[MC_CTR_STRIDE * threadIdx.x] = 0ull;   // pass B's work queue (same stream, runs after this)
   const bool al = (R & 3) == 0 && (reinterpret_cast<uintptr_t>(sdf) & 15) == 0;
   const long long ngr = nrows * G;
   const long long wstride = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -186,13 +200,13 @@ __global__ void __launch_bounds__(256, 4) k_mc_emit(const float* __restrict__ sd
   __shared__ float s_q[8][8][MC_QC];
   __shared__ unsigned s_m0[8][MC_QC], s_m1[8][MC_QC];
   __shared__ unsigned short s_off[8][MC_QC];   // <= 5 MC_QC triangles
-  __shared__ __align__(16) uint8_t s_tri[256][15];   // tables in shared memory: per-thread (divergent) indices
+  __shared__ __align__(16) uint16_t s_tri[256][5];   // tables in shared memory: per-thread (divergent) indices
   __shared__ __align__(16) uint8_t s_ntri[256];
-  __shared__ __align__(16) uint8_t s_edge[12][2];
-  for (int t = threadIdx.x; t < 256 * 15 / 4; t += blockDim.x)
+  __shared__ __align__(16) uint8_t s_edge[16];
+  for (int t = threadIdx.x; t < 256 * 5 / 2; t += blockDim.x)
     reinterpret_cast<uint32_t*>(&s_tri[0][0])[t] = reinterpret_cast<const uint32_t*>(&c_mc_tri[0][0])[t];
   if (threadIdx.x < 64) reinterpret_cast<uint32_t*>(s_ntri)[threadIdx.x] = reinterpret_cast<const uint32_t*>(c_mc_ntri)[threadIdx.x];
-  if (threadIdx.x < 6) reinterpret_cast<uint32_t*>(&s_edge[0][0])[threadIdx.x] = reinterpret_cast<const uint32_t*>(&c_mc_edge[0][0])[threadIdx.x];
+  if (threadIdx.x < 4) reinterpret_cast<uint32_t*>(s_edge)[threadIdx.x] = reinterpret_cast<const uint32_t*>(c_mc_edge)[threadIdx.x];
   __syncthreads();
   int qn = 0;   // queued cubes (warp-uniform)
   auto flush = [&]() {
@@ -250,18 +264,27 @@ __global__ void __launch_bounds__(256, 4) k_mc_emit(const float* __restrict__ sd
       const int t = idx - (s_off[warp][L] - s_ntri[cL]);
       const int iL = (int)(m0 & 0xFFFFu), jL = (int)(m0 >> 16), kL = (int)(m1 & 0xFFFFFFu);
       float* out = tris + 9 * ((long long)wbase + idx);
+      const unsigned pk = s_tri[cL][t];
 #pragma unroll
       for (int m = 0; m < 3; ++m) {
-        const int e = s_tri[cL][3 * t + m];
-        const int v0 = s_edge[e][0], v1 = s_edge[e][1];
+        // vertex on edge e: from its lower corner v0 along axis ax; t = s0 / (s0 - s1) (R24).  The other two
+        // coordinates are the lower corner's own (p0 + t * 0), so only the edge axis is interpolated.
+        const unsigned eb = s_edge[(pk >> (4 * m)) & 15u];
+        const int v0 = (int)(eb & 7u), ax = (int)(eb >> 3), v1 = v0 | (1 << ax);
         // corner v = x + 2 y + 4 z is queue row 4 x + (v >> 1)
         const float a0 = s_q[warp][4 * (v0 & 1) + (v0 >> 1)][L], a1 = s_q[warp][4 * (v1 & 1) + (v1 >> 1)][L];
-        const float tt = a0 / (a0 - a1);
-        const float p0x = axis[iL + (v0 & 1)], p0y = axis[jL + ((v0 >> 1) & 1)], p0z = axis[kL + (v0 >> 2)];
-        const float p1x = axis[iL + (v1 & 1)], p1y = axis[jL + ((v1 >> 1) & 1)], p1z = axis[kL + (v1 >> 2)];
-        out[3 * m] = p0x + tt * (p1x - p0x);
-        out[3 * m + 1] = p0y + tt * (p1y - p0y);
-        out[3 * m + 2] = p0z + tt * (p1z - p0z);
+        const float tt = __fdividef(a0, a0 - a1);
+        const int i0 = iL + (v0 & 1), j0 = jL + ((v0 >> 1) & 1), k0 = kL + (v0 >> 2);
+        float px = axis[i0], py = axis[j0], pz = axis[k0];
+        const float pe0 = ax == 0 ? px : ax == 1 ? py : pz;
+        const float pe1 = axis[(ax == 0 ? i0 : ax == 1 ? j0 : k0) + 1];
+        const float pe = pe0 + tt * (pe1 - pe0);
+        if (ax == 0) px = pe;
+        else if (ax == 1) py = pe;
+        else pz = pe;
+        out[3 * m] = px;
+        out[3 * m + 1] = py;
+        out[3 * m + 2] = pz;
       }
     }
     __syncwarp();
@@ -271,12 +294,26 @@ __global__ void __launch_bounds__(256, 4) k_mc_emit(const float* __restrict__ sd
   // lane tasks are handed out by a global counter (surface-dense tasks run up to 16 flushes, empty ones none)
   const long long ntask = 4ll * G * R1 * (kc1 - kc0);
   const long long nwt = (ntask + 31) >> 5;
+  // range r holds the warp tasks t = r (mod MC_NRANGE), so all ranges carry the same mix of dense and empty tasks
+  // and run dry together; lane 0 draws tickets from its warp's home range and, once that is dry, from the next
+  // two (a longer walk would only add dependent atomics to the kernel's tail)
+  int rg = (int)(((long long)blockIdx.x * 8 + warp) % MC_NRANGE), dry = 0;
+  auto issue = [&]() { return (long long)atomicAdd(taskctr + MC_CTR_STRIDE * rg, 1ull); };
+  auto resolve = [&](long long raw) {   // ticket of range rg -> warp task, or -1 when the warp is done
+    while (true) {
+      const long long t = raw * MC_NRANGE + rg;
+      if (t < nwt) return t;
+      if (++dry >= 3) return -1ll;
+      rg = rg + 1 == MC_NRANGE ? 0 : rg + 1;
+      raw = issue();
+    }
+  };
   long long wt = 0;
-  if (lane == 0) wt = (long long)atomicAdd(taskctr, 1ull);
+  if (lane == 0) wt = resolve(issue());
   wt = __shfl_sync(0xffffffffu, wt, 0);
-  while (wt < nwt) {
+  while (wt >= 0) {
     long long nxt = 0;
-    if (lane == 0) nxt = (long long)atomicAdd(taskctr, 1ull);   // next task, fetched under this one
+    if (lane == 0) nxt = issue();   // next ticket, fetched under this task
     const long long t = wt * 32 + lane;
     const bool valid = t < ntask;
     const int q = (int)(t & 3);
@@ -335,6 +372,7 @@ __global__ void __launch_bounds__(256, 4) k_mc_emit(const float* __restrict__ sd
       qn += pushed;
       if (__any_sync(0xffffffffu, m != 0)) flush();   // something did not fit
     }
+    if (lane == 0) nxt = resolve(nxt);
     wt = __shfl_sync(0xffffffffu, nxt, 0);
   }
   flush();
@@ -350,12 +388,13 @@ cudaError_t launch_grid_points(const float* axis, int R, int k0, int np, float* 
   return cudaGetLastError();
 }
 
+size_t mc_counter_words() { return (size_t)MC_CTR_STRIDE * (1 + MC_NRANGE); }   // uint64: triangle count + task counters
 size_t mc_sign_words(int R, int planes) { return (size_t)4 * ((R + 127) / 128) * (size_t)R * (size_t)planes; }
 
 // signs: scratch of mc_sign_words(R, kc1 - kc0 + 1) uint32 (16-byte aligned)
 cudaError_t launch_marching_cubes(const float* sdf, int R, int kc0, int kc1, int kp0, const float* axis, float* tris,
                                   long long cap, unsigned long long* counter, uint32_t* signs, int num_sms,
-                                  cudaStream_t st) {   // counter: 2 words (triangle count, pass B's task counter)
+                                  cudaStream_t st) {   // counter: mc_counter_words() uint64 (triangle count, task counters)
   if (R < 2 || kc1 <= kc0) return cudaSuccess;
   if (R > 65535) return cudaErrorInvalidValue;   // queue entries pack x and j into 16 bits each
   const int G = (R + 127) / 128;
@@ -363,12 +402,12 @@ cudaError_t launch_marching_cubes(const float* sdf, int R, int kc0, int kc1, int
   const long long row0 = (long long)(kc0 - kp0) * R, nrows = (long long)(kc1 - kc0 + 1) * R;
   const long long ngr = nrows * G;
   const long long ba = std::min<long long>((ngr + 7) / 8, (long long)num_sms * 16);
-  k_mc_signs<<<(unsigned)ba, 256, 0, st>>>(sdf + row0 * R, R, nrows, G, signs + 4 * row0 * G, counter + 1);
+  k_mc_signs<<<(unsigned)ba, 256, 0, st>>>(sdf + row0 * R, R, nrows, G, signs + 4 * row0 * G, counter + MC_CTR_STRIDE);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const long long nwt = (4ll * G * (R - 1) * (kc1 - kc0) + 31) / 32;
   const long long bb = std::min<long long>((nwt + 7) / 8, (long long)num_sms * 4);
-  k_mc_emit<<<(unsigned)bb, 256, 0, st>>>(sdf, signs, R, kc0, kc1, kp0, axis, tris, cap, counter, counter + 1);
+  k_mc_emit<<<(unsigned)bb, 256, 0, st>>>(sdf, signs, R, kc0, kc1, kp0, axis, tris, cap, counter, counter + MC_CTR_STRIDE);
   return cudaGetLastError();
 }
 

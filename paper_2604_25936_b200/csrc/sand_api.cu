@@ -793,7 +793,7 @@ static int mesh_prepare(sand_ctx* ctx, int R, int planes) {
     ctx->axis_R = R;
     CU(launch_grid_axis(R, ctx->d_axis, ctx->stream));
   }
-  if (!ctx->d_tricount) CU(cudaMalloc(&ctx->d_tricount, 2 * sizeof(unsigned long long)));   // + the MC task counter
+  if (!ctx->d_tricount) CU(cudaMalloc(&ctx->d_tricount, mc_counter_words() * sizeof(unsigned long long)));
   CU(cudaMemsetAsync(ctx->d_tricount, 0, sizeof(unsigned long long), ctx->stream));
   return SAND_OK;
 }

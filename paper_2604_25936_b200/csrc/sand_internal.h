@@ -111,6 +111,7 @@ bool depthpop_supported(int H);
 cudaError_t mc_upload_tables();
 cudaError_t launch_grid_axis(int R, float* axis, cudaStream_t st);
 cudaError_t launch_grid_points(const float* axis, int R, int k0, int np, float* pts, int num_sms, cudaStream_t st);
+size_t mc_counter_words();                 // uint64 words of the counter block (triangle count + pass B's task counters)
 size_t mc_sign_words(int R, int planes);   // scratch (uint32 words) for the vertex signs of `planes` grid planes
 cudaError_t launch_marching_cubes(const float* sdf, int R, int kc0, int kc1, int kp0, const float* axis, float* tris,
                                   long long cap, unsigned long long* counter, uint32_t* signs, int num_sms,
