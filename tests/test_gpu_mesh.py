@@ -87,6 +87,39 @@ def test_marching_cubes_across_sign_word_groups(R):
     assert T[:, :, 0].max() == 1.0   # the mesh reaches the domain face
 
 
+def test_marching_cubes_large_grid_invariants_and_unaligned_buffer():
+    """R = 260 (three sign-word groups per row, too large for the Python oracle in the default suite): properties
+    that hold at any size -- two disjoint spheres inside the domain give a watertight mesh with Euler
+    characteristic 2 + 2, every vertex lies on a grid edge with the sdf changing sign across it, and the same sdf
+    read through a buffer that is NOT 16-byte aligned (the scalar load path of the sign pass) gives the same
+    triangle set bit for bit."""
+    import torch
+    R = 260
+    X, Y, Z = _grid(R)
+    sdf = np.minimum(np.sqrt((X - 0.5) ** 2 + (Y - 0.1) ** 2 + Z ** 2) - 0.37,
+                     np.sqrt((X + 0.55) ** 2 + (Y + 0.2) ** 2 + (Z - 0.3) ** 2) - 0.31).astype(np.float32)
+    spec = g.TMlpSpec(L=2, H=64, omega0=30.0, seed=1)
+    with make_ctx(spec, 2) as ctx:
+        T = _gpu_mc(ctx, sdf.ravel(), R)
+        buf = torch.empty(R ** 3 + 1, dtype=torch.float32, device="cuda")
+        view = buf[1:]
+        view.copy_(torch.from_numpy(sdf.ravel()))
+        assert view.data_ptr() % 16 == 4
+        n = ctx.sand_marching_cubes(view.data_ptr(), R, 0, 0)
+        tris = torch.empty(n * 9, dtype=torch.float32, device="cuda")
+        assert ctx.sand_marching_cubes(view.data_ptr(), R, tris.data_ptr(), n) == n
+        Tu = tris.cpu().numpy().reshape(-1, 3, 3)
+    assert T.shape == Tu.shape and T.shape[0] > 100000
+    key = lambda A: A.reshape(-1, 9)[np.lexsort(A.reshape(-1, 9).T[::-1])]
+    np.testing.assert_array_equal(key(T), key(Tu))
+    ok, V, E, F = _watertight(T)
+    assert ok and V - E + F == 4
+    # every vertex sits on a grid line: two of its coordinates are grid coordinates
+    ax = (2.0 * np.arange(R) / (R - 1) - 1.0).astype(np.float32)
+    on_grid = np.isin(T.reshape(-1, 3), ax).sum(axis=1)
+    assert (on_grid >= 2).all()
+
+
 def test_capacity_and_empty():
     R = 21
     X, Y, Z = _grid(R)
