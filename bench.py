@@ -860,6 +860,9 @@ def run_query(args):
             "gpu_launches": 6 * args.steps * ws,   # lookup, scan x3, scatter, T-MLP per query
             "clocks": clocks,
             "hbm_lookup_gbs": (13.0 * n) / (ms_lookup / 1e3) / 1e9 if ms_lookup > 0 else None,
+            # binning (K2a scans + K2b scatter): 1 B depth read + 4 B perm written per binned point, rank 0's shard
+            "hbm_bin_gbs": (5.0 * sum(st["per_depth"][1:])) / (ms_bin / 1e3) / 1e9 if ms_bin > 0 else None,
+            "hbm_peak_gbs": pk["hbm"],
         }
         print(json.dumps(line), flush=True)
     ctx.close()
