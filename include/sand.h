@@ -238,7 +238,12 @@ int sand_query_dynamic(sand_ctx* ctx, const float* d_points, int64_t n, float r,
  * device, caller-owned, room for cap triangles).  *n_tris (host) receives the number of triangles of
  * the surface; only the first min(n, cap) are written, so a call with cap = 0 sizes the buffer.  The
  * order of triangles is not deterministic (the set is).  Synchronous (returns after the count is
- * read back).  Errors: SAND_ERR_ARG, SAND_ERR_STATE, SAND_ERR_CUDA, SAND_ERR_OOM. */
+ * read back).  2 <= R <= 65535.  The context keeps R / 8 bytes per grid vertex row of scratch (vertex sign
+ * words of the planes one call covers).  A vertex on a crossing edge is the edge's lower corner moved by
+ * t = s0 / (s0 - s1) along the edge's axis (t by the fast divide: within 2 ulp; the two cubes sharing an
+ * edge evaluate the same expression, so shared vertices are bit-identical).
+ * Errors: SAND_ERR_ARG (R < 2 or R > 65535, cap < 0, NULL argument), SAND_ERR_STATE, SAND_ERR_CUDA,
+ * SAND_ERR_OOM. */
 
 /* Marching cubes on a caller-provided sdf grid (R^3 float32, device). */
 int sand_marching_cubes(sand_ctx* ctx, const float* d_sdf, int R, float* d_tris, int64_t cap, int64_t* n_tris);

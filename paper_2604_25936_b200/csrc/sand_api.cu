@@ -809,8 +809,8 @@ static int mesh_finish(sand_ctx* ctx, int64_t* n_tris) {
 extern "C" int sand_marching_cubes(sand_ctx* ctx, const float* d_sdf, int R, float* d_tris, int64_t cap,
                                    int64_t* n_tris) {
   if (!ctx) return fail(ctx, SAND_ERR_ARG, "NULL ctx");
-  if (R < 2 || cap < 0 || !n_tris || !d_sdf || (cap > 0 && !d_tris))
-    return fail(ctx, SAND_ERR_ARG, "sand_marching_cubes: R < 2, cap < 0 or NULL argument");
+  if (R < 2 || R > 65535 || cap < 0 || !n_tris || !d_sdf || (cap > 0 && !d_tris))
+    return fail(ctx, SAND_ERR_ARG, "sand_marching_cubes: R outside [2, 65535], cap < 0 or NULL argument");
   CU(cudaSetDevice(ctx->cfg.device));
   int rc = mesh_prepare(ctx, R, R);
   if (rc) return rc;
@@ -822,8 +822,8 @@ extern "C" int sand_marching_cubes(sand_ctx* ctx, const float* d_sdf, int R, flo
 extern "C" int sand_mesh_grid(sand_ctx* ctx, int R, int slab, float* d_tris, int64_t cap, int64_t* n_tris) {
   NvtxRange nvtx_("sand_mesh_grid");
   if (!ctx) return fail(ctx, SAND_ERR_ARG, "NULL ctx");
-  if (R < 2 || slab < 0 || cap < 0 || !n_tris || (cap > 0 && !d_tris))
-    return fail(ctx, SAND_ERR_ARG, "sand_mesh_grid: R < 2, slab < 0, cap < 0 or NULL argument");
+  if (R < 2 || R > 65535 || slab < 0 || cap < 0 || !n_tris || (cap > 0 && !d_tris))
+    return fail(ctx, SAND_ERR_ARG, "sand_mesh_grid: R outside [2, 65535], slab < 0, cap < 0 or NULL argument");
   if (!ctx->have_w || !ctx->have_dm) return fail(ctx, SAND_ERR_STATE, "load weights and depth map first");
   CU(cudaSetDevice(ctx->cfg.device));
   if (slab == 0) slab = 64;
