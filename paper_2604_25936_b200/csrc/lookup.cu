@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(kLookupThreads) k_lookup(const float* __restri
   const float maxc = (float)((1u << lp.level) - 1u);
   const long long base = (long long)blockIdx.x * kLookupChunk;
   const int lane = threadIdx.x & 31;
-#pragma unroll 1
+#pragma unroll (KIND == 0 ? 4 : 1)   // dense map without cached sdf: 4 chunks of loads in flight (0.354 -> 0.333 ms on C2); the far-field and descent variants measured slower unrolled
   for (int it = 0; it < kLookupChunk / (4 * kLookupThreads); ++it) {
     const long long p0 = base + (long long)it * 4 * kLookupThreads + 4 * threadIdx.x;
     const long long rem = n - p0;
